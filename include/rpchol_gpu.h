@@ -1,0 +1,162 @@
+/*
+ * rpchol_gpu.h — C-ABI of the B200-native accelerated RPCholesky library
+ * (librpchol_b200.so, built from paper_2410_03969_b200/csrc).
+ *
+ * Drop-in boundary for the reference hot path
+ *   CholeskyResult rpchol::accelerated_rpcholesky(const PsdOracle&, const RunConfig&)
+ *     /root/reference/proj/include/rpchol/rpcholesky.hpp:338-401
+ * specialised to the implicit kernel oracle
+ *   KernelOracle(DataMatrix X, KernelSpec{kind, sigma}, DistanceMode)
+ *     /root/reference/proj/include/rpchol/oracle.hpp:243-258
+ * Plain pointers and sizes only; no torch, no Eigen in any signature.  Every
+ * entry point returns an rpc_status; rpc_last_error() gives the message, which
+ * reuses the reference's exception strings where one exists.
+ *
+ * There is no CPU fallback: without a usable sm_100a device every compute entry
+ * point fails with RPC_ECUDA.
+ */
+#ifndef RPCHOL_GPU_H
+#define RPCHOL_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct rpc_ctx rpc_ctx;
+typedef struct rpc_result rpc_result;
+
+/* Status codes <-> reference exception classes (rpchol_cli.cpp:26-28). */
+typedef enum {
+  RPC_OK = 0,
+  RPC_EINVAL = 1,   /* std::invalid_argument */
+  RPC_ERANGE = 2,   /* std::out_of_range */
+  RPC_ENUMERIC = 3, /* std::runtime_error (numerical) */
+  RPC_ECUDA = 4,    /* CUDA failure / no device */
+  RPC_ENCCL = 5,    /* NCCL failure */
+  RPC_ENOMEM = 6    /* device or host allocation failed */
+} rpc_status;
+
+/* KernelKind (kernels.hpp:20) — the kinds the kernel oracle path supports. */
+typedef enum { RPC_KERNEL_GAUSSIAN = 0, RPC_KERNEL_L1LAPLACE = 1 } rpc_kernel_kind;
+/* DistanceMode (oracle.hpp:37); DEFAULT = default_distance_mode (oracle.hpp:39-42). */
+typedef enum { RPC_DIST_DIRECT = 0, RPC_DIST_GRAM = 1, RPC_DIST_DEFAULT = -1 } rpc_distance_mode;
+/* RunConfig::Mode (rpcholesky.hpp:37). */
+typedef enum { RPC_FIXED_ROUNDS = 0, RPC_UNTIL_RANK = 1 } rpc_run_mode;
+typedef enum { RPC_COL_MAJOR = 0, RPC_ROW_MAJOR = 1 } rpc_layout;
+
+/* KernelSpec (kernels.hpp:41-51) + the oracle's DistanceMode. */
+typedef struct {
+  int kind;          /* rpc_kernel_kind */
+  double sigma;      /* bandwidth, > 0 and finite */
+  int distance_mode; /* rpc_distance_mode */
+} rpc_kernel_spec;
+
+/* RunConfig (rpcholesky.hpp:36-67) plus B200 execution flags. */
+enum {
+  RPC_FLAG_REPLAY_SCAN = 1u /* sequential cumulative_sums + upper_bound exactly as
+                               rng.hpp:67-96 (single shard only; slower) */
+};
+typedef struct {
+  int64_t block_size;  /* b >= 1 (this build: b <= 256) */
+  int mode;            /* rpc_run_mode */
+  int64_t rounds;      /* FixedRounds: t >= 1 */
+  int64_t target_rank; /* UntilRank: k >= 1 */
+  uint64_t seed;       /* SplitMix64 seed */
+  double stop_tol;     /* 0 disables the early exit */
+  uint32_t flags;
+} rpc_run_config;
+
+/* ---- context ------------------------------------------------------------ */
+/* One GPU, one shard. */
+int rpc_create(int device, rpc_ctx** out);
+/* One GPU holding n_shards row shards with device-local collectives; produces
+ * the same pivots and factor as an n_shards-GPU run (p-invariance testing). */
+int rpc_create_virtual(int device, int n_shards, rpc_ctx** out);
+/* One process per GPU: rank `rank` of `nranks`, NCCL communicator built from a
+ * 128-byte ncclUniqueId produced by rpc_nccl_unique_id on one rank and shared
+ * by the caller (e.g. over torch.distributed / MPI / files). */
+int rpc_nccl_unique_id(void* id128);
+int rpc_create_nccl(int device, const void* id128, int nranks, int rank, rpc_ctx** out);
+void rpc_destroy(rpc_ctx* ctx);
+/* Message of the last failing call on this thread (or on ctx when non-null). */
+const char* rpc_last_error(const rpc_ctx* ctx);
+/* Global shard layout of a run on N points: rows [row0, row0+nrows) are owned by
+ * this process's shard `local` (0 unless virtual). */
+int rpc_shard_rows(const rpc_ctx* ctx, int64_t n, int local, int64_t* row0, int64_t* nrows);
+
+/* ---- the hot path: accelerated_rpcholesky over a kernel oracle ----------- */
+/* X: host N x d points (layout + leading dimension ldx).  Every rank passes the
+ * same full X; each uploads only its own rows. */
+int rpc_accelerated_rpcholesky(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                               int layout, rpc_kernel_spec kernel, rpc_run_config cfg,
+                               rpc_result** out);
+/* Same with the points already resident on the device: x_dev holds this
+ * process's shard rows [row0, row0+nrows) (see rpc_shard_rows) in `layout`
+ * with leading dimension ldx.  No host<->device traffic besides per-round
+ * status words. */
+int rpc_accelerated_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, int64_t d,
+                                      int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                      rpc_run_config cfg, rpc_result** out);
+
+/* ---- result (CholeskyResult, rpcholesky.hpp:106-110) --------------------- */
+int64_t rpc_result_n(const rpc_result* r);
+int64_t rpc_result_rank(const rpc_result* r); /* factor columns = |pivots| */
+int rpc_result_pivots(const rpc_result* r, int64_t* out); /* rank entries */
+/* Factor rows owned by this process: writes rows [row0, row0+nrows) of the
+ * N x rank factor into out (global row indexing; ld = leading dimension). */
+int rpc_result_factor_copy(const rpc_result* r, double* out, int64_t ld, int layout);
+/* chol_factor: rank x rank lower triangle, column-major (rpcholesky.hpp:140-145). */
+int rpc_result_chol_copy(const rpc_result* r, double* out);
+/* residual_diag rows owned by this process (global indexing into out[N]). */
+int rpc_result_residual_diag_copy(const rpc_result* r, double* out);
+int64_t rpc_result_num_rounds(const rpc_result* r);
+int64_t rpc_result_block_size(const rpc_result* r);
+/* PivotTrace rounds (rpcholesky.hpp:78-104): proposed has block_size entries;
+ * accepted receives up to block_size entries, *n_accepted its count. */
+int rpc_result_round(const rpc_result* r, int64_t round, int64_t* proposed, int64_t* accepted,
+                     int64_t* n_accepted);
+int rpc_result_rank_exhausted(const rpc_result* r);
+int64_t rpc_result_surplus(const rpc_result* r);
+double rpc_result_captured_sq(const rpc_result* r);
+/* relative_trace_error (rpcholesky.hpp:577-583), from the device-resident factor. */
+double rpc_result_relative_trace_error(const rpc_result* r);
+/* Device-resident factor of this process's (first) shard: row-major, ld = *ldf. */
+const double* rpc_result_factor_device(const rpc_result* r, int64_t* ldf, int64_t* row0,
+                                       int64_t* nrows);
+
+typedef struct {
+  double factorize_ms;     /* device time, first kernel to factor complete (CUDA events) */
+  double upload_ms;        /* X host->device + packing */
+  double update_ms;        /* sum over rounds of the fused K5+K6 update kernel(s) */
+  double update_flops;     /* algorithmic FP64 flops of those launches */
+  double update_bytes;     /* algorithmic HBM bytes of those launches */
+  int64_t update_launches; /* update-kernel launches */
+  int64_t kernel_launches; /* all kernels launched by the factorization */
+} rpc_timing;
+int rpc_result_timing(const rpc_result* r, rpc_timing* t);
+void rpc_result_free(rpc_result* r);
+
+/* ---- component entry points (reference public functions) ---------------- */
+/* KernelOracle::columns (oracle.hpp:188-191) through the standalone K5 kernel:
+ * out (N x m, column-major, ld) = A(:, cols).  *device_ms = kernel time. */
+int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                       int layout, rpc_kernel_spec kernel, const int64_t* cols, int64_t m,
+                       double* out, int64_t ld_out, double* device_ms);
+/* b draws of sample_discrete (rng.hpp:80-96) against cumulative_sums(u), using
+ * SplitMix64(seed) draws [draw0, draw0+b).  replay != 0: sequential scan. */
+int rpc_sample_discrete(rpc_ctx* ctx, const double* u, int64_t n, int64_t b, uint64_t seed,
+                        uint64_t draw0, int replay, int64_t* out);
+/* rejection_sample_submatrix (rpcholesky.hpp:167-201): h is b x b column-major;
+ * accept draws are SplitMix64(seed) draws [draw0, draw0+b).  chol: m x m
+ * column-major (capacity b*b). */
+int rpc_rejection_sweep(rpc_ctx* ctx, const double* h, int64_t b, const int64_t* proposals,
+                        uint64_t seed, uint64_t draw0, int64_t* accepted, int64_t* positions,
+                        int64_t* m, double* chol);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RPCHOL_GPU_H */

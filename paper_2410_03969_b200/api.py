@@ -1,0 +1,290 @@
+"""Python mirror of the reference's hot-path API over the B200 C-ABI.
+
+Names and argument meaning follow /root/reference/proj/include/rpchol:
+  KernelSpec (kernels.hpp:41-51), DistanceMode (oracle.hpp:37),
+  KernelOracle (oracle.hpp:243-258), RunConfig (rpcholesky.hpp:36-67),
+  accelerated_rpcholesky (rpcholesky.hpp:338-401) -> CholeskyResult (106-110),
+  relative_trace_error (577-583).
+Errors map to the reference's exception classes: ValueError for
+std::invalid_argument, IndexError for std::out_of_range, RuntimeError for
+std::runtime_error.  Every call runs on the GPU through librpchol_b200.so;
+there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib as L
+
+KERNEL_KINDS = {"gaussian": L.RPC_KERNEL_GAUSSIAN, "l1laplace": L.RPC_KERNEL_L1LAPLACE,
+                "laplace": L.RPC_KERNEL_L1LAPLACE}
+DISTANCE_MODES = {None: L.RPC_DIST_DEFAULT, "direct": L.RPC_DIST_DIRECT, "gram": L.RPC_DIST_GRAM}
+
+
+@dataclass
+class KernelSpec:
+    kind: str = "gaussian"
+    bandwidth: float = 1.0
+
+
+@dataclass
+class RunConfig:
+    block_size: int = 1
+    mode: str = "until_rank"
+    rounds: int = 0
+    target_rank: int = 0
+    seed: int = 0
+    stop_tol: float = 0.0
+    replay_scan: bool = False
+
+    @staticmethod
+    def fixed_rounds(t: int, b: int, seed: int) -> "RunConfig":
+        if t < 1 or b < 1:
+            raise ValueError("RunConfig: t, b must be >= 1")
+        return RunConfig(block_size=b, mode="fixed_rounds", rounds=t, seed=seed)
+
+    @staticmethod
+    def until_rank(k: int, b: int, seed: int) -> "RunConfig":
+        if k < 1 or b < 1:
+            raise ValueError("RunConfig: k, b must be >= 1")
+        return RunConfig(block_size=b, mode="until_rank", target_rank=k, seed=seed)
+
+    def to_c(self) -> L.RunConfigC:
+        mode = L.RPC_FIXED_ROUNDS if self.mode == "fixed_rounds" else L.RPC_UNTIL_RANK
+        return L.RunConfigC(self.block_size, mode, self.rounds, self.target_rank,
+                            self.seed & 0xFFFFFFFFFFFFFFFF, self.stop_tol,
+                            L.RPC_FLAG_REPLAY_SCAN if self.replay_scan else 0)
+
+
+class Context:
+    """One GPU (optionally holding `virtual_shards` row shards), or one rank of
+    an NCCL job (`nccl_id`, `nranks`, `rank`)."""
+
+    def __init__(self, device: int = 0, virtual_shards: int = 1, nccl_id: bytes | None = None,
+                 nranks: int = 1, rank: int = 0):
+        lib = L.load()
+        h = C.c_void_p()
+        if nccl_id is not None:
+            L.check(lib.rpc_create_nccl(device, nccl_id, nranks, rank, C.byref(h)))
+        elif virtual_shards > 1:
+            L.check(lib.rpc_create_virtual(device, virtual_shards, C.byref(h)))
+        else:
+            L.check(lib.rpc_create(device, C.byref(h)))
+        self.handle = h
+        self.virtual_shards = virtual_shards
+
+    def close(self):
+        if self.handle:
+            L.load().rpc_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def shard_rows(self, n: int, local: int = 0):
+        r0, nr = C.c_int64(), C.c_int64()
+        L.check(L.load().rpc_shard_rows(self.handle, n, local, C.byref(r0), C.byref(nr)))
+        return r0.value, nr.value
+
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    L.check(L.load().rpc_nccl_unique_id(buf))
+    return buf.raw
+
+
+_default_ctx: Context | None = None
+
+
+def default_context() -> Context:
+    global _default_ctx
+    if _default_ctx is None:
+        _default_ctx = Context(0)
+    return _default_ctx
+
+
+class KernelOracle:
+    """Implicit kernel matrix over points X (N x d), as oracle.hpp:243-327."""
+
+    def __init__(self, points: np.ndarray, spec: KernelSpec, distance_mode: str | None = None):
+        x = np.asarray(points, dtype=np.float64)
+        if x.ndim != 2:
+            raise ValueError("DataMatrix: need at least one point and one dimension")
+        self.points = x
+        self.spec = spec
+        self.distance_mode = distance_mode
+
+    def dimension(self) -> int:
+        return self.points.shape[0]
+
+    def _c_spec(self) -> L.KernelSpecC:
+        kind = KERNEL_KINDS.get(self.spec.kind)
+        if kind is None:
+            raise ValueError("unknown kernel: " + str(self.spec.kind))
+        return L.KernelSpecC(kind, float(self.spec.bandwidth), DISTANCE_MODES[self.distance_mode])
+
+    def _host_layout(self):
+        x = self.points
+        if x.flags.f_contiguous and not x.flags.c_contiguous:
+            return x, L.RPC_COL_MAJOR, x.shape[0]
+        x = np.ascontiguousarray(x)
+        return x, L.RPC_ROW_MAJOR, x.shape[1]
+
+    def columns(self, cols, ctx: Context | None = None, return_ms: bool = False):
+        """A(:, cols) via the standalone K5 kernel (PsdOracle::columns)."""
+        ctx = ctx or default_context()
+        x, lay, ld = self._host_layout()
+        c = np.ascontiguousarray(cols, dtype=np.int64)
+        n = x.shape[0]
+        out = np.zeros((n, c.size), dtype=np.float64, order="F")
+        ms = C.c_double()
+        L.check(L.load().rpc_kernel_columns(ctx.handle, x.ctypes.data, n, x.shape[1], ld, lay,
+                                            self._c_spec(), c.ctypes.data, c.size,
+                                            out.ctypes.data, n, C.byref(ms)), ctx.handle)
+        return (out, ms.value) if return_ms else out
+
+
+@dataclass
+class CholeskyResult:
+    """CholeskyResult (rpcholesky.hpp:106-110) with the factor kept on the device
+    until `factor` is first read."""
+    _handle: C.c_void_p
+    _ctx: Context
+    n: int
+    pivots: np.ndarray
+    chol_factor: np.ndarray
+    proposed: list
+    accepted: list
+    rank_exhausted: bool
+    surplus: int
+    captured_sq: float
+    relative_trace_error: float
+    timing: dict = field(default_factory=dict)
+    _factor: np.ndarray | None = None
+
+    @property
+    def rank(self) -> int:
+        return int(self.pivots.size)
+
+    def factor_into(self, out: np.ndarray, layout: str = "F") -> np.ndarray:
+        lay = L.RPC_COL_MAJOR if layout == "F" else L.RPC_ROW_MAJOR
+        ld = out.shape[0] if layout == "F" else out.shape[1]
+        L.check(L.load().rpc_result_factor_copy(self._handle, out.ctypes.data, ld, lay),
+                self._ctx.handle)
+        return out
+
+    @property
+    def factor(self) -> np.ndarray:
+        if self._factor is None:
+            self._factor = self.factor_into(np.zeros((self.n, self.rank), order="F"))
+        return self._factor
+
+    @property
+    def residual_diag(self) -> np.ndarray:
+        out = np.zeros(self.n)
+        L.check(L.load().rpc_result_residual_diag_copy(self._handle, out.ctypes.data),
+                self._ctx.handle)
+        return out
+
+    def free(self):
+        if self._handle:
+            L.load().rpc_result_free(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def _wrap_result(h: C.c_void_p, ctx: Context) -> CholeskyResult:
+    lib = L.load()
+    n = lib.rpc_result_n(h)
+    k = lib.rpc_result_rank(h)
+    piv = np.zeros(k, np.int64)
+    lib.rpc_result_pivots(h, piv.ctypes.data)
+    chol = np.zeros((k, k), order="F")
+    lib.rpc_result_chol_copy(h, chol.ctypes.data)
+    b = lib.rpc_result_block_size(h)
+    proposed, accepted = [], []
+    for r in range(lib.rpc_result_num_rounds(h)):
+        pr = np.zeros(b, np.int64)
+        ac = np.zeros(b, np.int64)
+        na = C.c_int64()
+        L.check(lib.rpc_result_round(h, r, pr.ctypes.data, ac.ctypes.data, C.byref(na)))
+        proposed.append(pr)
+        accepted.append(ac[: na.value].copy())
+    t = L.TimingC()
+    lib.rpc_result_timing(h, C.byref(t))
+    timing = {f: getattr(t, f) for f, _ in L.TimingC._fields_}
+    return CholeskyResult(h, ctx, n, piv, chol, proposed, accepted,
+                          bool(lib.rpc_result_rank_exhausted(h)), int(lib.rpc_result_surplus(h)),
+                          float(lib.rpc_result_captured_sq(h)),
+                          float(lib.rpc_result_relative_trace_error(h)), timing)
+
+
+def accelerated_rpcholesky(oracle: KernelOracle, cfg: RunConfig,
+                           ctx: Context | None = None) -> CholeskyResult:
+    """rpchol::accelerated_rpcholesky (rpcholesky.hpp:338-401) on the GPU."""
+    if not isinstance(oracle, KernelOracle):
+        raise ValueError("accelerated_rpcholesky (B200): only KernelOracle inputs are supported")
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    h = C.c_void_p()
+    L.check(L.load().rpc_accelerated_rpcholesky(ctx.handle, x.ctypes.data, x.shape[0],
+                                                x.shape[1], ld, lay, oracle._c_spec(),
+                                                cfg.to_c(), C.byref(h)), ctx.handle)
+    return _wrap_result(h, ctx)
+
+
+def accelerated_rpcholesky_device(x_dev_ptr: int, n: int, d: int, ld: int, layout: int,
+                                  spec: KernelSpec, cfg: RunConfig, ctx: Context,
+                                  distance_mode: str | None = None) -> CholeskyResult:
+    """Same, with this process's shard rows already resident on the device."""
+    o = KernelOracle(np.zeros((1, 1)), spec, distance_mode)
+    h = C.c_void_p()
+    L.check(L.load().rpc_accelerated_rpcholesky_device(ctx.handle, C.c_void_p(x_dev_ptr), n, d,
+                                                       ld, layout, o._c_spec(), cfg.to_c(),
+                                                       C.byref(h)), ctx.handle)
+    return _wrap_result(h, ctx)
+
+
+def relative_trace_error(oracle: KernelOracle, result: CholeskyResult) -> float:
+    """rpcholesky.hpp:577-583, evaluated from the device-resident factor."""
+    return result.relative_trace_error
+
+
+def sample_discrete(u: np.ndarray, b: int, seed: int, draw0: int = 0, replay: bool = False,
+                    ctx: Context | None = None) -> np.ndarray:
+    """b draws of rng.hpp:80-96 against cumulative_sums(u), on the GPU."""
+    ctx = ctx or default_context()
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    out = np.zeros(b, np.int64)
+    L.check(L.load().rpc_sample_discrete(ctx.handle, u.ctypes.data, u.size, b, seed, draw0,
+                                         int(replay), out.ctypes.data), ctx.handle)
+    return out
+
+
+def rejection_sample_submatrix(h: np.ndarray, proposals, seed: int, draw0: int,
+                               ctx: Context | None = None):
+    """rpcholesky.hpp:167-201 on the GPU: (accepted, positions, chol)."""
+    ctx = ctx or default_context()
+    h = np.asfortranarray(h, dtype=np.float64)
+    b = h.shape[0]
+    prop = np.ascontiguousarray(proposals, dtype=np.int64)
+    acc = np.zeros(b, np.int64)
+    pos = np.zeros(b, np.int64)
+    chol = np.zeros(b * b)
+    m = C.c_int64()
+    L.check(L.load().rpc_rejection_sweep(ctx.handle, h.ctypes.data, b, prop.ctypes.data, seed,
+                                         draw0, acc.ctypes.data, pos.ctypes.data, C.byref(m),
+                                         chol.ctypes.data), ctx.handle)
+    k = m.value
+    return acc[:k].copy(), pos[:k].copy(), chol[: k * k].reshape(k, k, order="F").copy()

@@ -1,0 +1,1044 @@
+// api.cu — host runtime and C-ABI of librpchol_b200.so.
+//
+// Replaces rpchol::accelerated_rpcholesky (rpcholesky.hpp:338-401) for kernel
+// oracles (oracle.hpp:243-327).  The host drives the round loop; all N-sized
+// work stays on the device(s).  One host<->device synchronisation per round
+// reads back the round's status words (scan total, accepted count, pivot ids)
+// that the reference's PivotTrace needs anyway.
+//
+// Row sharding: global scan chunks of 4096 rows are split into
+// P equal contiguous chunk ranges, one per shard.  A shard is either this
+// process's GPU (NCCL mode, one process per GPU) or one of several virtual
+// shards on a single GPU (collectives become local device copies).  Per round
+// the shards exchange only: chunk totals (+ previous round ||G||^2 partials),
+// and the b proposal records (id, ||x||^2, x, F row).  The sweep and L^{-1}
+// are computed redundantly and bit-identically on every shard.
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rpchol_gpu.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace rpcb;
+
+namespace {
+
+struct RpcError {
+  int code;
+  std::string msg;
+};
+
+[[noreturn]] void raise(int code, const std::string& msg) { throw RpcError{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    raise(e == cudaErrorMemoryAllocation ? RPC_ENOMEM : RPC_ECUDA,
+          std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+#define CK(x) cuda_check((x), #x)
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess) raise(RPC_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
+}
+#define NK(x) nccl_check((x), #x)
+
+thread_local std::string g_last_error;
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+}  // namespace
+
+struct rpc_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int world = 1, rank = 0;
+  ncclComm_t comm = nullptr;
+  int nvirt = 1;
+  std::mutex mu;
+  std::string err;
+  std::multimap<size_t, void*> pool;  // cached device blocks (size -> ptr)
+  void* host_pinned = nullptr;
+  size_t host_pinned_bytes = 0;
+
+  int nshards() const { return world * nvirt; }
+  int first_shard() const { return rank * nvirt; }
+
+  void* dalloc(size_t bytes) {
+    bytes = std::max<size_t>(256, round_up((int64_t)bytes, 256));
+    auto it = pool.lower_bound(bytes);
+    if (it != pool.end() && it->first <= bytes * 2) {
+      void* p = it->second;
+      pool.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {  // release the cache and retry once
+      cudaGetLastError();
+      trim();
+      CK(cudaMalloc(&p, bytes));
+    }
+    return p;
+  }
+  void dfree(void* p, size_t bytes) {
+    if (!p) return;
+    bytes = std::max<size_t>(256, round_up((int64_t)bytes, 256));
+    pool.emplace(bytes, p);
+  }
+  void trim() {
+    cudaStreamSynchronize(stream);
+    for (auto& kv : pool) cudaFree(kv.second);
+    pool.clear();
+  }
+  void* pinned(size_t bytes) {
+    if (bytes > host_pinned_bytes) {
+      if (host_pinned) cudaFreeHost(host_pinned);
+      host_pinned = nullptr;
+      CK(cudaMallocHost(&host_pinned, bytes));
+      host_pinned_bytes = bytes;
+    }
+    return host_pinned;
+  }
+};
+
+namespace {
+
+// Device buffer owned through the ctx pool.
+struct DBuf {
+  rpc_ctx* ctx = nullptr;
+  void* p = nullptr;
+  size_t bytes = 0;
+  DBuf() = default;
+  DBuf(rpc_ctx* c, size_t b) : ctx(c), bytes(b) { p = b ? c->dalloc(b) : nullptr; }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
+  DBuf& operator=(DBuf&& o) noexcept {
+    release();
+    ctx = o.ctx;
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    return *this;
+  }
+  ~DBuf() { release(); }
+  void release() {
+    if (p && ctx) ctx->dfree(p, bytes);
+    p = nullptr;
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+struct Layout {
+  int64_t n = 0;
+  int P = 1;
+  int nc = 0;    // real chunks
+  int cpr = 0;   // chunks per shard
+  int ncg = 0;   // P * cpr
+  int64_t row0(int s) const { return std::min<int64_t>(n, (int64_t)s * cpr * kChunk); }
+  int64_t rows(int s) const {
+    return std::min<int64_t>(n, (int64_t)(s + 1) * cpr * kChunk) - row0(s);
+  }
+  int chunks(int s) const { return (int)((rows(s) + kChunk - 1) / kChunk); }
+};
+
+Layout make_layout(int64_t n, int P) {
+  Layout L;
+  L.n = n;
+  L.P = P;
+  L.nc = (int)((n + kChunk - 1) / kChunk);
+  L.cpr = (L.nc + P - 1) / P;
+  L.ncg = L.cpr * P;
+  return L;
+}
+
+struct Shard {
+  int gidx = 0;  // global shard index
+  int64_t row0 = 0, n_loc = 0;
+  int chunk0 = 0, nchunks = 0;
+  DBuf X, sqn, F, u, tile_g2;
+};
+
+}  // namespace
+
+struct rpc_result {
+  rpc_ctx* ctx = nullptr;
+  int64_t n = 0, d = 0, kcur = 0, ldf = 0, b = 0;
+  std::vector<Shard> shards;
+  std::vector<int64_t> pivots;
+  std::vector<std::vector<int64_t>> proposed, accepted;
+  bool exhausted = false;
+  int64_t surplus = 0;
+  double captured_sq = 0.0;
+  double fro2 = 0.0;
+  std::vector<double> chol;  // kcur x kcur column-major
+  rpc_timing timing{};
+};
+
+namespace {
+
+int fail(rpc_ctx* ctx, int code, const std::string& msg) {
+  g_last_error = msg;
+  if (ctx) ctx->err = msg;
+  return code;
+}
+
+template <class F>
+int guarded(rpc_ctx* ctx, F&& f) {
+  try {
+    f();
+    return RPC_OK;
+  } catch (const RpcError& e) {
+    return fail(ctx, e.code, e.msg);
+  } catch (const std::bad_alloc&) {
+    return fail(ctx, RPC_ENOMEM, "out of host memory");
+  } catch (const std::exception& e) {
+    return fail(ctx, RPC_ENUMERIC, e.what());
+  }
+}
+
+// Allgather of `count` doubles per global shard, in place in buf[P][count].
+void allgather(rpc_ctx* ctx, double* buf, size_t count) {
+  if (ctx->world == 1) return;  // virtual shards already write into buf directly
+  NK(ncclAllGather(buf + (size_t)ctx->rank * ctx->nvirt * count, buf, count * ctx->nvirt,
+                   ncclDouble, ctx->comm, ctx->stream));
+}
+
+void validate(int64_t n, int64_t d, const rpc_kernel_spec& k, rpc_run_config& cfg, int& kind) {
+  if (n < 1 || d < 1) raise(RPC_EINVAL, "DataMatrix: need at least one point and one dimension");
+  if (!(k.sigma > 0.0) || !std::isfinite(k.sigma))
+    raise(RPC_EINVAL, "KernelSpec: bandwidth must be positive");
+  int mode = k.distance_mode;
+  if (k.kind == RPC_KERNEL_GAUSSIAN) {
+    if (mode == RPC_DIST_DEFAULT) mode = RPC_DIST_GRAM;
+    if (mode != RPC_DIST_GRAM && mode != RPC_DIST_DIRECT) raise(RPC_EINVAL, "unknown distance mode");
+    kind = mode == RPC_DIST_GRAM ? kGaussGram : kGaussDirect;
+  } else if (k.kind == RPC_KERNEL_L1LAPLACE) {
+    if (mode == RPC_DIST_DEFAULT) mode = RPC_DIST_DIRECT;
+    if (mode == RPC_DIST_GRAM)
+      raise(RPC_EINVAL, "KernelOracle: GramTrick requires an l2 translation-invariant kernel");
+    kind = kL1;
+  } else {
+    raise(RPC_EINVAL, "unknown kernel kind");
+  }
+  if (cfg.block_size < 1) raise(RPC_EINVAL, "accelerated_rpcholesky: block size must be >= 1");
+  if (cfg.block_size > 256)
+    raise(RPC_EINVAL, "accelerated_rpcholesky: this build supports block size <= 256");
+  if (cfg.mode == RPC_FIXED_ROUNDS) {
+    if (cfg.rounds < 1) raise(RPC_EINVAL, "RunConfig: t, b must be >= 1");
+  } else if (cfg.mode == RPC_UNTIL_RANK) {
+    if (cfg.target_rank < 1) raise(RPC_EINVAL, "RunConfig: k, b must be >= 1");
+  } else {
+    raise(RPC_EINVAL, "RunConfig: unknown mode");
+  }
+}
+
+struct Ev {
+  cudaEvent_t e = nullptr;
+  Ev() { CK(cudaEventCreate(&e)); }
+  Ev(const Ev&) = delete;
+  Ev& operator=(const Ev&) = delete;
+  Ev(Ev&& o) noexcept : e(o.e) { o.e = nullptr; }
+  ~Ev() {
+    if (e) cudaEventDestroy(e);
+  }
+};
+
+__global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, int64_t row0,
+                                   int64_t n_loc, const int64_t* __restrict__ piv, int64_t k,
+                                   double* __restrict__ out_rm) {
+  const int64_t i = blockIdx.x;
+  const int64_t lr = piv[i] - row0;
+  if (lr < 0 || lr >= n_loc) return;
+  for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[i * k + j] = F[lr * ldf + j];
+}
+
+// The factorization proper.  `src` points to this process's shard rows (device
+// memory when src_on_device, else host memory of the full X).
+void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
+                       int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
+                       rpc_run_config cfg, rpc_result* res) {
+  int kind = 0;
+  validate(n, d, kspec, cfg, kind);
+  if (layout != RPC_COL_MAJOR && layout != RPC_ROW_MAJOR) raise(RPC_EINVAL, "unknown layout");
+  const bool replay = (cfg.flags & RPC_FLAG_REPLAY_SCAN) != 0;
+  if (replay && ctx->nshards() != 1)
+    raise(RPC_EINVAL, "replay scan requires a single shard (sequential cumulative_sums)");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->stream;
+  const int b = (int)cfg.block_size;
+  int64_t cap = cfg.mode == RPC_FIXED_ROUNDS ? cfg.rounds * cfg.block_size
+                                             : cfg.target_rank + cfg.block_size;
+  cap = std::min(cap, n);
+  const int64_t ldf = round_up(std::max<int64_t>(cap, 1), 16);
+  const int64_t dpad = round_up(d, 16);
+  const Layout L = make_layout(n, ctx->nshards());
+  RecordLayout lay;
+  lay.xoff = 2;
+  lay.foff = 2 + dpad;
+  lay.rec = 2 + dpad + ldf;
+
+  res->ctx = ctx;
+  res->n = n;
+  res->d = d;
+  res->ldf = ldf;
+  res->b = b;
+  rpc_timing& tm = res->timing;
+  int64_t launches = 0;
+
+  // ---- per-shard state + upload -------------------------------------------
+  Ev ev_up0, ev_up1, ev_t0, ev_t1;
+  CK(cudaEventRecord(ev_up0.e, st));
+  res->shards.resize(ctx->nvirt);
+  DBuf nonfinite(ctx, sizeof(int));
+  CK(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
+  int64_t max_tiles = 0;
+  for (int v = 0; v < ctx->nvirt; ++v) {
+    Shard& s = res->shards[v];
+    s.gidx = ctx->first_shard() + v;
+    s.row0 = L.row0(s.gidx);
+    s.n_loc = L.rows(s.gidx);
+    s.chunk0 = s.gidx * L.cpr;
+    s.nchunks = L.chunks(s.gidx);
+    const int64_t nl = std::max<int64_t>(s.n_loc, 1);
+    s.X = DBuf(ctx, sizeof(double) * nl * dpad);
+    s.sqn = DBuf(ctx, sizeof(double) * nl);
+    s.F = DBuf(ctx, sizeof(double) * nl * ldf);
+    s.u = DBuf(ctx, sizeof(double) * nl);
+    s.tile_g2 = DBuf(ctx, sizeof(double) * (nl / 64 + 2));
+    max_tiles = std::max<int64_t>(max_tiles, nl / 64 + 2);
+    if (s.n_loc == 0) continue;
+    // stage this shard's raw rows on the device, then pack (pad, norms)
+    const double* dsrc = nullptr;
+    DBuf tmp;
+    int64_t ld_src = 0;
+    if (src_on_device) {
+      // x_dev holds this process's rows; with virtual shards that is all rows
+      const int64_t off = ctx->nvirt > 1 ? s.row0 : 0;
+      dsrc = layout == RPC_ROW_MAJOR ? src + off * ldx : src + off;
+      ld_src = ldx;
+    } else {
+      if (layout == RPC_ROW_MAJOR) {
+        tmp = DBuf(ctx, sizeof(double) * s.n_loc * d);
+        CK(cudaMemcpy2DAsync(tmp.p, d * sizeof(double), src + s.row0 * ldx, ldx * sizeof(double),
+                             d * sizeof(double), s.n_loc, cudaMemcpyHostToDevice, st));
+        ld_src = d;
+      } else {
+        tmp = DBuf(ctx, sizeof(double) * s.n_loc * d);
+        CK(cudaMemcpy2DAsync(tmp.p, s.n_loc * sizeof(double), src + s.row0, ldx * sizeof(double),
+                             s.n_loc * sizeof(double), d, cudaMemcpyHostToDevice, st));
+        ld_src = s.n_loc;
+      }
+      dsrc = tmp.as<double>();
+    }
+    launch_pack_points(dsrc, s.n_loc, (int)d, ld_src, layout == RPC_ROW_MAJOR, dpad,
+                       s.X.as<double>(), s.sqn.as<double>(), nonfinite.as<int>(), st);
+    launch_fill(s.u.as<double>(), s.n_loc, 1.0, st);  // u = max(diag, 0) = 1 (oracle.hpp:263)
+    launches += 2;
+    if (tmp.p) CK(cudaStreamSynchronize(st));  // tmp returns to the pool
+  }
+  CK(cudaEventRecord(ev_up1.e, st));
+  {  // DataMatrix rejects non-finite entries (data_matrix.hpp:26-28)
+    int bad = 0;
+    CK(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (ctx->world > 1) {
+      NK(ncclAllReduce(nonfinite.p, nonfinite.p, 1, ncclInt, ncclMax, ctx->comm, st));
+      CK(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    }
+    if (bad) raise(RPC_EINVAL, "DataMatrix: non-finite entry");
+  }
+
+  // ---- replicated per-round buffers ---------------------------------------
+  const int P = L.P;
+  DBuf totals_all(ctx, sizeof(double) * L.ncg), g2_all(ctx, sizeof(double) * L.ncg),
+      chunk_end(ctx, sizeof(double) * L.ncg);
+  DBuf recv(ctx, sizeof(double) * (size_t)P * b * lay.rec), prop(ctx, sizeof(double) * b * lay.rec);
+  DBuf owner(ctx, sizeof(int) * b), Hbuf(ctx, sizeof(double) * b * b),
+      lcol(ctx, sizeof(double) * b * b), lacc(ctx, sizeof(double) * b * b);
+  const int64_t ldl = 256, nbl = 256;
+  DBuf linv(ctx, sizeof(double) * nbl * ldl), pos(ctx, sizeof(int) * b),
+      acc_ids(ctx, sizeof(int64_t) * b), hp(ctx, sizeof(double) * ((size_t)b * (b + 1) / 2 + 1));
+  DBuf status(ctx, sizeof(ScanStatus) + sizeof(SweepOut));
+  DBuf shard_c0(ctx, sizeof(int) * (P + 1));
+  DBuf cumsum;
+  if (replay) cumsum = DBuf(ctx, sizeof(double) * n);
+  {
+    std::vector<int> c0(P + 1);
+    for (int s = 0; s <= P; ++s) c0[s] = s * L.cpr;
+    CK(cudaMemcpyAsync(shard_c0.p, c0.data(), sizeof(int) * (P + 1), cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemsetAsync(totals_all.p, 0, sizeof(double) * L.ncg, st));
+  CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
+  ScanStatus* d_scan = status.as<ScanStatus>();
+  SweepOut* d_sweep = reinterpret_cast<SweepOut*>(d_scan + 1);
+
+  // pinned host mirror: ScanStatus | SweepOut | proposal ids (double) [b] | accepted ids [b]
+  const size_t hbytes = sizeof(ScanStatus) + sizeof(SweepOut) + sizeof(double) * b +
+                        sizeof(int64_t) * b + 64;
+  char* hbuf = static_cast<char*>(ctx->pinned(hbytes));
+  ScanStatus* h_scan = reinterpret_cast<ScanStatus*>(hbuf);
+  SweepOut* h_sweep = reinterpret_cast<SweepOut*>(h_scan + 1);
+  double* h_prop_ids = reinterpret_cast<double*>(h_sweep + 1);
+  int64_t* h_acc_ids = reinterpret_cast<int64_t*>(h_prop_ids + b);
+
+  const double trace_a = (double)n;  // sum of diag(A) = N exactly
+  int64_t kcur = 0;
+  double captured_sq = 0.0;
+  bool pending_g2 = false;
+  std::vector<Ev> upd_ev;
+  upd_ev.reserve(8);
+  double update_ms = 0.0, flops = 0.0, bytes = 0.0;
+  int64_t upd_launches = 0;
+
+  CK(cudaEventRecord(ev_t0.e, st));
+  for (int64_t round = 0;; ++round) {
+    if (cfg.mode == RPC_FIXED_ROUNDS ? round >= cfg.rounds : kcur >= cfg.target_rank) break;
+    const uint64_t draw0 = 2ull * (uint64_t)b * (uint64_t)round;
+    // -- K2: scan of the residual diagonal (+ previous round's ||G||^2 partials)
+    for (Shard& s : res->shards) {
+      launch_chunk_totals(s.u.as<double>(), s.n_loc, s.nchunks, totals_all.as<double>() + s.chunk0, st);
+      ++launches;
+    }
+    allgather(ctx, totals_all.as<double>(), L.cpr);
+    if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
+    launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr, L.ncg,
+                        chunk_end.as<double>(), d_scan, st);
+    ++launches;
+    if (replay) {
+      launch_replay_scan(res->shards[0].u.as<double>(), n, cumsum.as<double>(), d_scan, st);
+      ++launches;
+    }
+    // -- K1/K2: b proposals; owners write their records
+    for (Shard& s : res->shards) {
+      SampleParams sp{};
+      sp.u = s.u.as<double>();
+      sp.X = s.X.as<double>();
+      sp.sqn = s.sqn.as<double>();
+      sp.F = s.F.as<double>();
+      sp.n_loc = s.n_loc;
+      sp.dpad = dpad;
+      sp.ldf = ldf;
+      sp.kcur = (int)kcur;
+      sp.row0 = s.row0;
+      sp.chunk0 = s.chunk0;
+      sp.n_chunks_local = s.nchunks;
+      sp.n_chunks_global = L.ncg;
+      sp.shard = s.gidx;
+      sp.n_shards = P;
+      sp.shard_chunk0 = shard_c0.as<int>();
+      sp.chunk_end = chunk_end.as<double>();
+      sp.seed = cfg.seed;
+      sp.draw0 = draw0;
+      sp.b = b;
+      sp.lay = lay;
+      sp.records = recv.as<double>() + (size_t)s.gidx * b * lay.rec;
+      sp.owner = owner.as<int>();
+      if (replay) launch_replay_sample(sp, cumsum.as<double>(), st);
+      else if (s.n_loc > 0) launch_sample(sp, st);
+      ++launches;
+    }
+    allgather(ctx, recv.as<double>(), (size_t)b * lay.rec);
+    const int64_t words = 2 + dpad + kcur;
+    launch_select(recv.as<double>(), (int64_t)b * lay.rec, owner.as<int>(), b, lay.rec, words,
+                  prop.as<double>(), st);
+    // -- K3: H block; K4: rejection sweep (replicated on every shard)
+    launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
+                  Hbuf.as<double>(), st);
+    launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
+                 pos.as<int>(), acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(), d_sweep,
+                 hp.as<double>(), st);
+    launches += 3;
+    CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
+                       cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),
+                         sizeof(double), b, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    if (pending_g2) {
+      captured_sq += h_scan->g2_prev;  // captured_sq += ||G||_F^2 (rpcholesky.hpp:388)
+      pending_g2 = false;
+    }
+    if (h_scan->exhausted) {  // rpcholesky.hpp:356-359
+      res->exhausted = true;
+      break;
+    }
+    if (cfg.stop_tol > 0.0 && (trace_a - captured_sq) <= cfg.stop_tol * trace_a) break;
+    const int m = h_sweep->m;
+    std::vector<int64_t> pr(b), ac(m);
+    for (int j = 0; j < b; ++j) pr[j] = (int64_t)h_prop_ids[j];
+    for (int a = 0; a < m; ++a) ac[a] = h_acc_ids[a];
+    if (m > 0) {
+      if (kcur + m > cap)
+        raise(RPC_ENUMERIC, "accelerated_rpcholesky: factor capacity exceeded (duplicate pivot)");
+      CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+      launch_linv(lacc.as<double>(), m, (int)nbl, ldl, linv.as<double>(), st);
+      ++launches;
+      CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
+      for (Shard& s : res->shards) {
+        if (s.n_loc == 0) continue;
+        UpdateParams up{};
+        up.X = s.X.as<double>();
+        up.ldx = dpad;
+        up.dchunks = (int)(dpad / 16);
+        up.d = (int)d;
+        up.sqn = s.sqn.as<double>();
+        up.F = s.F.as<double>();
+        up.ldf = ldf;
+        up.kcur = (int)kcur;
+        up.u = s.u.as<double>();
+        up.n_loc = s.n_loc;
+        up.row0 = s.row0;
+        up.prop = prop.as<double>();
+        up.lay = lay;
+        up.pos = pos.as<int>();
+        up.m = m;
+        up.linv = linv.as<double>();
+        up.ldl = ldl;
+        up.sigma = kspec.sigma;
+        up.kind = kind;
+        up.tile_g2 = s.tile_g2.as<double>();
+        upd_ev.emplace_back();
+        upd_ev.emplace_back();
+        CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
+        const int bm = launch_update(up, st);
+        CK(cudaEventRecord(upd_ev.back().e, st));
+        if (bm < 0) raise(RPC_EINVAL, "unsupported accepted block size");
+        const int64_t ntiles = (s.n_loc + bm - 1) / bm;
+        launch_tile_to_chunk(s.tile_g2.as<double>(), (int)ntiles, kChunk / bm, s.nchunks,
+                             g2_all.as<double>() + s.chunk0, st);
+        launches += 2;
+        ++upd_launches;
+        const double N = (double)s.n_loc;
+        flops += 2.0 * N * m * kcur + N * (double)m * m + 2.0 * N * m * d;
+        bytes += 8.0 * (N * kcur + N * m + N * d + 2.0 * N);
+      }
+      pending_g2 = true;
+      res->pivots.insert(res->pivots.end(), ac.begin(), ac.end());
+      kcur += m;
+    }
+    res->proposed.push_back(std::move(pr));
+    res->accepted.push_back(std::move(ac));
+  }
+  CK(cudaEventRecord(ev_t1.e, st));
+  // ---- finalize ----------------------------------------------------------------
+  if (pending_g2) {  // last round's ||G||^2 (no further scan consumed it)
+    allgather(ctx, g2_all.as<double>(), L.cpr);
+    launch_chunk_prefix(totals_all.as<double>(), g2_all.as<double>(), L.ncg,
+                        chunk_end.as<double>(), d_scan, st);
+    ++launches;
+    CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    captured_sq += h_scan->g2_prev;
+  }
+  res->kcur = kcur;
+  res->captured_sq = captured_sq;
+  if (cfg.mode == RPC_UNTIL_RANK && kcur > cfg.target_rank) res->surplus = kcur - cfg.target_rank;
+  // ||F||_F^2 for relative_trace_error (chunk partials, global chunk order)
+  for (Shard& s : res->shards) {
+    launch_fsq_chunks(s.F.as<double>(), ldf, s.n_loc, (int)kcur, s.nchunks,
+                      totals_all.as<double>() + s.chunk0, st);
+    ++launches;
+  }
+  CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
+  allgather(ctx, totals_all.as<double>(), L.cpr);
+  launch_chunk_prefix(g2_all.as<double>(), totals_all.as<double>(), L.ncg, chunk_end.as<double>(),
+                      d_scan, st);
+  ++launches;
+  CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  res->fro2 = h_scan->g2_prev;
+  // chol_factor = lower(F(pivots, :)) (rpcholesky.hpp:140-145): owners gather pivot rows
+  res->chol.assign((size_t)kcur * kcur, 0.0);
+  if (kcur > 0) {
+    DBuf piv(ctx, sizeof(int64_t) * kcur), cb(ctx, sizeof(double) * kcur * kcur);
+    CK(cudaMemcpyAsync(piv.p, res->pivots.data(), sizeof(int64_t) * kcur, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(cb.p, 0, sizeof(double) * kcur * kcur, st));
+    for (Shard& s : res->shards) {
+      if (s.n_loc == 0) continue;
+      chol_gather_kernel<<<(unsigned)kcur, 128, 0, st>>>(s.F.as<double>(), ldf, s.row0, s.n_loc,
+                                                          piv.as<int64_t>(), kcur, cb.as<double>());
+      ++launches;
+    }
+    if (ctx->world > 1)  // each pivot row lives on exactly one rank: sum the zeros away
+      NK(ncclAllReduce(cb.p, cb.p, (size_t)kcur * kcur, ncclDouble, ncclSum, ctx->comm, st));
+    std::vector<double> rm((size_t)kcur * kcur);
+    CK(cudaMemcpyAsync(rm.data(), cb.p, sizeof(double) * kcur * kcur, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < kcur; ++i)
+      for (int64_t j = 0; j <= i; ++j) res->chol[j * kcur + i] = rm[i * kcur + j];
+  }
+  float ms = 0.f;
+  CK(cudaEventElapsedTime(&ms, ev_t0.e, ev_t1.e));
+  tm.factorize_ms = ms;
+  CK(cudaEventElapsedTime(&ms, ev_up0.e, ev_up1.e));
+  tm.upload_ms = ms;
+  for (size_t i = 0; i + 1 < upd_ev.size(); i += 2) {
+    CK(cudaEventElapsedTime(&ms, upd_ev[i].e, upd_ev[i + 1].e));
+    update_ms += ms;
+  }
+  tm.update_ms = update_ms;
+  tm.update_flops = flops;
+  tm.update_bytes = bytes;
+  tm.update_launches = upd_launches;
+  tm.kernel_launches = launches;
+  // release the point copies; F, u stay with the result
+  for (Shard& s : res->shards) {
+    s.X.release();
+    s.sqn.release();
+    s.tile_g2.release();
+  }
+}
+
+rpc_result* new_result() { return new rpc_result(); }
+
+}  // namespace
+
+// ============================================================================
+// C ABI
+// ============================================================================
+extern "C" {
+
+const char* rpc_last_error(const rpc_ctx* ctx) {
+  return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+static int make_ctx(int device, int nvirt, rpc_ctx** out) {
+  if (!out) return fail(nullptr, RPC_EINVAL, "null output pointer");
+  *out = nullptr;
+  rpc_ctx* ctx = new rpc_ctx();
+  int rc = guarded(ctx, [&] {
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) raise(RPC_ECUDA, "rpc_create: no such CUDA device");
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) raise(RPC_ECUDA, "rpc_create: this build targets sm_100a (B200)");
+    if (nvirt < 1 || nvirt > 64) raise(RPC_EINVAL, "rpc_create_virtual: n_shards must be in [1, 64]");
+    ctx->device = device;
+    ctx->nvirt = nvirt;
+    CK(cudaSetDevice(device));
+    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+  });
+  if (rc) {
+    g_last_error = ctx->err;
+    delete ctx;
+    return rc;
+  }
+  *out = ctx;
+  return RPC_OK;
+}
+
+int rpc_create(int device, rpc_ctx** out) { return make_ctx(device, 1, out); }
+int rpc_create_virtual(int device, int n_shards, rpc_ctx** out) {
+  return make_ctx(device, n_shards, out);
+}
+
+int rpc_nccl_unique_id(void* id128) {
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId size");
+  return guarded(nullptr, [&] {
+    ncclUniqueId id;
+    NK(ncclGetUniqueId(&id));
+    std::memcpy(id128, &id, sizeof id);
+  });
+}
+
+int rpc_create_nccl(int device, const void* id128, int nranks, int rank, rpc_ctx** out) {
+  int rc = make_ctx(device, 1, out);
+  if (rc) return rc;
+  rpc_ctx* ctx = *out;
+  rc = guarded(ctx, [&] {
+    if (nranks < 1 || rank < 0 || rank >= nranks) raise(RPC_EINVAL, "rpc_create_nccl: bad rank");
+    ctx->world = nranks;
+    ctx->rank = rank;
+    if (nranks > 1) {
+      ncclUniqueId id;
+      std::memcpy(&id, id128, sizeof id);
+      NK(ncclCommInitRank(&ctx->comm, nranks, id, rank));
+    }
+  });
+  if (rc) {
+    g_last_error = ctx->err;
+    rpc_destroy(ctx);
+    *out = nullptr;
+  }
+  return rc;
+}
+
+void rpc_destroy(rpc_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->trim();
+  if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  if (ctx->comm) ncclCommDestroy(ctx->comm);
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+int rpc_shard_rows(const rpc_ctx* ctx, int64_t n, int local, int64_t* row0, int64_t* nrows) {
+  if (!ctx || local < 0 || local >= ctx->nvirt || n < 0) return RPC_EINVAL;
+  const Layout L = make_layout(n, ctx->nshards());
+  const int s = ctx->first_shard() + local;
+  *row0 = L.row0(s);
+  *nrows = L.rows(s);
+  return RPC_OK;
+}
+
+int rpc_accelerated_rpcholesky(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                               int layout, rpc_kernel_spec kernel, rpc_run_config cfg,
+                               rpc_result** out) {
+  if (!ctx || !out) return fail(ctx, RPC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *out = nullptr;
+  rpc_result* r = new_result();
+  int rc = guarded(ctx, [&] {
+    if (!x && n > 0) raise(RPC_EINVAL, "null point matrix");
+    if (ldx < (layout == RPC_ROW_MAJOR ? d : n)) raise(RPC_EINVAL, "leading dimension too small");
+    run_factorization(ctx, x, false, n, d, ldx, layout, kernel, cfg, r);
+  });
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return RPC_OK;
+}
+
+int rpc_accelerated_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, int64_t d,
+                                      int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                      rpc_run_config cfg, rpc_result** out) {
+  if (!ctx || !out) return fail(ctx, RPC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *out = nullptr;
+  rpc_result* r = new_result();
+  int rc = guarded(ctx, [&] { run_factorization(ctx, x_dev, true, n, d, ldx, layout, kernel, cfg, r); });
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return RPC_OK;
+}
+
+int64_t rpc_result_n(const rpc_result* r) { return r ? r->n : 0; }
+int64_t rpc_result_rank(const rpc_result* r) { return r ? r->kcur : 0; }
+int64_t rpc_result_num_rounds(const rpc_result* r) { return r ? (int64_t)r->proposed.size() : 0; }
+int64_t rpc_result_block_size(const rpc_result* r) { return r ? r->b : 0; }
+int rpc_result_rank_exhausted(const rpc_result* r) { return r ? (int)r->exhausted : 0; }
+int64_t rpc_result_surplus(const rpc_result* r) { return r ? r->surplus : 0; }
+double rpc_result_captured_sq(const rpc_result* r) { return r ? r->captured_sq : 0.0; }
+
+double rpc_result_relative_trace_error(const rpc_result* r) {
+  if (!r || r->n <= 0) return 1.0;
+  const double tr = (double)r->n;
+  return std::clamp((tr - r->fro2) / tr, 0.0, 1.0);
+}
+
+int rpc_result_pivots(const rpc_result* r, int64_t* out) {
+  if (!r || (!out && r->kcur)) return RPC_EINVAL;
+  std::copy(r->pivots.begin(), r->pivots.end(), out);
+  return RPC_OK;
+}
+
+int rpc_result_chol_copy(const rpc_result* r, double* out) {
+  if (!r || (!out && r->kcur)) return RPC_EINVAL;
+  std::copy(r->chol.begin(), r->chol.end(), out);
+  return RPC_OK;
+}
+
+int rpc_result_round(const rpc_result* r, int64_t round, int64_t* proposed, int64_t* accepted,
+                     int64_t* n_accepted) {
+  if (!r || round < 0 || round >= (int64_t)r->proposed.size()) return RPC_ERANGE;
+  if (proposed) std::copy(r->proposed[round].begin(), r->proposed[round].end(), proposed);
+  if (accepted) std::copy(r->accepted[round].begin(), r->accepted[round].end(), accepted);
+  if (n_accepted) *n_accepted = (int64_t)r->accepted[round].size();
+  return RPC_OK;
+}
+
+int rpc_result_factor_copy(const rpc_result* r, double* out, int64_t ld, int layout) {
+  if (!r) return RPC_EINVAL;
+  rpc_ctx* ctx = r->ctx;
+  return guarded(ctx, [&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t k = r->kcur;
+    if (k == 0) return;
+    for (const Shard& s : r->shards) {
+      if (s.n_loc == 0) continue;
+      if (layout == RPC_ROW_MAJOR) {
+        if (ld < k) raise(RPC_EINVAL, "leading dimension too small");
+        CK(cudaMemcpy2DAsync(out + s.row0 * ld, ld * sizeof(double), s.F.p,
+                             r->ldf * sizeof(double), k * sizeof(double), s.n_loc,
+                             cudaMemcpyDeviceToHost, st));
+      } else {
+        if (ld < s.n_loc) raise(RPC_EINVAL, "leading dimension too small");
+        // transpose column blocks on the device, then one 2D copy per block
+        const int64_t cb = std::max<int64_t>(1, std::min<int64_t>(k, (int64_t)(512ll << 20) / (8 * s.n_loc)));
+        DBuf tmp(ctx, sizeof(double) * s.n_loc * cb);
+        for (int64_t c0 = 0; c0 < k; c0 += cb) {
+          const int64_t nc = std::min(cb, k - c0);
+          launch_f_to_colmajor(s.F.as<double>(), r->ldf, s.n_loc, (int)c0, (int)nc,
+                               tmp.as<double>(), s.n_loc, st);
+          CK(cudaMemcpy2DAsync(out + c0 * ld + s.row0, ld * sizeof(double), tmp.p,
+                               s.n_loc * sizeof(double), s.n_loc * sizeof(double), nc,
+                               cudaMemcpyDeviceToHost, st));
+        }
+        CK(cudaStreamSynchronize(st));
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int rpc_result_residual_diag_copy(const rpc_result* r, double* out) {
+  if (!r) return RPC_EINVAL;
+  rpc_ctx* ctx = r->ctx;
+  return guarded(ctx, [&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    for (const Shard& s : r->shards)
+      if (s.n_loc)
+        CK(cudaMemcpyAsync(out + s.row0, s.u.p, sizeof(double) * s.n_loc, cudaMemcpyDeviceToHost,
+                           ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
+const double* rpc_result_factor_device(const rpc_result* r, int64_t* ldf, int64_t* row0,
+                                       int64_t* nrows) {
+  if (!r || r->shards.empty()) return nullptr;
+  if (ldf) *ldf = r->ldf;
+  if (row0) *row0 = r->shards[0].row0;
+  if (nrows) *nrows = r->shards[0].n_loc;
+  return r->shards[0].F.as<double>();
+}
+
+int rpc_result_timing(const rpc_result* r, rpc_timing* t) {
+  if (!r || !t) return RPC_EINVAL;
+  *t = r->timing;
+  return RPC_OK;
+}
+
+void rpc_result_free(rpc_result* r) {
+  if (!r) return;
+  if (r->ctx) {
+    std::lock_guard<std::mutex> lk(r->ctx->mu);
+    cudaStreamSynchronize(r->ctx->stream);
+    r->shards.clear();  // buffers return to the ctx pool
+  }
+  delete r;
+}
+
+// ---- component entry points --------------------------------------------------
+int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                       int layout, rpc_kernel_spec kspec, const int64_t* cols, int64_t m,
+                       double* out, int64_t ld_out, double* device_ms) {
+  if (!ctx) return fail(nullptr, RPC_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded(ctx, [&] {
+    int kind = 0;
+    rpc_run_config cfg{1, RPC_UNTIL_RANK, 0, 1, 0, 0.0, 0};
+    validate(n, d, kspec, cfg, kind);
+    for (int64_t j = 0; j < m; ++j)
+      if (cols[j] < 0 || cols[j] >= n) raise(RPC_ERANGE, "KernelOracle cols: index out of range");
+    if (ld_out < n) raise(RPC_EINVAL, "leading dimension too small");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t dpad = round_up(d, 16);
+    DBuf X(ctx, sizeof(double) * n * dpad), sqn(ctx, sizeof(double) * n),
+        raw(ctx, sizeof(double) * n * d);
+    if (layout == RPC_ROW_MAJOR)
+      CK(cudaMemcpy2DAsync(raw.p, d * 8, x, ldx * 8, d * 8, n, cudaMemcpyHostToDevice, st));
+    else
+      CK(cudaMemcpy2DAsync(raw.p, n * 8, x, ldx * 8, n * 8, d, cudaMemcpyHostToDevice, st));
+    launch_pack_points(raw.as<double>(), n, (int)d, layout == RPC_ROW_MAJOR ? d : n,
+                       layout == RPC_ROW_MAJOR, dpad, X.as<double>(), sqn.as<double>(), nullptr,
+                       st);
+    RecordLayout lay{2 + dpad, 2, 2 + dpad};
+    const int64_t mb = std::min<int64_t>(m, 256);
+    DBuf prop(ctx, sizeof(double) * std::max<int64_t>(mb, 1) * lay.rec),
+        pos(ctx, sizeof(int) * 256), outd(ctx, sizeof(double) * n * std::max<int64_t>(mb, 1)),
+        tile(ctx, sizeof(double) * (n / 64 + 2));
+    std::vector<int> hpos(256);
+    for (int i = 0; i < 256; ++i) hpos[i] = i;
+    CK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * 256, cudaMemcpyHostToDevice, st));
+    double total_ms = 0.0;
+    Ev e0, e1;
+    for (int64_t c0 = 0; c0 < m; c0 += mb) {
+      const int64_t nc = std::min(mb, m - c0);
+      // records: id, ||x||^2, x (from the packed device copy)
+      for (int64_t j = 0; j < nc; ++j) {
+        CK(cudaMemcpyAsync(prop.as<double>() + j * lay.rec + 1, sqn.as<double>() + cols[c0 + j],
+                           sizeof(double), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(prop.as<double>() + j * lay.rec + 2,
+                           X.as<double>() + cols[c0 + j] * dpad, sizeof(double) * dpad,
+                           cudaMemcpyDeviceToDevice, st));
+      }
+      std::vector<double> ids(nc);
+      for (int64_t j = 0; j < nc; ++j) ids[j] = (double)cols[c0 + j];
+      CK(cudaMemcpy2DAsync(prop.p, lay.rec * 8, ids.data(), 8, 8, nc, cudaMemcpyHostToDevice, st));
+      UpdateParams up{};
+      up.X = X.as<double>();
+      up.ldx = dpad;
+      up.dchunks = (int)(dpad / 16);
+      up.d = (int)d;
+      up.sqn = sqn.as<double>();
+      up.F = X.as<double>();
+      up.ldf = dpad;
+      up.kcur = 0;
+      up.u = nullptr;
+      up.n_loc = n;
+      up.row0 = 0;
+      up.prop = prop.as<double>();
+      up.lay = lay;
+      up.pos = pos.as<int>();
+      up.m = (int)nc;
+      up.sigma = kspec.sigma;
+      up.kind = kind;
+      up.tile_g2 = tile.as<double>();
+      up.columns_only = 1;
+      up.cols_out = outd.as<double>();
+      up.ld_out = n;
+      CK(cudaEventRecord(e0.e, st));
+      if (launch_update(up, st) < 0) raise(RPC_EINVAL, "unsupported column block");
+      CK(cudaEventRecord(e1.e, st));
+      CK(cudaMemcpy2DAsync(out + c0 * ld_out, ld_out * 8, outd.p, n * 8, n * 8, nc,
+                           cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      CK(cudaEventElapsedTime(&ms, e0.e, e1.e));
+      total_ms += ms;
+    }
+    CK(cudaGetLastError());
+    if (device_ms) *device_ms = total_ms;
+  });
+}
+
+int rpc_sample_discrete(rpc_ctx* ctx, const double* u, int64_t n, int64_t b, uint64_t seed,
+                        uint64_t draw0, int replay, int64_t* out) {
+  if (!ctx) return fail(nullptr, RPC_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded(ctx, [&] {
+    if (n == 0) raise(RPC_EINVAL, "sample_discrete: empty weights");
+    if (b < 1 || b > 65535) raise(RPC_EINVAL, "sample_discrete: bad draw count");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const Layout L = make_layout(n, 1);
+    DBuf du(ctx, sizeof(double) * n), totals(ctx, sizeof(double) * L.ncg),
+        cend(ctx, sizeof(double) * L.ncg), status(ctx, sizeof(ScanStatus)),
+        rec(ctx, sizeof(double) * 2 * b), owner(ctx, sizeof(int) * b), c0(ctx, sizeof(int) * 2),
+        zeros(ctx, sizeof(double) * n), cs;
+    CK(cudaMemcpyAsync(du.p, u, sizeof(double) * n, cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(zeros.p, 0, sizeof(double) * n, st));
+    int hc0[2] = {0, L.ncg};
+    CK(cudaMemcpyAsync(c0.p, hc0, sizeof hc0, cudaMemcpyHostToDevice, st));
+    SampleParams sp{};
+    sp.u = du.as<double>();
+    sp.X = zeros.as<double>();
+    sp.sqn = zeros.as<double>();
+    sp.F = zeros.as<double>();
+    sp.n_loc = n;
+    sp.dpad = 0;
+    sp.ldf = 0;
+    sp.kcur = 0;
+    sp.chunk0 = 0;
+    sp.n_chunks_local = L.nc;
+    sp.n_chunks_global = L.ncg;
+    sp.shard = 0;
+    sp.n_shards = 1;
+    sp.shard_chunk0 = c0.as<int>();
+    sp.chunk_end = cend.as<double>();
+    sp.seed = seed;
+    sp.draw0 = draw0;
+    sp.b = (int)b;
+    sp.lay = RecordLayout{2, 2, 2};
+    sp.records = rec.as<double>();
+    sp.owner = owner.as<int>();
+    ScanStatus hs{};
+    if (replay) {
+      cs = DBuf(ctx, sizeof(double) * n);
+      launch_replay_scan(du.as<double>(), n, cs.as<double>(), status.as<ScanStatus>(), st);
+      CK(cudaMemcpyAsync(&hs, status.p, sizeof hs, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (hs.exhausted) raise(RPC_EINVAL, "sample_discrete: total weight must be > 0");
+      launch_replay_sample(sp, cs.as<double>(), st);
+    } else {
+      launch_chunk_totals(du.as<double>(), n, L.nc, totals.as<double>(), st);
+      CK(cudaMemsetAsync(totals.as<double>() + L.nc, 0, sizeof(double) * (L.ncg - L.nc), st));
+      launch_chunk_prefix(totals.as<double>(), nullptr, L.ncg, cend.as<double>(),
+                          status.as<ScanStatus>(), st);
+      CK(cudaMemcpyAsync(&hs, status.p, sizeof hs, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (hs.exhausted) raise(RPC_EINVAL, "sample_discrete: total weight must be > 0");
+      launch_sample(sp, st);
+    }
+    std::vector<double> h(2 * b);
+    CK(cudaMemcpyAsync(h.data(), rec.p, sizeof(double) * 2 * b, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    for (int64_t j = 0; j < b; ++j) out[j] = (int64_t)h[2 * j];
+  });
+}
+
+int rpc_rejection_sweep(rpc_ctx* ctx, const double* h, int64_t b, const int64_t* proposals,
+                        uint64_t seed, uint64_t draw0, int64_t* accepted, int64_t* positions,
+                        int64_t* m_out, double* chol) {
+  if (!ctx) return fail(nullptr, RPC_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded(ctx, [&] {
+    if (b < 1 || b > 256) raise(RPC_EINVAL, "rejection_sample_submatrix: size mismatch");
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    std::vector<double> hrm((size_t)b * b), rec((size_t)2 * b);
+    for (int64_t p = 0; p < b; ++p)
+      for (int64_t q = 0; q < b; ++q) hrm[p * b + q] = h[q * b + p];
+    for (int64_t j = 0; j < b; ++j) {
+      rec[2 * j] = (double)proposals[j];
+      rec[2 * j + 1] = 0.0;
+    }
+    DBuf dH(ctx, sizeof(double) * b * b), dprop(ctx, sizeof(double) * 2 * b),
+        dpos(ctx, sizeof(int) * b), dids(ctx, sizeof(int64_t) * b),
+        dl(ctx, sizeof(double) * b * b), dla(ctx, sizeof(double) * b * b),
+        dout(ctx, sizeof(SweepOut)), dhp(ctx, sizeof(double) * (b * (b + 1) / 2 + 1));
+    CK(cudaMemcpyAsync(dH.p, hrm.data(), sizeof(double) * b * b, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(dprop.p, rec.data(), sizeof(double) * 2 * b, cudaMemcpyHostToDevice, st));
+    launch_sweep(dH.as<double>(), (int)b, seed, draw0, dprop.as<double>(), RecordLayout{2, 2, 2},
+                 dpos.as<int>(), dids.as<int64_t>(), dl.as<double>(), dla.as<double>(),
+                 dout.as<SweepOut>(), dhp.as<double>(), st);
+    SweepOut so{};
+    CK(cudaMemcpyAsync(&so, dout.p, sizeof so, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    const int m = so.m;
+    std::vector<int> hp(m);
+    if (m) {
+      CK(cudaMemcpyAsync(hp.data(), dpos.p, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(accepted, dids.p, sizeof(int64_t) * m, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(chol, dla.p, sizeof(double) * m * m, cudaMemcpyDeviceToHost, st));
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    for (int i = 0; i < m; ++i) positions[i] = hp[i];
+    *m_out = m;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,114 @@
+// kernels.h — host-side launch wrappers for the sm_100a kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rpcb {
+
+enum DistKind { kGaussGram = 0, kGaussDirect = 1, kL1 = 2 };
+
+// Proposal record layout (one per draw, fp64 words):
+//   [0] global id (exact in fp64), [1] ||x||^2, [2, 2+dpad) x, [2+dpad, 2+dpad+ldf) F row
+struct RecordLayout {
+  int64_t rec;    // record stride (even)
+  int64_t xoff;   // = 2
+  int64_t foff;   // = 2 + dpad
+};
+
+// ---- K2: residual-diagonal scan + inverse-CDF sampling --------------------
+// Per-chunk totals of u over this shard's chunks (deterministic tree).
+void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
+                         cudaStream_t st);
+// Sequential prefix over all global chunk totals -> chunk_end[], status.
+struct ScanStatus {
+  double total;       // cumsum[N-1]
+  double g2_prev;     // sum over chunks of previous round's ||G||^2 partials
+  int32_t exhausted;  // !(total > 0)
+  int32_t pad;
+};
+void launch_chunk_prefix(const double* totals_all, const double* g2_all, int n_chunks,
+                         double* chunk_end, ScanStatus* status, cudaStream_t st);
+// One CTA per draw: draw j uses SplitMix64 counter draw0 + j.
+struct SampleParams {
+  const double* u;        // this shard's residual diagonal
+  const double* X;        // [n_loc][dpad]
+  const double* sqn;      // [n_loc]
+  const double* F;        // [n_loc][ldf]
+  int64_t n_loc, dpad, ldf;
+  int kcur;
+  int64_t row0;           // global row of local row 0 (multiple of kChunk)
+  int chunk0;             // first global chunk of this shard
+  int n_chunks_local;
+  int n_chunks_global;
+  int shard;              // global shard index
+  int n_shards;
+  const int* shard_chunk0;  // [n_shards + 1] chunk ranges (device)
+  const double* chunk_end;  // [n_chunks_global]
+  uint64_t seed, draw0;
+  int b;
+  RecordLayout lay;
+  double* records;          // this shard's slot: [b][rec]
+  int* owner;               // [b]
+};
+void launch_sample(const SampleParams& p, cudaStream_t st);
+// Replay mode (single shard): strictly sequential cumulative_sums (rng.hpp:67-75)
+// and std::upper_bound + clamp + plateau walk (rng.hpp:80-96), reference rounding.
+void launch_replay_scan(const double* u, int64_t n, double* cumsum, ScanStatus* status,
+                        cudaStream_t st);
+void launch_replay_sample(const SampleParams& p, const double* cumsum, cudaStream_t st);
+// prop[j] = records of owner[j]'s slot
+void launch_select(const double* recv, int64_t slot_stride, const int* owner, int b,
+                   int64_t rec, int64_t words, double* prop, cudaStream_t st);
+
+// ---- K3/K4: H block, rejection sweep, L^{-1} ------------------------------
+void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d, int kcur,
+                   int kind, double sigma, double* H, cudaStream_t st);
+struct SweepOut {
+  int32_t m;
+  int32_t pad;
+};
+// H: [b][b] row-major (only the lower triangle is read). Outputs pos[m], acc_ids[m],
+// lcol[m][b] (column c of the elimination = c-th acceptance), lacc_cm[c][a] (m x m,
+// column-major), status.
+void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
+                  RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
+                  SweepOut* out, double* scratch_hp, cudaStream_t st);
+// linv_rm[a][c] = (L^{-1})[a][c], [nb][ldl], zero outside the lower m x m triangle.
+void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, double* linv_rm,
+                 cudaStream_t st);
+
+// ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
+struct UpdateParams {
+  const double* X;  int64_t ldx; int dchunks; int d;
+  const double* sqn;
+  double* F; int64_t ldf; int kcur;
+  double* u;
+  int64_t n_loc; int64_t row0;
+  const double* prop; RecordLayout lay;
+  const int* pos; int m;
+  const double* linv; int64_t ldl;
+  double sigma; int kind;
+  double* tile_g2;          // [n_tiles] per-CTA ||G||^2 partial (row order)
+  // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
+  int columns_only; double* cols_out; int64_t ld_out;
+};
+// Returns the row-tile height used (64 or 128), or -1 if m unsupported.
+int update_tile_rows(int m);
+int launch_update(const UpdateParams& p, cudaStream_t st);
+// per-chunk sum of per-tile partials (tile = rows_per_tile rows)
+void launch_tile_to_chunk(const double* tile_g2, int n_tiles, int tiles_per_chunk,
+                          int n_chunks_local, double* chunk_g2, cudaStream_t st);
+// per-chunk ||F(rows, :k)||^2
+void launch_fsq_chunks(const double* F, int64_t ldf, int64_t n_loc, int k, int n_chunks_local,
+                       double* chunk_out, cudaStream_t st);
+// F row-major [n_loc][ldf] columns [c0, c0+nc) -> out col-major [nc][ld_out]
+void launch_f_to_colmajor(const double* F, int64_t ldf, int64_t n_loc, int c0, int nc,
+                          double* out, int64_t ld_out, cudaStream_t st);
+// X (host layout already on device as col-major or row-major) -> padded row-major + norms
+// *nonfinite is set to 1 if any input coordinate is NaN/Inf (DataMatrix, data_matrix.hpp:26-28)
+void launch_pack_points(const double* src, int64_t n_loc, int d, int64_t ld_src,
+                        int src_row_major, int64_t dpad, double* X, double* sqn,
+                        int* nonfinite, cudaStream_t st);
+void launch_fill(double* p, int64_t n, double v, cudaStream_t st);
+
+}  // namespace rpcb

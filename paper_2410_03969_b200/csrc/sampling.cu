@@ -1,0 +1,386 @@
+// sampling.cu — K1/K2: SplitMix64 counter draws, residual-diagonal scan and
+// inverse-CDF proposal sampling; plus small utility kernels.
+//
+// Reference semantics (rng.hpp:67-96, rpcholesky.hpp:361-365): cumsum is the
+// inclusive prefix of u; a draw maps r = next_double() to target = r * total,
+// idx = first i with cumsum[i] > target, clamped to N-1, then walked back over
+// a zero-weight plateau.  Draw j of round t is SplitMix64 counter 2*b*t + j.
+//
+// Fast mode replaces the strictly sequential scan by a fixed, p-invariant
+// two-level sequence that is still a monotone prefix sum with the zero-plateau
+// property (adding a zero weight never changes the running value):
+//   global chunks of kChunk = 4096 rows; inside a chunk thread t owns rows
+//   [16t, 16t+16) and runs s_e = s_{e-1} + u_e; thread bases B_0 = 0,
+//   B_{t+1} = B_t + s_15(t) (serial); local_e = B_t + s_e; chunk offsets
+//   off_0 = 0, chunk_end[c] = off_c + local_last(c), off_{c+1} = chunk_end[c];
+//   cumsum_i = off_c + local_i.
+// Every addition is one IEEE rounding, so cumsum differs from the reference's
+// sequential sum only by association.  Replay mode runs the
+// reference's exact sequential scan and std::upper_bound on one thread.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rpcb {
+
+// Per-thread sequential partials and serial thread bases for one chunk.
+// sh must hold kScanThreads + 1 doubles.  Returns this thread's base B_t.
+__device__ __forceinline__ double chunk_scan_core(const double* __restrict__ uc, int n_valid,
+                                                  double (&s)[16], double* sh) {
+  const int t = threadIdx.x;
+  const int e0 = t * 16;
+  double acc = 0.0;
+  if (e0 + 16 <= n_valid) {
+    const double2* v2 = reinterpret_cast<const double2*>(uc + e0);
+    double v[16];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const double2 w = __ldg(v2 + q);
+      v[2 * q] = w.x;
+      v[2 * q + 1] = w.y;
+    }
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      acc = __dadd_rn(acc, v[e]);
+      s[e] = acc;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const double v = (e0 + e < n_valid) ? __ldg(uc + e0 + e) : 0.0;
+      acc = __dadd_rn(acc, v);
+      s[e] = acc;
+    }
+  }
+  sh[t] = acc;
+  __syncthreads();
+  if (t == 0) {
+    double b = 0.0;
+    for (int i = 0; i < kScanThreads; i += 8) {
+      double tt[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) tt[q] = sh[i + q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        sh[i + q] = b;
+        b = __dadd_rn(b, tt[q]);
+      }
+    }
+    sh[kScanThreads] = b;
+  }
+  __syncthreads();
+  return sh[t];
+}
+
+__global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double* __restrict__ u,
+                                                                    int64_t n_loc,
+                                                                    double* __restrict__ totals) {
+  __shared__ double sh[kScanThreads + 1];
+  const int c = blockIdx.x;
+  const int64_t r0 = (int64_t)c * kChunk;
+  const int n_valid = (int)lmin(kChunk, n_loc - r0);
+  double s[16];
+  const double base = chunk_scan_core(u + r0, n_valid, s, sh);
+  const int last = n_valid - 1;
+  if (threadIdx.x == (last >> 4)) {
+    double v = 0.0;
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      if (e == (last & 15)) v = s[e];
+    totals[c] = __dadd_rn(base, v);
+  }
+}
+
+void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
+                         cudaStream_t st) {
+  if (n_chunks > 0) chunk_totals_kernel<<<n_chunks, kScanThreads, 0, st>>>(u, n_loc, totals);
+}
+
+__global__ void chunk_prefix_kernel(const double* __restrict__ totals, const double* g2_all,
+                                    int n_chunks, double* __restrict__ chunk_end,
+                                    ScanStatus* status) {
+  if (threadIdx.x != 0) return;
+  double off = 0.0;
+  for (int c = 0; c < n_chunks; ++c) {
+    off = __dadd_rn(off, totals[c]);
+    chunk_end[c] = off;
+  }
+  double g2 = 0.0;
+  if (g2_all)
+    for (int c = 0; c < n_chunks; ++c) g2 = __dadd_rn(g2, g2_all[c]);
+  status->total = off;
+  status->g2_prev = g2;
+  status->exhausted = !(off > 0.0);
+}
+
+void launch_chunk_prefix(const double* totals_all, const double* g2_all, int n_chunks,
+                         double* chunk_end, ScanStatus* status, cudaStream_t st) {
+  chunk_prefix_kernel<<<1, 32, 0, st>>>(totals_all, g2_all, n_chunks, chunk_end, status);
+}
+
+// Copies the sampled point's record (id, ||x||^2, x, F row) into rec.
+__device__ __forceinline__ void write_record(const SampleParams& p, int64_t lrow, double* rec) {
+  if (threadIdx.x == 0) {
+    rec[0] = (double)(p.row0 + lrow);
+    rec[1] = p.sqn[lrow];
+  }
+  const double* xr = p.X + lrow * p.dpad;
+  for (int i = threadIdx.x; i < p.dpad; i += blockDim.x) rec[p.lay.xoff + i] = xr[i];
+  const double* fr = p.F + lrow * p.ldf;
+  for (int k = threadIdx.x; k < p.kcur; k += blockDim.x) rec[p.lay.foff + k] = fr[k];
+}
+
+__global__ void __launch_bounds__(kScanThreads) sample_kernel(SampleParams p) {
+  __shared__ double sh[kScanThreads + 1];
+  __shared__ int s_chunk, s_mode, s_owner, s_best;
+  __shared__ double s_off, s_target;
+  const int j = blockIdx.x;
+  if (threadIdx.x == 0) {
+    const double r = u01(splitmix64_draw(p.seed, p.draw0 + (uint64_t)j));
+    const int nc = p.n_chunks_global;
+    const double total = p.chunk_end[nc - 1];
+    const double target = __dmul_rn(r, total);
+    int lo = 0, hi = nc;  // upper_bound over chunk ends
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (target < p.chunk_end[mid]) hi = mid; else lo = mid + 1;
+    }
+    int mode = 0;
+    if (lo == nc) {  // clamp to N-1, then walk back over the zero plateau
+      int c = nc - 1;
+      while (c > 0 && p.chunk_end[c] == p.chunk_end[c - 1]) --c;
+      lo = c;
+      mode = 1;
+    }
+    int o = 0;
+    while (o + 1 < p.n_shards && p.shard_chunk0[o + 1] <= lo) ++o;
+    s_chunk = lo;
+    s_mode = mode;
+    s_target = target;
+    s_off = lo ? p.chunk_end[lo - 1] : 0.0;
+    s_owner = o;
+    s_best = mode ? -1 : INT_MAX;
+    p.owner[j] = o;
+  }
+  __syncthreads();
+  if (s_owner != p.shard) return;
+  const int lc = s_chunk - p.chunk0;
+  const int64_t r0 = (int64_t)lc * kChunk;
+  const int n_valid = (int)lmin(kChunk, p.n_loc - r0);
+  double s[16];
+  const double base = chunk_scan_core(p.u + r0, n_valid, s, sh);
+  const double off = s_off, target = s_target;
+  const int e0 = threadIdx.x * 16;
+  if (s_mode == 0) {
+    int best = INT_MAX;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const double cum = __dadd_rn(off, __dadd_rn(base, s[e]));
+      if (e0 + e < n_valid && cum > target && best == INT_MAX) best = e0 + e;
+    }
+    if (best != INT_MAX) atomicMin(&s_best, best);
+  } else {
+    int best = -1;
+    double prev = __dadd_rn(off, base);
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      const double cum = __dadd_rn(off, __dadd_rn(base, s[e]));
+      if (e0 + e < n_valid && cum > prev) best = e0 + e;
+      prev = cum;
+    }
+    if (best >= 0) atomicMax(&s_best, best);
+  }
+  __syncthreads();
+  int best = s_best;
+  if (best == INT_MAX || best < 0) best = 0;  // unreachable when total > 0
+  write_record(p, r0 + best, p.records + (int64_t)j * p.lay.rec);
+}
+
+void launch_sample(const SampleParams& p, cudaStream_t st) {
+  sample_kernel<<<p.b, kScanThreads, 0, st>>>(p);
+}
+
+// ---- replay mode -----------------------------------------------------------
+__global__ void replay_scan_kernel(const double* __restrict__ u, int64_t n,
+                                   double* __restrict__ cumsum, ScanStatus* status) {
+  if (threadIdx.x != 0) return;
+  double acc = 0.0;
+  int64_t i = 0;
+  for (; i + 8 <= n; i += 8) {
+    double v[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[q] = __ldg(u + i + q);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      acc = __dadd_rn(acc, v[q]);
+      cumsum[i + q] = acc;
+    }
+  }
+  for (; i < n; ++i) {
+    acc = __dadd_rn(acc, u[i]);
+    cumsum[i] = acc;
+  }
+  status->total = acc;
+  status->exhausted = !(acc > 0.0);
+}
+
+void launch_replay_scan(const double* u, int64_t n, double* cumsum, ScanStatus* status,
+                        cudaStream_t st) {
+  replay_scan_kernel<<<1, 32, 0, st>>>(u, n, cumsum, status);
+}
+
+__global__ void replay_sample_kernel(SampleParams p, const double* __restrict__ cumsum) {
+  __shared__ int64_t s_idx;
+  const int j = blockIdx.x;
+  if (threadIdx.x == 0) {
+    const int64_t n = p.n_loc;
+    const double total = cumsum[n - 1];
+    const double target = __dmul_rn(u01(splitmix64_draw(p.seed, p.draw0 + (uint64_t)j)), total);
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = lo + ((hi - lo) >> 1);
+      if (target < cumsum[mid]) hi = mid; else lo = mid + 1;
+    }
+    int64_t idx = lo;
+    if (idx >= n) idx = n - 1;
+    while (idx > 0 && cumsum[idx] == cumsum[idx - 1]) --idx;
+    s_idx = idx;
+    p.owner[j] = 0;
+  }
+  __syncthreads();
+  write_record(p, s_idx, p.records + (int64_t)j * p.lay.rec);
+}
+
+void launch_replay_sample(const SampleParams& p, const double* cumsum, cudaStream_t st) {
+  replay_sample_kernel<<<p.b, 128, 0, st>>>(p, cumsum);
+}
+
+__global__ void select_kernel(const double* __restrict__ recv, int64_t slot_stride,
+                              const int* __restrict__ owner, int64_t rec, int64_t words,
+                              double* __restrict__ prop) {
+  const int j = blockIdx.x;
+  const double* src = recv + (int64_t)owner[j] * slot_stride + (int64_t)j * rec;
+  double* dst = prop + (int64_t)j * rec;
+  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
+}
+
+void launch_select(const double* recv, int64_t slot_stride, const int* owner, int b,
+                   int64_t rec, int64_t words, double* prop, cudaStream_t st) {
+  select_kernel<<<b, 256, 0, st>>>(recv, slot_stride, owner, rec, words, prop);
+}
+
+// ---- utilities ---------------------------------------------------------------
+__global__ void tile_to_chunk_kernel(const double* __restrict__ tile_g2, int n_tiles,
+                                     int tiles_per_chunk, int n_chunks,
+                                     double* __restrict__ chunk_g2) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n_chunks) return;
+  double s = 0.0;
+  const int t0 = c * tiles_per_chunk;
+  const int t1 = min(n_tiles, t0 + tiles_per_chunk);
+  for (int t = t0; t < t1; ++t) s = __dadd_rn(s, tile_g2[t]);
+  chunk_g2[c] = s;
+}
+
+void launch_tile_to_chunk(const double* tile_g2, int n_tiles, int tiles_per_chunk,
+                          int n_chunks_local, double* chunk_g2, cudaStream_t st) {
+  if (n_chunks_local > 0)
+    tile_to_chunk_kernel<<<(n_chunks_local + 127) / 128, 128, 0, st>>>(
+        tile_g2, n_tiles, tiles_per_chunk, n_chunks_local, chunk_g2);
+}
+
+__global__ void __launch_bounds__(256) fsq_chunks_kernel(const double* __restrict__ F,
+                                                         int64_t ldf, int64_t n_loc, int k,
+                                                         double* __restrict__ out) {
+  __shared__ double sh[256];
+  const int64_t r0 = (int64_t)blockIdx.x * kChunk;
+  const int64_t r1 = lmin(n_loc, r0 + kChunk);
+  double acc = 0.0;
+  for (int64_t r = r0 + threadIdx.x; r < r1; r += 256) {
+    const double* fr = F + r * ldf;
+    double s = 0.0;
+    for (int c = 0; c < k; ++c) s = __dadd_rn(s, __dmul_rn(fr[c], fr[c]));
+    acc = __dadd_rn(acc, s);
+  }
+  sh[threadIdx.x] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int i = 0; i < 256; ++i) t = __dadd_rn(t, sh[i]);
+    out[blockIdx.x] = t;
+  }
+}
+
+void launch_fsq_chunks(const double* F, int64_t ldf, int64_t n_loc, int k, int n_chunks_local,
+                       double* chunk_out, cudaStream_t st) {
+  if (n_chunks_local > 0)
+    fsq_chunks_kernel<<<n_chunks_local, 256, 0, st>>>(F, ldf, n_loc, k, chunk_out);
+}
+
+__global__ void f_to_colmajor_kernel(const double* __restrict__ F, int64_t ldf, int64_t n_loc,
+                                     int c0, int nc, double* __restrict__ out, int64_t ld_out) {
+  __shared__ double tile[32][33];
+  const int64_t rb = (int64_t)blockIdx.x * 32;
+  const int cb = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = rb + i;
+    const int c = cb + threadIdx.x;
+    tile[i][threadIdx.x] = (r < n_loc && c < nc) ? F[r * ldf + c0 + c] : 0.0;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int c = cb + i;
+    const int64_t r = rb + threadIdx.x;
+    if (r < n_loc && c < nc) out[(int64_t)c * ld_out + r] = tile[threadIdx.x][i];
+  }
+}
+
+void launch_f_to_colmajor(const double* F, int64_t ldf, int64_t n_loc, int c0, int nc,
+                          double* out, int64_t ld_out, cudaStream_t st) {
+  if (n_loc <= 0 || nc <= 0) return;
+  dim3 grid((unsigned)((n_loc + 31) / 32), (unsigned)((nc + 31) / 32)), block(32, 8);
+  f_to_colmajor_kernel<<<grid, block, 0, st>>>(F, ldf, n_loc, c0, nc, out, ld_out);
+}
+
+// src: this shard's rows, either row-major [n_loc][ld_src] or column-major
+// [d][ld_src].  Output padded row-major X and ||x||^2 in ascending coordinate
+// order without FMA contraction (oracle.hpp:252).
+__global__ void pack_points_kernel(const double* __restrict__ src, int64_t n_loc, int d,
+                                   int64_t ld_src, int src_row_major, int64_t dpad,
+                                   double* __restrict__ X, double* __restrict__ sqn,
+                                   int* nonfinite) {
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n_loc) return;
+  double s = 0.0;
+  bool bad = false;
+  for (int c = 0; c < dpad; ++c) {
+    double v = 0.0;
+    if (c < d) v = src_row_major ? src[r * ld_src + c] : src[(int64_t)c * ld_src + r];
+    bad |= !isfinite(v);
+    X[r * dpad + c] = v;
+    if (c < d) s = __dadd_rn(s, __dmul_rn(v, v));
+  }
+  sqn[r] = s;
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+}
+
+void launch_pack_points(const double* src, int64_t n_loc, int d, int64_t ld_src,
+                        int src_row_major, int64_t dpad, double* X, double* sqn,
+                        int* nonfinite, cudaStream_t st) {
+  if (n_loc > 0)
+    pack_points_kernel<<<(unsigned)((n_loc + 255) / 256), 256, 0, st>>>(
+        src, n_loc, d, ld_src, src_row_major, dpad, X, sqn, nonfinite);
+}
+
+__global__ void fill_kernel(double* p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = v;
+}
+
+void launch_fill(double* p, int64_t n, double v, cudaStream_t st) {
+  if (n > 0) fill_kernel<<<(unsigned)lmin(4096, (n + 255) / 256), 256, 0, st>>>(p, n, v);
+}
+
+}  // namespace rpcb

@@ -1,0 +1,286 @@
+"""Parity of the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bars (BASELINE.json north_star): pivots bit-identical; factor within 1e-10
+relative Frobenius error; relative trace error within 1e-8.  Component kernels
+are checked at their own natural bars (exact for the sampler and the sweep given
+identical inputs; 1e-13 for kernel columns, which differ from the oracle only in
+the DMMA summation order of the Gram term and in the last ulp of exp()).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from paper_2410_03969_b200 import api
+from paper_2410_03969_b200 import workloads as wl
+
+pytestmark = pytest.mark.gpu
+
+F_TOL = 1e-10       # relative Frobenius error of the factor
+TRACE_TOL = 1e-8    # |trace error difference|
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    c = api.Context(0)
+    yield c
+    c.close()
+
+
+def run_both(x, kernel, sigma, k=None, b=8, seed=0, rounds=None, ctx=None, replay=False,
+             dist=None, stop_tol=0.0):
+    if rounds is not None:
+        cfg = api.RunConfig.fixed_rounds(rounds, b, seed)
+        okw = dict(mode="fixed_rounds", rounds=rounds)
+    else:
+        cfg = api.RunConfig.until_rank(k, b, seed)
+        okw = dict(target_rank=k)
+    cfg.replay_scan = replay
+    cfg.stop_tol = stop_tol
+    g = api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec(kernel, sigma), dist), cfg,
+                                   ctx)
+    o = po.Oracle(x=x, kernel=kernel, sigma=sigma, dist=dist, n_threads=8)
+    r = po.accelerated_rpcholesky(o, block_size=b, seed=seed, stop_tol=stop_tol, **okw)
+    return g, r, o
+
+
+def assert_parity(g, r, o):
+    assert np.array_equal(g.pivots, r.pivots)
+    assert len(g.proposed) == len(r.proposed)
+    for a, bb in zip(g.proposed, r.proposed):
+        assert np.array_equal(a, bb)
+    for a, bb in zip(g.accepted, r.accepted):
+        assert np.array_equal(a, bb)
+    assert g.rank_exhausted == r.rank_exhausted
+    assert g.surplus == r.surplus
+    f = g.factor
+    nrm = np.linalg.norm(r.factor)
+    rel = np.linalg.norm(f - r.factor) / nrm if nrm > 0 else np.linalg.norm(f)
+    assert rel <= F_TOL, rel
+    err_o = po.relative_trace_error(o, r.factor)
+    assert abs(g.relative_trace_error - err_o) <= TRACE_TOL
+    np.testing.assert_allclose(g.residual_diag, r.residual_diag, rtol=0, atol=1e-10)
+    np.testing.assert_allclose(g.chol_factor, r.chol, rtol=0, atol=1e-10)
+    return rel
+
+
+# ---------------------------------------------------------------- components
+def test_sample_discrete_replay_bitexact(ctx):
+    rng = np.random.default_rng(1)
+    for n in (1, 7, 4096, 4097, 10000, 50000):
+        u = rng.random(n)
+        u[rng.random(n) < 0.3] = 0.0
+        if n > 1:
+            u[-min(n // 3, 500):] = 0.0  # trailing zero plateau exercises the clamp walk
+        if u.sum() == 0:
+            u[0] = 1.0
+        cs = po.cumulative_sums(u)
+        for seed in (0, 3):
+            want = [po.sample_discrete(cs, po.u01(po.splitmix64_draw(seed, j))) for j in range(64)]
+            got = api.sample_discrete(u, 64, seed, 0, replay=True, ctx=ctx)
+            assert list(got) == want
+
+
+def test_sample_discrete_fast_matches(ctx):
+    rng = np.random.default_rng(2)
+    for n in (5, 4096, 12289, 100000):
+        u = rng.random(n) ** 3
+        u[rng.random(n) < 0.2] = 0.0
+        cs = po.cumulative_sums(u)
+        want = [po.sample_discrete(cs, po.u01(po.splitmix64_draw(9, j))) for j in range(200)]
+        got = api.sample_discrete(u, 200, 9, 0, replay=False, ctx=ctx)
+        assert list(got) == want
+        assert np.all(u[got] > 0.0)   # zero-weight entries are never returned
+
+
+def test_sample_discrete_clamp_case(ctx):
+    # r = 1 - 2^-53 draws may round target up to the total: clamp + plateau walk
+    u = np.array([0.0, 3.0, 0.0, 0.0, 0.0])
+    for replay in (False, True):
+        got = api.sample_discrete(u, 50, 123, 0, replay=replay, ctx=ctx)
+        assert np.all(got == 1)
+
+
+def test_sample_discrete_errors(ctx):
+    with pytest.raises(ValueError):
+        api.sample_discrete(np.zeros(10), 4, 0, ctx=ctx)
+
+
+def test_rejection_sweep_bitexact(ctx):
+    x = wl.gen_c1(400, 5, 3)
+    o = po.Oracle(x=x, kernel="gaussian", sigma=1.3)
+    rng = np.random.default_rng(4)
+    for b in (1, 2, 17, 40, 120, 200, 256):
+        prop = rng.integers(0, 400, b)
+        prop[b // 2:] = prop[: b - b // 2]  # duplicates
+        h = o.submatrix(prop, prop)
+        for seed in (0, 77):
+            ga, gp, gl = api.rejection_sample_submatrix(h, prop, seed, 5, ctx=ctx)
+            oa, op, ol = po.rejection_sweep(h, prop, seed, 5)
+            assert np.array_equal(ga, oa) and np.array_equal(gp, op)
+            assert np.array_equal(gl, ol)   # bit-identical given identical H
+
+
+def test_rejection_sweep_reference_properties(ctx):  # test_rpcholesky.cpp:98-140
+    for seed in range(50):
+        a, _, l = api.rejection_sample_submatrix(np.array([[0.37]]), [5], seed, 0, ctx=ctx)
+        assert list(a) == [5] and l[0, 0] == pytest.approx(math.sqrt(0.37))
+        a, _, _ = api.rejection_sample_submatrix(np.full((2, 2), 2.0), [3, 3], seed, 0, ctx=ctx)
+        assert len(a) == 1
+        a, _, _ = api.rejection_sample_submatrix(np.diag([0.5, 1.5, 0.25]), [0, 1, 2], seed, 0,
+                                                 ctx=ctx)
+        assert len(a) == 3
+
+
+@pytest.mark.parametrize("kernel,dist,d", [("gaussian", "gram", 10), ("gaussian", "gram", 37),
+                                           ("gaussian", "direct", 12), ("l1laplace", None, 50),
+                                           ("l1laplace", None, 3)])
+def test_kernel_columns(ctx, kernel, dist, d):
+    x = wl.gen_c3(5000, d, 1) * 3.0
+    sigma = math.sqrt(d) * 0.7
+    o = po.Oracle(x=x, kernel=kernel, sigma=sigma, dist=dist, n_threads=8)
+    ko = api.KernelOracle(x, api.KernelSpec(kernel, sigma), dist)
+    rng = np.random.default_rng(5)
+    for m in (1, 8, 9, 64, 120, 129, 200, 256, 300):
+        cols = rng.integers(0, 5000, m)
+        got = ko.columns(cols, ctx)
+        want = o.columns(cols)
+        assert np.max(np.abs(got - want)) <= 1e-13, (m, np.max(np.abs(got - want)))
+        # same-index pin: the pivot's own entry is exactly kappa(x, x) = 1
+        assert np.all(got[cols, np.arange(m)] == 1.0)
+
+
+def test_kernel_columns_colmajor_input(ctx):
+    x = np.asfortranarray(wl.gen_c1(3000, 6, 2))
+    o = po.Oracle(x=x, kernel="gaussian", sigma=2.0)
+    got = api.KernelOracle(x, api.KernelSpec("gaussian", 2.0)).columns([0, 5, 2999], ctx)
+    assert np.max(np.abs(got - o.columns([0, 5, 2999]))) <= 1e-13
+
+
+# ----------------------------------------------------------- full algorithm
+def test_c1_small_gaussian_parity(ctx):
+    x = wl.gen_c1(4000, 10, 0)
+    g, r, o = run_both(x, "gaussian", math.sqrt(10.0), k=200, b=40, ctx=ctx)
+    assert g.rank >= 200
+    assert_parity(g, r, o)
+
+
+def test_c1_full_parity(ctx):
+    w = wl.CONFIGS["C1"]
+    x = w.points()
+    g, r, o = run_both(x, w.kernel, w.sigma, k=w.k, b=w.b, seed=w.seed, ctx=ctx)
+    assert_parity(g, r, o)
+
+
+def test_c1_replay_mode_parity(ctx):
+    w = wl.CONFIGS["C1"]
+    x = w.points(8000)
+    g, r, o = run_both(x, w.kernel, w.sigma, k=w.k, b=w.b, ctx=ctx, replay=True)
+    assert_parity(g, r, o)
+
+
+def test_l1_parity(ctx):
+    x = wl.gen_c3(6000, 50, 0)
+    g, r, o = run_both(x, "l1laplace", 5.0, k=300, b=120, ctx=ctx)
+    assert_parity(g, r, o)
+
+
+def test_gaussian_direct_parity(ctx):
+    x = wl.gen_c2(5000, 20, 0)
+    g, r, o = run_both(x, "gaussian", math.sqrt(20.0), k=150, b=50, ctx=ctx, dist="direct")
+    assert_parity(g, r, o)
+
+
+def test_large_block_parity(ctx):  # b = 200 exercises the 64-row tile variant
+    x = wl.gen_c5(6000, 100, 0)
+    g, r, o = run_both(x, "l1laplace", 10.0, k=400, b=200, ctx=ctx)
+    assert_parity(g, r, o)
+
+
+@pytest.mark.parametrize("b", [1, 3, 8, 17])
+def test_fixed_rounds_and_small_blocks(ctx, b):
+    x = wl.gen_c1(2000, 4, 7)
+    g, r, o = run_both(x, "gaussian", 1.0, rounds=6, b=b, seed=11, ctx=ctx)
+    assert_parity(g, r, o)
+    assert all(len(a) >= 1 for a in g.accepted)   # first proposal always accepted
+
+
+def test_exact_rank_termination(ctx):  # test_rpcholesky.cpp:199-212
+    base = wl.gen_c1(5, 3, 1) * 2.0
+    x = np.repeat(base, 40, axis=0)          # kernel matrix of exact rank 5
+    for kernel in ("gaussian", "l1laplace"):
+        g, r, o = run_both(x, kernel, 1.0, k=5, b=2, ctx=ctx)
+        assert np.array_equal(g.pivots, r.pivots)
+        assert g.relative_trace_error <= 1e-9
+
+
+def test_rank_exhausted_flag(ctx):  # rpcholesky.hpp:356-359
+    x = np.zeros((50, 3))                    # all-ones kernel matrix: rank 1, u -> 0 exactly
+    g, r, o = run_both(x, "gaussian", 1.0, k=10, b=3, ctx=ctx)
+    assert g.rank_exhausted and r.rank_exhausted
+    assert g.rank == r.rank == 1
+    assert_parity(g, r, o)
+
+
+def test_stop_tol(ctx):
+    x = wl.gen_c1(3000, 2, 5)
+    g, r, o = run_both(x, "gaussian", 1.0, k=500, b=10, ctx=ctx, stop_tol=0.05)
+    assert g.rank < 500
+    assert g.relative_trace_error <= 0.05 + 1e-12
+    assert_parity(g, r, o)
+
+
+def test_tiny_n(ctx):
+    x = np.array([[0.0], [1.0], [3.0]])
+    g, r, o = run_both(x, "gaussian", 1.0, k=3, b=2, ctx=ctx)
+    assert_parity(g, r, o)
+    assert g.rank == 3
+
+
+def test_reference_invariants_on_gpu_output(ctx):  # test_rpcholesky.cpp:226-355
+    x = wl.gen_c2(3000, 20, 1)
+    cfg = api.RunConfig.until_rank(100, 30, 4)
+    g = api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec("gaussian", 4.0)), cfg, ctx)
+    assert len(set(g.pivots.tolist())) == g.rank
+    u = g.residual_diag
+    assert np.all(u >= 0.0) and np.all(u <= 1.0 + 1e-8)
+    f = g.factor
+    assert abs(u.sum() - (3000 - np.sum(f * f))) <= 1e-8 * 3000
+    assert np.array_equal(g.chol_factor, np.tril(f[g.pivots]))
+    assert abs(g.captured_sq - np.sum(f * f)) <= 1e-9 * 3000
+
+
+def test_invalid_arguments(ctx):
+    x = wl.gen_c1(100, 3, 0)
+    ko = api.KernelOracle(x, api.KernelSpec("gaussian", 1.0))
+    with pytest.raises(ValueError, match="block size"):
+        api.accelerated_rpcholesky(ko, api.RunConfig(block_size=0, target_rank=3), ctx)
+    with pytest.raises(ValueError, match="bandwidth"):
+        api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec("gaussian", -1.0)),
+                                   api.RunConfig.until_rank(3, 2, 0), ctx)
+    with pytest.raises(ValueError, match="GramTrick"):
+        api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec("l1laplace", 1.0), "gram"),
+                                   api.RunConfig.until_rank(3, 2, 0), ctx)
+    bad = x.copy()
+    bad[5, 1] = np.nan
+    with pytest.raises(ValueError, match="non-finite"):
+        api.accelerated_rpcholesky(api.KernelOracle(bad, api.KernelSpec("gaussian", 1.0)),
+                                   api.RunConfig.until_rank(3, 2, 0), ctx)
+
+
+# --------------------------------------------------------------- sharding
+@pytest.mark.parametrize("p", [2, 3, 5])
+def test_virtual_shards_p_invariance(p):
+    x = wl.gen_c1(20000, 10, 0)
+    cfg = api.RunConfig.until_rank(200, 40, 0)
+    ko = api.KernelOracle(x, api.KernelSpec("gaussian", math.sqrt(10.0)))
+    c1 = api.Context(0)
+    cp = api.Context(0, virtual_shards=p)
+    g1 = api.accelerated_rpcholesky(ko, cfg, c1)
+    gp = api.accelerated_rpcholesky(ko, cfg, cp)
+    assert np.array_equal(g1.pivots, gp.pivots)
+    assert np.array_equal(g1.factor, gp.factor)          # bitwise
+    assert g1.relative_trace_error == gp.relative_trace_error
+    assert g1.captured_sq == gp.captured_sq
+    assert np.array_equal(g1.chol_factor, gp.chol_factor)
