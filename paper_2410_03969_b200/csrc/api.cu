@@ -19,6 +19,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -56,6 +57,24 @@ void nccl_check(ncclResult_t r, const char* what) {
 #define NK(x) nccl_check((x), #x)
 
 thread_local std::string g_last_error;
+
+// RPC_DEBUG_SYNC=1: synchronise and check after every launch (localises faults).
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = std::getenv("RPC_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+void dbg(cudaStream_t st, const char* what) {
+  if (!debug_sync()) return;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw RpcError{RPC_ECUDA, std::string("after ") + what + ": " + cudaGetErrorString(e)};
+  }
+}
 
 int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
@@ -373,10 +392,13 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   DBuf recv(ctx, sizeof(double) * (size_t)P * b * lay.rec), prop(ctx, sizeof(double) * b * lay.rec);
   DBuf owner(ctx, sizeof(int) * b), Hbuf(ctx, sizeof(double) * b * b),
       lcol(ctx, sizeof(double) * b * b), lacc(ctx, sizeof(double) * b * b);
-  const int64_t ldl = 256, nbl = 256;
+  const int64_t ldl = 272, nbl = 256;  // L^{-1} columns shifted by kcur & 1 (update.cu)
   DBuf linv(ctx, sizeof(double) * nbl * ldl), pos(ctx, sizeof(int) * b),
       acc_ids(ctx, sizeof(int64_t) * b), hp(ctx, sizeof(double) * ((size_t)b * (b + 1) / 2 + 1));
   DBuf status(ctx, sizeof(ScanStatus) + sizeof(SweepOut));
+  // accepted-pivot operands of the fused update (rows permuted, see common.cuh perm_row)
+  DBuf xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * ldf),
+      sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
   DBuf shard_c0(ctx, sizeof(int) * (P + 1));
   DBuf cumsum;
   if (replay) cumsum = DBuf(ctx, sizeof(double) * n);
@@ -421,6 +443,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
     launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr, L.ncg,
                         chunk_end.as<double>(), d_scan, st);
+    dbg(st, "scan");
     ++launches;
     if (replay) {
       launch_replay_scan(res->shards[0].u.as<double>(), n, cumsum.as<double>(), d_scan, st);
@@ -453,6 +476,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.owner = owner.as<int>();
       if (replay) launch_replay_sample(sp, cumsum.as<double>(), st);
       else if (s.n_loc > 0) launch_sample(sp, st);
+      dbg(st, "sample");
       ++launches;
     }
     allgather(ctx, recv.as<double>(), (size_t)b * lay.rec);
@@ -462,9 +486,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // -- K3: H block; K4: rejection sweep (replicated on every shard)
     launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
                   Hbuf.as<double>(), st);
+    dbg(st, "hblock");
     launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
                  pos.as<int>(), acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(), d_sweep,
                  hp.as<double>(), st);
+    dbg(st, "sweep");
     launches += 3;
     CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
                        cudaMemcpyDeviceToHost, st));
@@ -490,16 +516,19 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       if (kcur + m > cap)
         raise(RPC_ENUMERIC, "accelerated_rpcholesky: factor capacity exceeded (duplicate pivot)");
       CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
-      launch_linv(lacc.as<double>(), m, (int)nbl, ldl, linv.as<double>(), st);
-      ++launches;
+      launch_linv(lacc.as<double>(), m, (int)nbl, ldl, (int)(kcur & 1), linv.as<double>(), st);
+      launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), m, 256, (int)kcur, (int)dpad,
+                             xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
+                             idS.as<double>(), st);
+      dbg(st, "linv+gather");
+      launches += 2;
       CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
       for (Shard& s : res->shards) {
         if (s.n_loc == 0) continue;
         UpdateParams up{};
         up.X = s.X.as<double>();
-        up.ldx = dpad;
+        up.dpad = dpad;
         up.dchunks = (int)(dpad / 16);
-        up.d = (int)d;
         up.sqn = s.sqn.as<double>();
         up.F = s.F.as<double>();
         up.ldf = ldf;
@@ -507,21 +536,25 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.u = s.u.as<double>();
         up.n_loc = s.n_loc;
         up.row0 = s.row0;
-        up.prop = prop.as<double>();
-        up.lay = lay;
-        up.pos = pos.as<int>();
+        up.xs = xs.as<double>();
+        up.fs = fs.as<double>();
+        up.ldfs = ldf;
+        up.sqnS = sqnS.as<double>();
+        up.idS = idS.as<double>();
         up.m = m;
         up.linv = linv.as<double>();
         up.ldl = ldl;
         up.sigma = kspec.sigma;
         up.kind = kind;
         up.tile_g2 = s.tile_g2.as<double>();
+        if (const char* e = std::getenv("RPC_DEBUG_UPDATE")) up.dbg = std::atoi(e);
         upd_ev.emplace_back();
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
         const int bm = launch_update(up, st);
         CK(cudaEventRecord(upd_ev.back().e, st));
-        if (bm < 0) raise(RPC_EINVAL, "unsupported accepted block size");
+        dbg(st, "update");
+        if (bm < 0) raise(RPC_ECUDA, "update kernel launch failed (code " + std::to_string(bm) + ")");
         const int64_t ntiles = (s.n_loc + bm - 1) / bm;
         launch_tile_to_chunk(s.tile_g2.as<double>(), (int)ntiles, kChunk / bm, s.nchunks,
                              g2_all.as<double>() + s.chunk0, st);
@@ -875,9 +908,10 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
                        st);
     RecordLayout lay{2 + dpad, 2, 2 + dpad};
     const int64_t mb = std::min<int64_t>(m, 256);
-    DBuf prop(ctx, sizeof(double) * std::max<int64_t>(mb, 1) * lay.rec),
-        pos(ctx, sizeof(int) * 256), outd(ctx, sizeof(double) * n * std::max<int64_t>(mb, 1)),
-        tile(ctx, sizeof(double) * (n / 64 + 2));
+    DBuf prop(ctx, sizeof(double) * 256 * lay.rec), pos(ctx, sizeof(int) * 256),
+        outd(ctx, sizeof(double) * n * std::max<int64_t>(mb, 1)), tile(ctx, sizeof(double) * (n / 64 + 2)),
+        xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * 16),
+        sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
     std::vector<int> hpos(256);
     for (int i = 0; i < 256; ++i) hpos[i] = i;
     CK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * 256, cudaMemcpyHostToDevice, st));
@@ -896,11 +930,13 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       std::vector<double> ids(nc);
       for (int64_t j = 0; j < nc; ++j) ids[j] = (double)cols[c0 + j];
       CK(cudaMemcpy2DAsync(prop.p, lay.rec * 8, ids.data(), 8, 8, nc, cudaMemcpyHostToDevice, st));
+      launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), (int)nc, 256, 0, (int)dpad,
+                             xs.as<double>(), fs.as<double>(), 16, sqnS.as<double>(),
+                             idS.as<double>(), st);
       UpdateParams up{};
       up.X = X.as<double>();
-      up.ldx = dpad;
+      up.dpad = dpad;
       up.dchunks = (int)(dpad / 16);
-      up.d = (int)d;
       up.sqn = sqn.as<double>();
       up.F = X.as<double>();
       up.ldf = dpad;
@@ -908,10 +944,14 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.u = nullptr;
       up.n_loc = n;
       up.row0 = 0;
-      up.prop = prop.as<double>();
-      up.lay = lay;
-      up.pos = pos.as<int>();
+      up.xs = xs.as<double>();
+      up.fs = fs.as<double>();
+      up.ldfs = 16;
+      up.sqnS = sqnS.as<double>();
+      up.idS = idS.as<double>();
       up.m = (int)nc;
+      up.linv = xs.as<double>();
+      up.ldl = 16;
       up.sigma = kspec.sigma;
       up.kind = kind;
       up.tile_g2 = tile.as<double>();
@@ -919,7 +959,8 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.cols_out = outd.as<double>();
       up.ld_out = n;
       CK(cudaEventRecord(e0.e, st));
-      if (launch_update(up, st) < 0) raise(RPC_EINVAL, "unsupported column block");
+      const int bm = launch_update(up, st);
+      if (bm < 0) raise(RPC_ECUDA, "kernel-column launch failed (code " + std::to_string(bm) + ")");
       CK(cudaEventRecord(e1.e, st));
       CK(cudaMemcpy2DAsync(out + c0 * ld_out, ld_out * 8, outd.p, n * 8, n * 8, nc,
                            cudaMemcpyDeviceToHost, st));

@@ -67,6 +67,71 @@ __device__ __forceinline__ int frag_row(int g, int f, bool paired) {
   return paired ? (2 * g + f) : g;
 }
 
+// Position of logical row n8 (0..7) inside its 8-row group in shared memory:
+// {0,1,2,3} -> {0,2,4,6}, {4,5,6,7} -> {1,3,5,7}.  A half-warp's fragment rows
+// then have distinct (row & 7) >> 1, so the 128B-swizzled fp64 fragment loads
+// of a DMMA m8n8k4 operand are bank-conflict free.
+__host__ __device__ __forceinline__ int perm8(int n8) { return n8 < 4 ? 2 * n8 : 2 * (n8 - 4) + 1; }
+__host__ __device__ __forceinline__ int perm_row(int n) { return (n & ~7) + perm8(n & 7); }
+
+// ---- mbarrier + TMA (sm_90+/sm_100a) ----------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// The retry loop is plain C++ so the compiler sees the branch and reconverges the
+// warp before any following .aligned instruction (mma.sync, shfl.sync).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  while (!mbar_try_wait(bar, parity)) {
+  }
+}
+// 2D tiled TMA load: box at (c0 = inner element, c1 = row) into shared memory,
+// completion signalled on `bar` via complete_tx.
+__device__ __forceinline__ void tma_load_2d(void* smem_dst, const void* tmap, int c0, int c1,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch_desc(const void* tmap) {
+  asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(tmap)) : "memory");
+}
+// Generic-proxy global writes made visible to later async-proxy (TMA) reads.
+__device__ __forceinline__ void fence_proxy_async_global() {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---- reductions -----------------------------------------------------------
 __device__ __forceinline__ double warp_sum_xor(double v) {
 #pragma unroll

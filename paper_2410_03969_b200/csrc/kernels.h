@@ -73,28 +73,37 @@ struct SweepOut {
 void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
                   RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
                   SweepOut* out, double* scratch_hp, cudaStream_t st);
-// linv_rm[a][c] = (L^{-1})[a][c], [nb][ldl], zero outside the lower m x m triangle.
-void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, double* linv_rm,
+// linv_rm[perm_row(a)][c + koff] = (L^{-1})[a][c], [nb][ldl], zero elsewhere (koff = kcur & 1,
+// matching the update kernel's 16-byte-aligned phase-2 tiles).
+void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
                  cudaStream_t st);
 
 // ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
 struct UpdateParams {
-  const double* X;  int64_t ldx; int dchunks; int d;
-  const double* sqn;
-  double* F; int64_t ldf; int kcur;
-  double* u;
+  const double* X; int64_t dpad; int dchunks;   // X shard [n_loc][dpad]
+  const double* sqn;                            // ||x||^2 [n_loc]
+  double* F; int64_t ldf; int kcur;             // F shard [n_loc][ldf]
+  double* u;                                    // residual diagonal [n_loc]
   int64_t n_loc; int64_t row0;
-  const double* prop; RecordLayout lay;
-  const int* pos; int m;
-  const double* linv; int64_t ldl;
+  const double* xs; const double* fs; int64_t ldfs;  // accepted operands [256][dpad|ldfs], rows perm_row(n)
+  const double* sqnS; const double* idS;        // [256] logical column order
+  int m;
+  const double* linv; int64_t ldl;             // L^{-1} rows perm_row(a), [256][ldl]
   double sigma; int kind;
-  double* tile_g2;          // [n_tiles] per-CTA ||G||^2 partial (row order)
+  double* tile_g2;                              // [n_tiles] per-CTA ||G||^2 partial (row order)
   // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
   int columns_only; double* cols_out; int64_t ld_out;
+  int dbg;  // fault bisection (RPC_DEBUG_UPDATE): 1 skip phase 2, 2 skip epilogue barriers
 };
-// Returns the row-tile height used (64 or 128), or -1 if m unsupported.
+// Row-tile height used for m accepted columns (128 or 64), or -1 if m unsupported.
 int update_tile_rows(int m);
+// Launch; returns the tile height, or < 0 on failure (-1 unsupported m, -2 smem attr, -3 TMA map).
 int launch_update(const UpdateParams& p, cudaStream_t st);
+// Gathers the accepted pivots' X rows, F rows (first kcur columns), norms and ids from the
+// proposal records into the update kernel's operand buffers (rows at perm_row(n), n < nb).
+void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,
+                            int kcur, int dpad, double* xs, double* fs, int64_t ldfs,
+                            double* sqnS, double* idS, cudaStream_t st);
 // per-chunk sum of per-tile partials (tile = rows_per_tile rows)
 void launch_tile_to_chunk(const double* tile_g2, int n_tiles, int tiles_per_chunk,
                           int n_chunks_local, double* chunk_g2, cudaStream_t st);

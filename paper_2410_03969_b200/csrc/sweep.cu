@@ -164,7 +164,7 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
 
 // One CTA per column c of L^{-1}: forward substitution L x = e_c, axpy form.
 __global__ void __launch_bounds__(256) linv_kernel(const double* __restrict__ lacc_cm, int m,
-                                                   int nb, int64_t ldl,
+                                                   int nb, int64_t ldl, int koff,
                                                    double* __restrict__ linv_rm) {
   extern __shared__ double rhs[];
   const int c = blockIdx.x, tid = threadIdx.x;
@@ -179,12 +179,12 @@ __global__ void __launch_bounds__(256) linv_kernel(const double* __restrict__ la
     __syncthreads();
   }
   for (int a = tid; a < nb; a += 256)
-    linv_rm[(int64_t)a * ldl + c] = (a >= c && a < m) ? rhs[a] : 0.0;
+    linv_rm[(int64_t)perm_row(a) * ldl + c + koff] = (a >= c && a < m) ? rhs[a] : 0.0;
 }
 
-void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, double* linv_rm,
+void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
                  cudaStream_t st) {
-  if (m > 0) linv_kernel<<<m, 256, m * sizeof(double), st>>>(lacc_cm, m, nb, ldl, linv_rm);
+  if (m > 0) linv_kernel<<<m, 256, m * sizeof(double), st>>>(lacc_cm, m, nb, ldl, koff, linv_rm);
 }
 
 }  // namespace rpcb

@@ -1,149 +1,140 @@
 // update.cu — K5+K6: the fused round update, one CTA per BM-row tile of the shard.
 //
 // For the accepted pivots S (m columns) of a round it computes, without ever
-// writing the N x m kernel panel to HBM:
+// materialising the N x m kernel panel in HBM:
 //   phase 1  acc  = -A(R, S)                      (K5: kernel columns, fused)
 //            acc += F(R, :kcur) F(S, :kcur)^T     (K6: FP64 DMMA GEMM)
-//            G    = -acc  = A(R,S) - F F_S^T      (rpcholesky.hpp:378-383)
-//   phase 2  G   <- G L^{-T}  as a DMMA GEMM with the precomputed L^{-1}
+//            G    = -acc = A(R,S) - F F_S^T       (rpcholesky.hpp:378-383)
+//            G is parked in its final place F(R, kcur:kcur+m) (L2-resident)
+//   phase 2  G   <- G L^{-T}: DMMA GEMM whose A operand is G streamed back by TMA
 //            (right_solve_lower_transposed, rpcholesky.hpp:147-151, 384)
 //   epilogue F(R, kcur:kcur+m) = G ; u(R) = max(u - rowwise||G||^2, 0) ;
 //            per-tile ||G||_F^2 partial                  (rpcholesky.hpp:385-388)
 // Kernel columns (oracle.hpp:71-90, kernels.hpp:60-64): the Gaussian Gram term
 // X(R,:) X(S,:)^T runs on the same DMMA pipeline as the residual GEMM (K = dpad),
-// followed by the clamp / same-index pin / exp epilogue in registers; the
-// Gaussian-direct and l1 distances run on the FP64 CUDA cores from the same
-// staged X tiles, accumulating coordinates in ascending order (bit-identical
-// distances to the reference's sequential sums).
+// followed by the clamp / same-index pin / exp epilogue in registers; Gaussian-direct
+// and l1 distances run on the FP64 CUDA cores from the same staged X tiles in
+// ascending coordinate order (bit-identical distances to the reference's sums).
 //
-// Data movement: cp.async (LDGSTS) multi-stage pipeline of [rows][16] fp64 tiles
-// with the 128-byte swizzle; DMMA fragments use the stride-2 row map so every
-// fragment load is bank-conflict free (common.cuh).
+// Execution: 8 consumer warps + 1 producer warp.  The producer's elected lane
+// streams [rows][16] fp64 tiles with 2D TMA (cp.async.bulk.tensor, 128B swizzle)
+// into an S-stage ring guarded by full/empty mbarriers; consumers run
+// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operand rows are permuted inside 8-row
+// groups (perm8, common.cuh) so every fragment load is bank-conflict free.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <cstdio>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace rpcb {
 
-template <int WC, int NFW>
+template <int NCW_, int WC, int NFW>
 struct UCfg {
-  static constexpr int NF = WC * NFW;  // 8-column fragments
-  static constexpr int NB = 8 * NF;    // tile columns (padded m)
-  static constexpr int NBK = 16 * ((NF + 1) / 2);
-  static constexpr int WR = 8 / WC;
-  static constexpr int BM = 16 * WR;   // tile rows
-  static constexpr int S1 = (WC == 1) ? 4 : 3;
-  static constexpr int S2 = (WC == 1) ? 3 : 2;
+  static constexpr int NCW = NCW_;          // consumer warps
+  static constexpr int NT = 32 * (NCW + 1); // + producer warp
+  static constexpr int WR = NCW / WC;
+  static constexpr int BM = 16 * WR;        // tile rows
+  static constexpr int NF = WC * NFW;       // 8-column fragments
+  static constexpr int NB = 8 * NF;         // tile columns (m padded)
+  static constexpr int S = 4;               // pipeline stages
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = NB * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int GT_BYTES = BM * NBK * 8;
-  static constexpr int FIN_LD = NB + 1;
-  static constexpr int FIN_BYTES = BM * FIN_LD * 8;
-  static constexpr int R1a = S1 * STAGE > GT_BYTES ? S1 * STAGE : GT_BYTES;
-  static constexpr int R1 = ((R1a > FIN_BYTES ? R1a : FIN_BYTES) + 1023) / 1024 * 1024;
-  static constexpr int R2 = S2 * B_BYTES;
-  static constexpr int MISC = NB * (4 + 8 + 8) + BM * 8;
-  static constexpr int SMEM = R1 + R2 + MISC + 1024;
+  static constexpr int MISC = NB * 16 + WC * BM * 8 + BM * 8 + (2 * S + 2) * 8;
+  static constexpr int SMEM = S * STAGE + MISC + 1024;
 };
-
-__device__ __forceinline__ int colmap(int Q, int n8, int NF) {
-  return ((Q | 1) < NF) ? (16 * (Q >> 1) + 2 * n8 + (Q & 1)) : (16 * (Q >> 1) + n8);
-}
 
 __device__ __forceinline__ double lds64(const unsigned char* base, uint32_t off) {
   return *reinterpret_cast<const double*>(base + off);
 }
 
-template <int WC, int NFW>
-__global__ void __launch_bounds__(256, 1) update_kernel(UpdateParams p) {
-  using C = UCfg<WC, NFW>;
-  constexpr int NF = C::NF, NB = C::NB, BM = C::BM;
-  extern __shared__ __align__(1024) unsigned char smem_raw[];
-  unsigned char* smem =
-      (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* r1 = smem;
-  unsigned char* r2 = smem + C::R1;
-  int* s_pos = reinterpret_cast<int*>(r2 + C::R2);
-  double* s_sqnS = reinterpret_cast<double*>(s_pos + NB);
-  double* s_idS = s_sqnS + NB;
-  double* s_rowg2 = s_idS + NB;
+template <int NCW_, int WC, int NFW>
+__global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
+    update_kernel(UpdateParams p, const __grid_constant__ CUtensorMap tmX,
+                  const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmF,
+                  const __grid_constant__ CUtensorMap tmFS, const __grid_constant__ CUtensorMap tmG,
+                  const __grid_constant__ CUtensorMap tmL) {
+  using C = UCfg<NCW_, WC, NFW>;
+  constexpr int BM = C::BM, S = C::S, NCW = C::NCW;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* stages = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  double* s_sqnS = reinterpret_cast<double*>(stages + S * C::STAGE);
+  double* s_idS = s_sqnS + C::NB;
+  double* s_rown = s_idS + C::NB;  // [WC][BM]
+  double* s_rowg2 = s_rown + WC * BM;
+  uint64_t* full = reinterpret_cast<uint64_t*>(s_rowg2 + BM);
+  uint64_t* empty = full + S;
+  uint64_t* gready = empty + S;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, t = lane & 3;
-  const int wr = warp / WC, wc = warp % WC;
   const int64_t tile_row0 = (int64_t)blockIdx.x * BM;
-  const int m = p.m;
-  const int kcur = p.kcur;
+  const int m = p.m, kcur = p.kcur;
   const int nX = p.dchunks;
   const int nFk = (kcur + 15) >> 4;
-  const int total1 = nX + nFk;
+  // Phase-2 A tiles start at F column kcur - koff: TMA box starts must be 16-byte
+  // aligned in the inner dimension, so for odd kcur one extra leading column is
+  // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
+  const int koff = kcur & 1;
+  const int nL = (p.columns_only || (p.dbg & 1)) ? 0 : (m + koff + 15) >> 4;
+  const int total = nX + nFk + nL;
 
-  for (int n = tid; n < NB; n += 256) {
-    if (n < m) {
-      const int ps = p.pos[n];
-      s_pos[n] = ps;
-      const double* rec = p.prop + (int64_t)ps * p.lay.rec;
-      s_idS[n] = rec[0];
-      s_sqnS[n] = rec[1];
-    } else {
-      s_pos[n] = -1;
-      s_idS[n] = -1.0;
-      s_sqnS[n] = 0.0;
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
     }
+    mbar_init(gready, NCW);
+    mbar_fence_init();
+  }
+  for (int n = tid; n < C::NB; n += C::NT) {
+    s_sqnS[n] = p.sqnS[n];
+    s_idS[n] = p.idS[n];
   }
   __syncthreads();
 
-  // ---- tile loaders ------------------------------------------------------
-  auto load_stage1 = [&](int stage, int kc) {
-    unsigned char* As = r1 + stage * C::STAGE;
-    unsigned char* Bs = As + C::A_BYTES;
-    const bool isx = kc < nX;
-    const int k0 = isx ? kc * 16 : (kc - nX) * 16;
-    for (int i = tid; i < BM * 8; i += 256) {
-      const int r = i >> 3, c16 = i & 7;
-      const int64_t grow = tile_row0 + r;
-      const void* src = p.X;
-      int bytes = 0;
-      if (grow < p.n_loc) {
-        if (isx) {
-          src = p.X + grow * p.ldx + k0 + 2 * c16;
-          bytes = 16;
+  if (warp == NCW) {  // ---------------- producer warp ----------------------
+    if (lane == 0) {
+      tma_prefetch_desc(&tmX);
+      tma_prefetch_desc(&tmXS);
+      tma_prefetch_desc(&tmF);
+      tma_prefetch_desc(&tmFS);
+      tma_prefetch_desc(&tmG);
+      tma_prefetch_desc(&tmL);
+      const int r0 = (int)tile_row0;
+      for (int c = 0; c < total; ++c) {
+        const int s = c % S;
+        if (c >= S) mbar_wait(&empty[s], ((c / S) & 1) ^ 1);
+        if (c == nX + nFk) mbar_wait(gready, 0);  // phase-2 A operand parked in F
+        unsigned char* As = stages + s * C::STAGE;
+        unsigned char* Bs = As + C::A_BYTES;
+        mbar_arrive_expect_tx(&full[s], C::STAGE);
+        if (c < nX) {
+          tma_load_2d(As, &tmX, 16 * c, r0, &full[s]);
+          tma_load_2d(Bs, &tmXS, 16 * c, 0, &full[s]);
+        } else if (c < nX + nFk) {
+          tma_load_2d(As, &tmF, 16 * (c - nX), r0, &full[s]);
+          tma_load_2d(Bs, &tmFS, 16 * (c - nX), 0, &full[s]);
         } else {
-          const int kk = k0 + 2 * c16;
-          bytes = max(0, min(16, (kcur - kk) * 8));
-          if (bytes) src = p.F + grow * p.ldf + kk;
+          tma_load_2d(As, &tmG, kcur - koff + 16 * (c - nX - nFk), r0, &full[s]);
+          tma_load_2d(Bs, &tmL, 16 * (c - nX - nFk), 0, &full[s]);
         }
       }
-      cp_async16(As + r * 128 + ((c16 ^ (r & 7)) << 4), src, bytes);
     }
-    for (int i = tid; i < NB * 8; i += 256) {
-      const int n = i >> 3, c16 = i & 7;
-      const void* src = p.X;
-      int bytes = 0;
-      if (n < m) {
-        const double* rec = p.prop + (int64_t)s_pos[n] * p.lay.rec;
-        if (isx) {
-          src = rec + p.lay.xoff + k0 + 2 * c16;
-          bytes = 16;
-        } else {
-          const int kk = k0 + 2 * c16;
-          bytes = max(0, min(16, (kcur - kk) * 8));
-          if (bytes) src = rec + p.lay.foff + kk;
-        }
-      }
-      cp_async16(Bs + n * 128 + ((c16 ^ (n & 7)) << 4), src, bytes);
-    }
-  };
-  auto load_stage2 = [&](int stage, int kc) {
-    unsigned char* Bs = r2 + stage * C::B_BYTES;
-    for (int i = tid; i < NB * 8; i += 256) {
-      const int n = i >> 3, c16 = i & 7;
-      cp_async16(Bs + n * 128 + ((c16 ^ (n & 7)) << 4), p.linv + (int64_t)n * p.ldl + kc * 16 + 2 * c16,
-                 16);
-    }
-  };
+    return;
+  }
+
+  // ------------------------------ consumer warps ------------------------------
+  const int g = lane >> 2, t = lane & 3;
+  const int wr = warp / WC, wc = warp % WC;
+  const int pg = perm8(g);
+  int arow[2];  // tile rows of this lane's A-fragment rows
+#pragma unroll
+  for (int fr = 0; fr < 2; ++fr) arow[fr] = wr * 16 + 8 * fr + pg;
 
   double acc[2][NFW][2];
 #pragma unroll
@@ -151,37 +142,44 @@ __global__ void __launch_bounds__(256, 1) update_kernel(UpdateParams p) {
 #pragma unroll
     for (int q = 0; q < NFW; ++q) acc[fr][q][0] = acc[fr][q][1] = 0.0;
 
-  const int ra0 = wr * 16 + 2 * g;  // rows of A fragments: ra0 + fr
+  // Swizzled byte offsets of this lane's fragment element (row & 7 == pg, k = 4s + t)
+  // inside any 8-row group: identical for the A and B operands, so every fragment
+  // load below is base + compile-time immediate + one of these four registers.
+  uint32_t foff[4];
+#pragma unroll
+  for (int s = 0; s < 4; ++s) foff[s] = swz_off(pg, 4 * s + t);
+  const uint32_t a_base = (uint32_t)(wr * 16) * 128u;
 
-  auto mma_tile = [&](const unsigned char* As, uint32_t a_block_off, const unsigned char* Bs) {
+  auto mma_stage = [&](const unsigned char* As, const unsigned char* Bs) {
+    const unsigned char* Aw = As + a_base;
+    const unsigned char* Bw = Bs + (uint32_t)(wc * NFW) * 1024u;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       double a[2];
 #pragma unroll
-      for (int fr = 0; fr < 2; ++fr) a[fr] = lds64(As, a_block_off + swz_off(ra0 + fr, 4 * s + t));
+      for (int fr = 0; fr < 2; ++fr) a[fr] = lds64(Aw + fr * 1024, foff[s]);
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
-        const int Q = wc * NFW + q;
-        const double bv = lds64(Bs, swz_off(colmap(Q, g, NF), 4 * s + t));
+        const double bv = lds64(Bw + q * 1024, foff[s]);
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[fr], bv);
       }
     }
   };
 
-  auto dist_tile = [&](const unsigned char* As, const unsigned char* Bs) {
+  auto dist_stage = [&](const unsigned char* As, const unsigned char* Bs) {
     const bool l1 = p.kind == kL1;
-#pragma unroll 2
+#pragma unroll 4
     for (int j = 0; j < 16; ++j) {
       double xr[2];
 #pragma unroll
-      for (int fr = 0; fr < 2; ++fr) xr[fr] = lds64(As, swz_off(ra0 + fr, j));
+      for (int fr = 0; fr < 2; ++fr) xr[fr] = lds64(As, swz_off(arow[fr], j));
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
         const int Q = wc * NFW + q;
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const double xs = lds64(Bs, swz_off(colmap(Q, 2 * t + v, NF), j));
+          const double xs = lds64(Bs, swz_off(8 * Q + perm8(2 * t + v), j));
 #pragma unroll
           for (int fr = 0; fr < 2; ++fr) {
             const double df = __dsub_rn(xr[fr], xs);
@@ -193,20 +191,19 @@ __global__ void __launch_bounds__(256, 1) update_kernel(UpdateParams p) {
     }
   };
 
-  auto transform = [&]() {
+  auto transform = [&]() {  // acc (Gram dot / distance) -> -A(R, S)
     const double sig2 = __dmul_rn(p.sigma, p.sigma);
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr) {
-      const int64_t grow = tile_row0 + ra0 + fr;
+      const int64_t grow = tile_row0 + arow[fr];
       const bool rin = grow < p.n_loc;
       const double sqr = rin ? p.sqn[grow] : 0.0;
       const double gid = (double)(p.row0 + grow);
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
-        const int Q = wc * NFW + q;
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int col = colmap(Q, 2 * t + v, NF);
+          const int col = 8 * (wc * NFW + q) + 2 * t + v;
           double val = 0.0;
           if (col < m && rin) {
             const double a = acc[fr][q][v];
@@ -228,116 +225,108 @@ __global__ void __launch_bounds__(256, 1) update_kernel(UpdateParams p) {
     }
   };
 
-  // ---- phase 1: kernel columns + residual GEMM ------------------------------
+  // ---- phase 1 ------------------------------------------------------------------
 #pragma unroll 1
-  for (int s = 0; s < C::S1 - 1; ++s) {
-    if (s < total1) load_stage1(s, s);
-    cp_async_commit();
-  }
-#pragma unroll 1
-  for (int c = 0; c < total1; ++c) {
-    cp_async_wait<C::S1 - 2>();
-    __syncthreads();
-    const int nxt = c + C::S1 - 1;
-    if (nxt < total1) load_stage1(nxt % C::S1, nxt);
-    cp_async_commit();
-    const unsigned char* As = r1 + (c % C::S1) * C::STAGE;
+  for (int c = 0; c < nX + nFk; ++c) {
+    const int s = c % S;
+    mbar_wait(&full[s], (c / S) & 1);
+    __syncwarp();
+    const unsigned char* As = stages + s * C::STAGE;
     const unsigned char* Bs = As + C::A_BYTES;
-    if (c >= nX || p.kind == kGaussGram) {
-      mma_tile(As, 0u, Bs);
-    } else {
-      dist_tile(As, Bs);
-    }
+    if (c >= nX || p.kind == kGaussGram) mma_stage(As, Bs);
+    else dist_stage(As, Bs);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
     if (c == nX - 1) transform();
   }
-  cp_async_wait<0>();
-  __syncthreads();
 
-  double* fin = reinterpret_cast<double*>(r1);
-  if (p.columns_only) {
-    // standalone K5: A(R, S) = -acc, column-major output (KernelOracle::columns)
+  if (p.columns_only) {  // standalone K5: A(R, S) -> column-major output
 #pragma unroll
-    for (int fr = 0; fr < 2; ++fr)
+    for (int fr = 0; fr < 2; ++fr) {
+      const int64_t grow = tile_row0 + arow[fr];
+      if (grow >= p.n_loc) continue;
 #pragma unroll
       for (int q = 0; q < NFW; ++q)
 #pragma unroll
-        for (int v = 0; v < 2; ++v)
-          fin[(ra0 + fr) * C::FIN_LD + colmap(wc * NFW + q, 2 * t + v, NF)] = -acc[fr][q][v];
-    __syncthreads();
-    for (int idx = tid; idx < BM * m; idx += 256) {
-      const int col = idx / BM, r = idx % BM;
-      const int64_t grow = tile_row0 + r;
-      if (grow < p.n_loc) p.cols_out[(int64_t)col * p.ld_out + grow] = fin[r * C::FIN_LD + col];
+        for (int v = 0; v < 2; ++v) {
+          const int col = 8 * (wc * NFW + q) + 2 * t + v;
+          if (col < m) p.cols_out[(int64_t)col * p.ld_out + grow] = -acc[fr][q][v];
+        }
     }
     return;
   }
 
-  // ---- phase 2: G <- G L^{-T} ------------------------------------------------
-  unsigned char* gt = r1;  // NBK/16 swizzled [BM][16] blocks holding G = -acc
+  // ---- park G = -acc in F(R, kcur:kcur+m) for phase 2 --------------------------
 #pragma unroll
-  for (int fr = 0; fr < 2; ++fr)
+  for (int fr = 0; fr < 2; ++fr) {
+    const int64_t grow = tile_row0 + arow[fr];
+    if (grow >= p.n_loc) continue;
+    double* frow = p.F + grow * p.ldf + kcur;
 #pragma unroll
     for (int q = 0; q < NFW; ++q)
 #pragma unroll
       for (int v = 0; v < 2; ++v) {
-        const int col = colmap(wc * NFW + q, 2 * t + v, NF);
-        *reinterpret_cast<double*>(gt + (col >> 4) * C::A_BYTES + swz_off(ra0 + fr, col & 15)) =
-            -acc[fr][q][v];
+        const int col = 8 * (wc * NFW + q) + 2 * t + v;
+        if (col < m) frow[col] = -acc[fr][q][v];
         acc[fr][q][v] = 0.0;
       }
-  if (NB != C::NBK) {  // zero the unused half of the last 16-column block
-    for (int i = tid; i < BM * 8; i += 256) {
-      const int r = i >> 3, k = 8 + (i & 7);
-      *reinterpret_cast<double*>(gt + (NB >> 4) * C::A_BYTES + swz_off(r, k)) = 0.0;
-    }
   }
-  __syncthreads();
-  const int nL = (m + 15) >> 4;
-#pragma unroll 1
-  for (int s = 0; s < C::S2 - 1; ++s) {
-    if (s < nL) load_stage2(s, s);
-    cp_async_commit();
+  if (!(p.dbg & 1)) {
+    fence_proxy_async_global();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(gready);
   }
-#pragma unroll 1
-  for (int c = 0; c < nL; ++c) {
-    cp_async_wait<C::S2 - 2>();
-    __syncthreads();
-    const int nxt = c + C::S2 - 1;
-    if (nxt < nL) load_stage2(nxt % C::S2, nxt);
-    cp_async_commit();
-    mma_tile(gt, (uint32_t)(c * C::A_BYTES), r2 + (c % C::S2) * C::B_BYTES);
-  }
-  cp_async_wait<0>();
-  __syncthreads();
 
-  // ---- epilogue: append columns to F, update the residual diagonal ----------
+  // ---- phase 2: G L^{-T} ------------------------------------------------------------
+#pragma unroll 1
+  for (int c = nX + nFk; c < total; ++c) {
+    const int s = c % S;
+    mbar_wait(&full[s], (c / S) & 1);
+    __syncwarp();
+    const unsigned char* As = stages + s * C::STAGE;
+    mma_stage(As, As + C::A_BYTES);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+
+  // ---- epilogue ------------------------------------------------------------------
+  double rs[2] = {0.0, 0.0};
 #pragma unroll
-  for (int fr = 0; fr < 2; ++fr)
+  for (int fr = 0; fr < 2; ++fr) {
+    const int64_t grow = tile_row0 + arow[fr];
+    const bool rin = grow < p.n_loc;
+    double* frow = p.F + grow * p.ldf + kcur;
 #pragma unroll
     for (int q = 0; q < NFW; ++q)
 #pragma unroll
-      for (int v = 0; v < 2; ++v)
-        fin[(ra0 + fr) * C::FIN_LD + colmap(wc * NFW + q, 2 * t + v, NF)] = acc[fr][q][v];
-  __syncthreads();
-  for (int r = warp; r < BM; r += 8) {
-    const int64_t grow = tile_row0 + r;
-    double s2 = 0.0;
-    if (grow < p.n_loc) {
-      double* frow = p.F + grow * p.ldf + kcur;
-      for (int col = lane; col < m; col += 32) {
-        const double v = fin[r * C::FIN_LD + col];
-        frow[col] = v;
-        s2 = fma(v, v, s2);
+      for (int v = 0; v < 2; ++v) {
+        const int col = 8 * (wc * NFW + q) + 2 * t + v;
+        if (col < m && rin) {
+          const double val = acc[fr][q][v];
+          frow[col] = val;
+          rs[fr] = fma(val, val, rs[fr]);
+        }
       }
-      s2 = warp_sum_xor(s2);
-      if (lane == 0) {
-        const double un = __dsub_rn(p.u[grow], s2);
-        p.u[grow] = un < 0.0 ? 0.0 : un;
-      }
-    }
-    if (lane == 0) s_rowg2[r] = grow < p.n_loc ? s2 : 0.0;
+    rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 1);
+    rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 2);
+    if (t == 0) s_rown[wc * BM + arow[fr]] = rs[fr];
   }
-  __syncthreads();
+  if (p.dbg & 2) return;
+  named_bar_sync(1, 32 * NCW);
+  if (tid < BM) {
+    const int64_t grow = tile_row0 + tid;
+    double s2 = 0.0;
+#pragma unroll
+    for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + tid]);
+    if (grow < p.n_loc) {
+      const double un = __dsub_rn(p.u[grow], s2);
+      p.u[grow] = un < 0.0 ? 0.0 : un;
+    } else {
+      s2 = 0.0;
+    }
+    s_rowg2[tid] = s2;
+  }
+  named_bar_sync(1, 32 * NCW);
   if (tid == 0) {
     double s = 0.0;
     for (int r = 0; r < BM; ++r) s = __dadd_rn(s, s_rowg2[r]);
@@ -345,20 +334,63 @@ __global__ void __launch_bounds__(256, 1) update_kernel(UpdateParams p) {
   }
 }
 
-template <int WC, int NFW>
+// ---------------------------------------------------------------------------
+// host side: tensor maps + dispatch
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// [rows][ld] row-major fp64, inner extent `inner` elements, box {16, box_rows}, 128B swizzle
+static bool make_map(CUtensorMap* m, const double* base, uint64_t inner, uint64_t rows,
+                     uint64_t ld, uint32_t box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {std::max<uint64_t>(inner, 1), std::max<uint64_t>(rows, 1)};
+  cuuint64_t strides[1] = {ld * sizeof(double)};
+  cuuint32_t box[2] = {16, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides,
+                  box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int NCW, int WC, int NFW>
 static int launch_t(const UpdateParams& p, cudaStream_t st) {
-  using C = UCfg<WC, NFW>;
+  using C = UCfg<NCW, WC, NFW>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(update_kernel<WC, NFW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         C::SMEM);
+    if (cudaFuncSetAttribute(update_kernel<NCW, WC, NFW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             C::SMEM) != cudaSuccess)
+      return -2;
     attr = true;
   }
+  CUtensorMap mX, mXS, mF, mFS, mG, mL;
+  bool ok = make_map(&mX, p.X, p.dpad, p.n_loc, p.dpad, C::BM) &&
+            make_map(&mXS, p.xs, p.dpad, C::NB, p.dpad, C::NB) &&
+            make_map(&mF, p.F, p.kcur, p.n_loc, p.ldf, C::BM) &&
+            make_map(&mFS, p.fs, p.kcur, C::NB, p.ldfs, C::NB) &&
+            make_map(&mG, p.F, p.kcur + p.m, p.n_loc, p.ldf, C::BM) &&
+            make_map(&mL, p.linv, p.ldl, C::NB, p.ldl, C::NB);
+  if (!ok) return -3;
   const unsigned grid = (unsigned)((p.n_loc + C::BM - 1) / C::BM);
-  if (grid) update_kernel<WC, NFW><<<grid, 256, C::SMEM, st>>>(p);
+  if (grid) update_kernel<NCW, WC, NFW><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
   return C::BM;
 }
 
+// 8 consumer warps + 1 TMA producer warp.  m <= 128: one warp column (BM = 128,
+// warp tile 16 x NB); m <= 256: two warp columns (BM = 64).
 int update_tile_rows(int m) {
   const int nf = (m + 7) / 8;
   if (nf <= 16) return 128;
@@ -368,27 +400,61 @@ int update_tile_rows(int m) {
 
 int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
-#define RPCB_CASE1(N) \
-  case N:             \
-    return launch_t<1, N>(p, st);
-#define RPCB_CASE2(N) \
-  case N:             \
-    return launch_t<2, N>(p, st);
+#define RPCB_CASE(W, N) \
+  case N:               \
+    return launch_t<8, W, N>(p, st);
   if (nf <= 16) {
     switch (nf) {
-      RPCB_CASE1(1) RPCB_CASE1(2) RPCB_CASE1(3) RPCB_CASE1(4) RPCB_CASE1(5) RPCB_CASE1(6)
-      RPCB_CASE1(7) RPCB_CASE1(8) RPCB_CASE1(9) RPCB_CASE1(10) RPCB_CASE1(11) RPCB_CASE1(12)
-      RPCB_CASE1(13) RPCB_CASE1(14) RPCB_CASE1(15) RPCB_CASE1(16)
+      RPCB_CASE(1, 1) RPCB_CASE(1, 2) RPCB_CASE(1, 3) RPCB_CASE(1, 4) RPCB_CASE(1, 5)
+      RPCB_CASE(1, 6) RPCB_CASE(1, 7) RPCB_CASE(1, 8) RPCB_CASE(1, 9) RPCB_CASE(1, 10)
+      RPCB_CASE(1, 11) RPCB_CASE(1, 12) RPCB_CASE(1, 13) RPCB_CASE(1, 14) RPCB_CASE(1, 15)
+      RPCB_CASE(1, 16)
     }
   } else if (nf <= 32) {
     switch ((nf + 1) / 2) {
-      RPCB_CASE2(9) RPCB_CASE2(10) RPCB_CASE2(11) RPCB_CASE2(12) RPCB_CASE2(13)
-      RPCB_CASE2(14) RPCB_CASE2(15) RPCB_CASE2(16)
+      RPCB_CASE(2, 9) RPCB_CASE(2, 10) RPCB_CASE(2, 11) RPCB_CASE(2, 12)
+      RPCB_CASE(2, 13) RPCB_CASE(2, 14) RPCB_CASE(2, 15) RPCB_CASE(2, 16)
     }
   }
-#undef RPCB_CASE1
-#undef RPCB_CASE2
+#undef RPCB_CASE
   return -1;
+}
+
+// Accepted-pivot operands for the update: rows stored at perm_row(n) of
+// [256][ld] buffers (zero rows beyond m, zero columns [kcur, round16(kcur))).
+__global__ void gather_accepted_kernel(const double* __restrict__ prop, RecordLayout lay,
+                                       const int* __restrict__ pos, int m, int kcur, int kpad,
+                                       int dpad, double* __restrict__ xs, double* __restrict__ fs,
+                                       int64_t ldfs, double* __restrict__ sqnS,
+                                       double* __restrict__ idS) {
+  const int n = blockIdx.x;
+  const int dst = perm_row(n);
+  double* xr = xs + (int64_t)dst * dpad;
+  double* fr = fs + (int64_t)dst * ldfs;
+  if (n < m) {
+    const double* rec = prop + (int64_t)pos[n] * lay.rec;
+    for (int i = threadIdx.x; i < dpad; i += blockDim.x) xr[i] = rec[lay.xoff + i];
+    for (int k = threadIdx.x; k < kpad; k += blockDim.x) fr[k] = k < kcur ? rec[lay.foff + k] : 0.0;
+    if (threadIdx.x == 0) {
+      sqnS[n] = rec[1];
+      idS[n] = rec[0];
+    }
+  } else {
+    for (int i = threadIdx.x; i < dpad; i += blockDim.x) xr[i] = 0.0;
+    for (int k = threadIdx.x; k < kpad; k += blockDim.x) fr[k] = 0.0;
+    if (threadIdx.x == 0) {
+      sqnS[n] = 0.0;
+      idS[n] = -1.0;
+    }
+  }
+}
+
+void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,
+                            int kcur, int dpad, double* xs, double* fs, int64_t ldfs,
+                            double* sqnS, double* idS, cudaStream_t st) {
+  const int kpad = std::min<int64_t>(ldfs, ((kcur + 15) / 16) * 16);
+  gather_accepted_kernel<<<nb, 256, 0, st>>>(prop, lay, pos, m, kcur, kpad, dpad, xs, fs, ldfs,
+                                             sqnS, idS);
 }
 
 }  // namespace rpcb
