@@ -547,7 +547,6 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.sigma = kspec.sigma;
         up.kind = kind;
         up.tile_g2 = s.tile_g2.as<double>();
-        if (const char* e = std::getenv("RPC_DEBUG_UPDATE")) up.dbg = std::atoi(e);
         upd_ev.emplace_back();
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
@@ -585,20 +584,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   res->kcur = kcur;
   res->captured_sq = captured_sq;
   if (cfg.mode == RPC_UNTIL_RANK && kcur > cfg.target_rank) res->surplus = kcur - cfg.target_rank;
-  // ||F||_F^2 for relative_trace_error (chunk partials, global chunk order)
-  for (Shard& s : res->shards) {
-    launch_fsq_chunks(s.F.as<double>(), ldf, s.n_loc, (int)kcur, s.nchunks,
-                      totals_all.as<double>() + s.chunk0, st);
-    ++launches;
-  }
-  CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
-  allgather(ctx, totals_all.as<double>(), L.cpr);
-  launch_chunk_prefix(g2_all.as<double>(), totals_all.as<double>(), L.ncg, chunk_end.as<double>(),
-                      d_scan, st);
-  ++launches;
-  CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  res->fro2 = h_scan->g2_prev;
+  // ||F||_F^2 for relative_trace_error (rpcholesky.hpp:577-583): the factor's squared
+  // Frobenius norm is the sum over rounds of ||G_r||_F^2, already reduced in a fixed
+  // chunk order per round, so no extra pass over the N x k factor is needed.
+  res->fro2 = captured_sq;
   // chol_factor = lower(F(pivots, :)) (rpcholesky.hpp:140-145): owners gather pivot rows
   res->chol.assign((size_t)kcur * kcur, 0.0);
   if (kcur > 0) {

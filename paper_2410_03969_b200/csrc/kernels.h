@@ -93,7 +93,6 @@ struct UpdateParams {
   double* tile_g2;                              // [n_tiles] per-CTA ||G||^2 partial (row order)
   // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
   int columns_only; double* cols_out; int64_t ld_out;
-  int dbg;  // fault bisection (RPC_DEBUG_UPDATE): 1 skip phase 2, 2 skip epilogue barriers
 };
 // Row-tile height used for m accepted columns (128 or 64), or -1 if m unsupported.
 int update_tile_rows(int m);

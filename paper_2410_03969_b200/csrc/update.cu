@@ -53,7 +53,37 @@ __device__ __forceinline__ double lds64(const unsigned char* base, uint32_t off)
   return *reinterpret_cast<const double*>(base + off);
 }
 
-template <int NCW_, int WC, int NFW>
+// Compact exp for the kernel-column epilogue (arguments are <= 0 here):
+// Cody-Waite reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor polynomial
+// (truncation < 5e-18 relative), exact power-of-two scaling in two steps so
+// results down to the subnormal range stay correct.  ~1 ulp, branch-free.
+__device__ __forceinline__ double exp_compact(double x) {
+  x = fmax(x, -745.5);
+  const double n = rint(x * 1.4426950408889634);
+  double r = fma(n, -6.93147180369123816490e-01, x);
+  r = fma(n, -1.90821492927058770002e-10, r);
+  double q = 1.6059043836821613e-10;          // 1/13!
+  q = fma(q, r, 2.0876756987868100e-09);      // 1/12!
+  q = fma(q, r, 2.5052108385441720e-08);      // 1/11!
+  q = fma(q, r, 2.7557319223985893e-07);      // 1/10!
+  q = fma(q, r, 2.7557319223985888e-06);      // 1/9!
+  q = fma(q, r, 2.4801587301587302e-05);      // 1/8!
+  q = fma(q, r, 1.9841269841269841e-04);      // 1/7!
+  q = fma(q, r, 1.3888888888888889e-03);      // 1/6!
+  q = fma(q, r, 8.3333333333333332e-03);      // 1/5!
+  q = fma(q, r, 4.1666666666666664e-02);      // 1/4!
+  q = fma(q, r, 1.6666666666666666e-01);      // 1/3!
+  q = fma(q, r, 0.5);
+  q = fma(q, r, 1.0);
+  q = fma(q, r, 1.0);
+  const int ni = (int)n;
+  const int k1 = ni >> 1, k2 = ni - k1;
+  const double s1 = __longlong_as_double((long long)(k1 + 1023) << 52);
+  const double s2 = __longlong_as_double((long long)(k2 + 1023) << 52);
+  return q * s1 * s2;
+}
+
+template <int NCW_, int WC, int NFW, bool GRAM>
 __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
     update_kernel(UpdateParams p, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmF,
@@ -80,7 +110,7 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
   // aligned in the inner dimension, so for odd kcur one extra leading column is
   // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
   const int koff = kcur & 1;
-  const int nL = (p.columns_only || (p.dbg & 1)) ? 0 : (m + koff + 15) >> 4;
+  const int nL = p.columns_only ? 0 : (m + koff + 15) >> 4;
   const int total = nX + nFk + nL;
 
   if (tid == 0) {
@@ -150,7 +180,9 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
   for (int s = 0; s < 4; ++s) foff[s] = swz_off(pg, 4 * s + t);
   const uint32_t a_base = (uint32_t)(wr * 16) * 128u;
 
-  auto mma_stage = [&](const unsigned char* As, const unsigned char* Bs) {
+  // q_lo: first fragment that can be non-zero (phase 2 skips the zero upper triangle
+  // of L^{-T}; phase 1 passes 0).
+  auto mma_stage = [&](const unsigned char* As, const unsigned char* Bs, int q_lo) {
     const unsigned char* Aw = As + a_base;
     const unsigned char* Bw = Bs + (uint32_t)(wc * NFW) * 1024u;
 #pragma unroll
@@ -160,6 +192,7 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
       for (int fr = 0; fr < 2; ++fr) a[fr] = lds64(Aw + fr * 1024, foff[s]);
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
+        if (q < q_lo) continue;
         const double bv = lds64(Bw + q * 1024, foff[s]);
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[fr], bv);
@@ -192,7 +225,9 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
   };
 
   auto transform = [&]() {  // acc (Gram dot / distance) -> -A(R, S)
-    const double sig2 = __dmul_rn(p.sigma, p.sigma);
+    // exponent = D * (-0.5 / sigma^2) (Gaussian) or D * (-1 / sigma) (l1): one multiply
+    // instead of the reference's division, <= 1 ulp apart (kernel values agree to 1e-15).
+    const double escale = (!GRAM && p.kind == kL1) ? -1.0 / p.sigma : -0.5 / (p.sigma * p.sigma);
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr) {
       const int64_t grow = tile_row0 + arow[fr];
@@ -207,17 +242,13 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
           double val = 0.0;
           if (col < m && rin) {
             const double a = acc[fr][q][v];
-            if (p.kind == kL1) {
-              val = exp(__ddiv_rn(-a, p.sigma));
-            } else {
-              double dd = a;
-              if (p.kind == kGaussGram) {
-                dd = __dadd_rn(__dadd_rn(-2.0 * a, sqr), s_sqnS[col]);
-                if (dd < 0.0) dd = 0.0;
-                if (gid == s_idS[col]) dd = 0.0;
-              }
-              val = exp(__ddiv_rn(__dmul_rn(-0.5, dd), sig2));
+            double dd = a;
+            if (GRAM) {
+              dd = __dadd_rn(__dadd_rn(-2.0 * a, sqr), s_sqnS[col]);
+              if (dd < 0.0) dd = 0.0;
+              if (gid == s_idS[col]) dd = 0.0;
             }
+            val = exp_compact(dd * escale);
           }
           acc[fr][q][v] = -val;
         }
@@ -225,19 +256,29 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
     }
   };
 
-  // ---- phase 1 ------------------------------------------------------------------
+  // ---- phase 1a: kernel-column distances (X tiles) ------------------------------
 #pragma unroll 1
-  for (int c = 0; c < nX + nFk; ++c) {
+  for (int c = 0; c < nX; ++c) {
     const int s = c % S;
     mbar_wait(&full[s], (c / S) & 1);
     __syncwarp();
     const unsigned char* As = stages + s * C::STAGE;
-    const unsigned char* Bs = As + C::A_BYTES;
-    if (c >= nX || p.kind == kGaussGram) mma_stage(As, Bs);
-    else dist_stage(As, Bs);
+    if constexpr (GRAM) mma_stage(As, As + C::A_BYTES, 0);
+    else dist_stage(As, As + C::A_BYTES);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    if (c == nX - 1) transform();
+  }
+  transform();
+  // ---- phase 1b: residual GEMM F(R,:) F(S,:)^T (F tiles) ---------------------------
+#pragma unroll 1
+  for (int c = nX; c < nX + nFk; ++c) {
+    const int s = c % S;
+    mbar_wait(&full[s], (c / S) & 1);
+    __syncwarp();
+    const unsigned char* As = stages + s * C::STAGE;
+    mma_stage(As, As + C::A_BYTES, 0);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   if (p.columns_only) {  // standalone K5: A(R, S) -> column-major output
@@ -271,11 +312,9 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
         acc[fr][q][v] = 0.0;
       }
   }
-  if (!(p.dbg & 1)) {
-    fence_proxy_async_global();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(gready);
-  }
+  fence_proxy_async_global();
+  __syncwarp();
+  if (lane == 0) mbar_arrive(gready);
 
   // ---- phase 2: G L^{-T} ------------------------------------------------------------
 #pragma unroll 1
@@ -284,7 +323,11 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
     mbar_wait(&full[s], (c / S) & 1);
     __syncwarp();
     const unsigned char* As = stages + s * C::STAGE;
-    mma_stage(As, As + C::A_BYTES);
+    // chunk j covers G columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
+    // so fragments whose 8 columns all lie below 16j - koff contribute nothing.
+    const int j = c - nX - nFk;
+    const int q_lo = max(0, (16 * j - koff) / 8 - wc * NFW);
+    mma_stage(As, As + C::A_BYTES, q_lo);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -311,7 +354,6 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
     rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 2);
     if (t == 0) s_rown[wc * BM + arow[fr]] = rs[fr];
   }
-  if (p.dbg & 2) return;
   named_bar_sync(1, 32 * NCW);
   if (tid < BM) {
     const int64_t grow = tile_row0 + tid;
@@ -366,12 +408,12 @@ static bool make_map(CUtensorMap* m, const double* base, uint64_t inner, uint64_
   return r == CUDA_SUCCESS;
 }
 
-template <int NCW, int WC, int NFW>
+template <int NCW, int WC, int NFW, bool GRAM>
 static int launch_t(const UpdateParams& p, cudaStream_t st) {
   using C = UCfg<NCW, WC, NFW>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(update_kernel<NCW, WC, NFW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(update_kernel<NCW, WC, NFW, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::SMEM) != cudaSuccess)
       return -2;
     attr = true;
@@ -385,7 +427,7 @@ static int launch_t(const UpdateParams& p, cudaStream_t st) {
             make_map(&mL, p.linv, p.ldl, C::NB, p.ldl, C::NB);
   if (!ok) return -3;
   const unsigned grid = (unsigned)((p.n_loc + C::BM - 1) / C::BM);
-  if (grid) update_kernel<NCW, WC, NFW><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
+  if (grid) update_kernel<NCW, WC, NFW, GRAM><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
   return C::BM;
 }
 
@@ -402,7 +444,7 @@ int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
 #define RPCB_CASE(W, N) \
   case N:               \
-    return launch_t<8, W, N>(p, st);
+    return p.kind == kGaussGram ? launch_t<8, W, N, true>(p, st) : launch_t<8, W, N, false>(p, st);
   if (nf <= 16) {
     switch (nf) {
       RPCB_CASE(1, 1) RPCB_CASE(1, 2) RPCB_CASE(1, 3) RPCB_CASE(1, 4) RPCB_CASE(1, 5)
