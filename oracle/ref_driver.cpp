@@ -1,0 +1,201 @@
+// ref_driver.cpp — C entry points around the REFERENCE's own headers
+// (/root/reference/proj/include/rpchol, compiled where they lie against the
+// Eigen-API shim in oracle/eigen_shim).  TEST INFRASTRUCTURE ONLY: it produces
+// oracle/_ref/libref_rpchol.so, used by tests/ to pin the C restatement
+// (oracle/rpc_oracle.c) against the reference's actual control flow and
+// arithmetic, and by bench.py's --impl reference arm.  No reference source is
+// copied into this repository.
+#include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rpchol/rpcholesky.hpp"
+
+namespace {
+thread_local std::string g_err;
+
+int code_of(const std::exception& e) {
+  if (dynamic_cast<const std::invalid_argument*>(&e)) return 1;
+  if (dynamic_cast<const std::out_of_range*>(&e)) return 2;
+  return 3;
+}
+
+// Same layout as rpo_result (oracle/rpc_oracle.h) so the Python binding is shared.
+struct Res {
+  int64_t n, rank;
+  double* factor;
+  int64_t* pivots;
+  double* chol;
+  double* residual_diag;
+  int64_t n_rounds, block_size;
+  int64_t* proposed;
+  int64_t* accepted_count;
+  int rank_exhausted;
+  int64_t surplus;
+  double captured_sq;
+};
+
+template <class T>
+T* dup(const T* src, size_t n) {
+  T* p = static_cast<T*>(std::malloc(sizeof(T) * (n ? n : 1)));
+  if (n) std::memcpy(p, src, sizeof(T) * n);
+  return p;
+}
+
+rpchol::RunConfig make_cfg(int64_t b, int mode, int64_t rounds, int64_t k, uint64_t seed,
+                           double stop_tol) {
+  rpchol::RunConfig cfg = mode == 0 ? rpchol::RunConfig::fixed_rounds(rounds, b, seed)
+                                    : rpchol::RunConfig::until_rank(k, b, seed);
+  cfg.stop_tol = stop_tol;
+  return cfg;
+}
+
+void fill(const rpchol::CholeskyResult& r, Res* out, int64_t b) {
+  const auto& f = r.approx.factor;
+  out->n = f.rows();
+  out->rank = f.cols();
+  out->factor = dup(f.data(), (size_t)(f.rows() * f.cols()));
+  std::vector<int64_t> piv(r.approx.pivots.begin(), r.approx.pivots.end());
+  out->pivots = dup(piv.data(), piv.size());
+  out->chol = dup(r.approx.chol_factor.data(),
+                  (size_t)(r.approx.chol_factor.rows() * r.approx.chol_factor.cols()));
+  out->residual_diag = dup(r.residual_diag.data(), (size_t)r.residual_diag.size());
+  out->n_rounds = (int64_t)r.trace.rounds.size();
+  out->block_size = b;
+  std::vector<int64_t> prop, cnt;
+  for (const auto& rr : r.trace.rounds) {
+    prop.insert(prop.end(), rr.proposed.begin(), rr.proposed.end());
+    cnt.push_back((int64_t)rr.accepted.size());
+  }
+  out->proposed = dup(prop.data(), prop.size());
+  out->accepted_count = dup(cnt.data(), cnt.size());
+  out->rank_exhausted = r.trace.rank_exhausted ? 1 : 0;
+  out->surplus = r.trace.surplus;
+  out->captured_sq = 0.0;
+}
+
+rpchol::KernelOracle make_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma,
+                                 int dist) {
+  Eigen::MatrixXd pts(n, d);
+  std::memcpy(pts.data(), x, sizeof(double) * (size_t)(n * d));
+  rpchol::KernelSpec spec(kind == 0 ? rpchol::KernelKind::Gaussian : rpchol::KernelKind::L1Laplace,
+                          sigma);
+  return rpchol::KernelOracle(rpchol::DataMatrix(std::move(pts)), spec,
+                              dist == 1 ? rpchol::DistanceMode::GramTrick
+                                        : rpchol::DistanceMode::Direct);
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error() { return g_err.c_str(); }
+
+// x: n x d column-major.  dist: 0 direct, 1 gram.
+int ref_accelerated_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                           int64_t b, int mode, int64_t rounds, int64_t k, uint64_t seed,
+                           double stop_tol, Res* out) {
+  try {
+    auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+    auto res = rpchol::accelerated_rpcholesky(oracle, make_cfg(b, mode, rounds, k, seed, stop_tol));
+    fill(res, out, b);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+int ref_accelerated_dense(const double* a, int64_t n, int64_t b, int mode, int64_t rounds,
+                          int64_t k, uint64_t seed, double stop_tol, Res* out) {
+  try {
+    Eigen::MatrixXd m(n, n);
+    std::memcpy(m.data(), a, sizeof(double) * (size_t)(n * n));
+    rpchol::DenseOracle oracle(std::move(m));
+    auto res = rpchol::accelerated_rpcholesky(oracle, make_cfg(b, mode, rounds, k, seed, stop_tol));
+    fill(res, out, b);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+double ref_relative_trace_error_kernel(const double* x, int64_t n, int64_t d, int kind,
+                                       double sigma, int dist, const double* factor, int64_t k) {
+  auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+  rpchol::LowRankApprox approx;
+  approx.factor.resize(n, k);
+  std::memcpy(approx.factor.data(), factor, sizeof(double) * (size_t)(n * k));
+  return rpchol::relative_trace_error(oracle, approx);
+}
+
+int ref_kernel_submatrix(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                         const int64_t* rows, int64_t nr, const int64_t* cols, int64_t nc,
+                         double* out) {
+  try {
+    auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+    std::vector<Eigen::Index> r(rows, rows + nr), c(cols, cols + nc);
+    Eigen::MatrixXd m = oracle.submatrix(r, c);
+    std::memcpy(out, m.data(), sizeof(double) * (size_t)(nr * nc));
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+int ref_sample_discrete(const double* w, int64_t n, uint64_t seed, uint64_t draw0, int64_t count,
+                        int64_t* out) {
+  try {
+    Eigen::VectorXd wv(n);
+    std::memcpy(wv.data(), w, sizeof(double) * (size_t)n);
+    const Eigen::VectorXd cs = rpchol::cumulative_sums(wv);
+    rpchol::SplitMix64 rng(seed);
+    for (uint64_t t = 0; t < draw0; ++t) rng.next_u64();
+    for (int64_t j = 0; j < count; ++j) out[j] = rpchol::sample_discrete(cs, rng);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+int ref_rejection_sweep(const double* h, int64_t b, const int64_t* proposals, uint64_t seed,
+                        uint64_t draw0, int64_t* accepted, int64_t* positions, int64_t* m_out,
+                        double* chol) {
+  try {
+    Eigen::MatrixXd hm(b, b);
+    std::memcpy(hm.data(), h, sizeof(double) * (size_t)(b * b));
+    std::vector<Eigen::Index> prop(proposals, proposals + b);
+    rpchol::SplitMix64 rng(seed);
+    for (uint64_t t = 0; t < draw0; ++t) rng.next_u64();
+    auto sel = rpchol::rejection_sample_submatrix(std::move(hm), prop, rng);
+    const int64_t m = (int64_t)sel.accepted.size();
+    for (int64_t i = 0; i < m; ++i) {
+      accepted[i] = sel.accepted[(size_t)i];
+      positions[i] = sel.positions[(size_t)i];
+    }
+    std::memcpy(chol, sel.chol_factor.data(), sizeof(double) * (size_t)(m * m));
+    *m_out = m;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+void ref_result_free(Res* r) {
+  std::free(r->factor);
+  std::free(r->pivots);
+  std::free(r->chol);
+  std::free(r->residual_diag);
+  std::free(r->proposed);
+  std::free(r->accepted_count);
+  std::memset(r, 0, sizeof *r);
+}
+
+}  // extern "C"
