@@ -97,26 +97,46 @@ void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* t
   if (n_chunks > 0) chunk_totals_kernel<<<n_chunks, kScanThreads, 0, st>>>(u, n_loc, totals);
 }
 
-__global__ void chunk_prefix_kernel(const double* __restrict__ totals, const double* g2_all,
-                                    int n_chunks, double* __restrict__ chunk_end,
-                                    ScanStatus* status) {
-  if (threadIdx.x != 0) return;
-  double off = 0.0;
-  for (int c = 0; c < n_chunks; ++c) {
-    off = __dadd_rn(off, totals[c]);
-    chunk_end[c] = off;
+// Serial chunk-offset chain (fixed order => p-invariant).  The totals are first staged
+// in shared memory by the whole CTA so the single-thread chain never waits on HBM.
+__global__ void __launch_bounds__(1024) chunk_prefix_kernel(const double* __restrict__ totals,
+                                                            const double* g2_all, int n_chunks,
+                                                            double* __restrict__ chunk_end,
+                                                            ScanStatus* status) {
+  extern __shared__ double st[];  // [n_chunks] totals, [n_chunks] g2 partials
+  double* sg = st + n_chunks;
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
+    st[c] = totals[c];
+    sg[c] = g2_all ? g2_all[c] : 0.0;
   }
-  double g2 = 0.0;
-  if (g2_all)
-    for (int c = 0; c < n_chunks; ++c) g2 = __dadd_rn(g2, g2_all[c]);
-  status->total = off;
-  status->g2_prev = g2;
-  status->exhausted = !(off > 0.0);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double off = 0.0, g2 = 0.0;
+    for (int c = 0; c < n_chunks; ++c) {
+      off = __dadd_rn(off, st[c]);
+      st[c] = off;
+      g2 = __dadd_rn(g2, sg[c]);
+    }
+    status->total = off;
+    status->g2_prev = g2;
+    status->exhausted = !(off > 0.0);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) chunk_end[c] = st[c];
 }
 
 void launch_chunk_prefix(const double* totals_all, const double* g2_all, int n_chunks,
                          double* chunk_end, ScanStatus* status, cudaStream_t st) {
-  chunk_prefix_kernel<<<1, 32, 0, st>>>(totals_all, g2_all, n_chunks, chunk_end, status);
+  const size_t smem = sizeof(double) * 2 * (size_t)n_chunks;
+  if (smem > 48 * 1024) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(chunk_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      attr = true;
+    }
+  }
+  chunk_prefix_kernel<<<1, 1024, smem, st>>>(totals_all, g2_all, n_chunks, chunk_end, status);
 }
 
 // Copies the sampled point's record (id, ||x||^2, x, F row) into rec.
@@ -345,32 +365,63 @@ void launch_f_to_colmajor(const double* F, int64_t ldf, int64_t n_loc, int c0, i
 
 // src: this shard's rows, either row-major [n_loc][ld_src] or column-major
 // [d][ld_src].  Output padded row-major X and ||x||^2 in ascending coordinate
-// order without FMA contraction (oracle.hpp:252).
-__global__ void pack_points_kernel(const double* __restrict__ src, int64_t n_loc, int d,
-                                   int64_t ld_src, int src_row_major, int64_t dpad,
-                                   double* __restrict__ X, double* __restrict__ sqn,
-                                   int* nonfinite) {
-  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= n_loc) return;
-  double s = 0.0;
+// order without FMA contraction (oracle.hpp:252).  A CTA stages kPackRows rows
+// through shared memory so both the read and the padded write are coalesced.
+constexpr int kPackRows = 64;
+__global__ void __launch_bounds__(256) pack_points_kernel(const double* __restrict__ src,
+                                                          int64_t n_loc, int d, int64_t ld_src,
+                                                          int src_row_major, int64_t dpad,
+                                                          double* __restrict__ X,
+                                                          double* __restrict__ sqn,
+                                                          int* nonfinite) {
+  extern __shared__ double tile[];  // [kPackRows][dpad]
+  const int64_t r0 = (int64_t)blockIdx.x * kPackRows;
+  const int nr = (int)lmin(kPackRows, n_loc - r0);
+  const int tid = threadIdx.x;
   bool bad = false;
-  for (int c = 0; c < dpad; ++c) {
-    double v = 0.0;
-    if (c < d) v = src_row_major ? src[r * ld_src + c] : src[(int64_t)c * ld_src + r];
-    bad |= !isfinite(v);
-    X[r * dpad + c] = v;
-    if (c < d) s = __dadd_rn(s, __dmul_rn(v, v));
+  if (src_row_major) {
+    for (int i = tid; i < nr * (int)dpad; i += blockDim.x) {
+      const int r = i / (int)dpad, c = i % (int)dpad;
+      double v = 0.0;
+      if (c < d) v = src[(r0 + r) * ld_src + c];
+      bad |= !isfinite(v);
+      tile[i] = v;
+    }
+  } else {
+    for (int i = tid; i < nr * (int)dpad; i += blockDim.x) {
+      const int c = i / nr, r = i % nr;
+      double v = 0.0;
+      if (c < d) v = src[(int64_t)c * ld_src + r0 + r];
+      bad |= !isfinite(v);
+      tile[r * dpad + c] = v;
+    }
   }
-  sqn[r] = s;
+  __syncthreads();
+  for (int i = tid; i < nr * (int)dpad; i += blockDim.x) X[r0 * dpad + i] = tile[i];
+  if (tid < nr) {
+    double s = 0.0;
+    for (int c = 0; c < d; ++c) {
+      const double v = tile[tid * dpad + c];
+      s = __dadd_rn(s, __dmul_rn(v, v));
+    }
+    sqn[r0 + tid] = s;
+  }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
 }
 
 void launch_pack_points(const double* src, int64_t n_loc, int d, int64_t ld_src,
                         int src_row_major, int64_t dpad, double* X, double* sqn,
                         int* nonfinite, cudaStream_t st) {
-  if (n_loc > 0)
-    pack_points_kernel<<<(unsigned)((n_loc + 255) / 256), 256, 0, st>>>(
-        src, n_loc, d, ld_src, src_row_major, dpad, X, sqn, nonfinite);
+  if (n_loc <= 0) return;
+  const size_t smem = sizeof(double) * kPackRows * (size_t)dpad;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(pack_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    attr = true;
+  }
+  pack_points_kernel<<<(unsigned)((n_loc + kPackRows - 1) / kPackRows), 256, smem, st>>>(
+      src, n_loc, d, ld_src, src_row_major, dpad, X, sqn, nonfinite);
 }
 
 __global__ void fill_kernel(double* p, int64_t n, double v) {

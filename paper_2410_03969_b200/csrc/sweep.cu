@@ -48,22 +48,23 @@ __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ 
                                                      RecordLayout lay, int b, int d, int kcur,
                                                      int kind, double sigma,
                                                      double* __restrict__ H) {
-  __shared__ double sp[16][33];
-  __shared__ double sq[16][33];
+  __shared__ double sp[16][129];
+  __shared__ double sq[16][129];
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
   const int p = blockIdx.y * 16 + ty, q = blockIdx.x * 16 + tx;
   double acc = 0.0;
-  for (int k0 = 0; k0 < kcur; k0 += 32) {
-    for (int i = tid; i < 16 * 32; i += 256) {
-      const int rr = i >> 5, kk = i & 31;
+  for (int k0 = 0; k0 < kcur; k0 += 128) {
+    for (int i = tid; i < 16 * 128; i += 256) {
+      const int rr = i >> 7, kk = i & 127;
       const int pp = blockIdx.y * 16 + rr, qq = blockIdx.x * 16 + rr;
       const bool kin = k0 + kk < kcur;
       sp[rr][kk] = (pp < b && kin) ? prop[(int64_t)pp * lay.rec + lay.foff + k0 + kk] : 0.0;
       sq[rr][kk] = (qq < b && kin) ? prop[(int64_t)qq * lay.rec + lay.foff + k0 + kk] : 0.0;
     }
     __syncthreads();
+    const int kend = min(128, kcur - k0);
 #pragma unroll 8
-    for (int kk = 0; kk < 32; ++kk) acc = __dadd_rn(acc, __dmul_rn(sp[ty][kk], sq[tx][kk]));
+    for (int kk = 0; kk < kend; ++kk) acc = __dadd_rn(acc, __dmul_rn(sp[ty][kk], sq[tx][kk]));
     __syncthreads();
   }
   if (p < b && q < b) {
@@ -81,21 +82,34 @@ void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d,
 }
 
 constexpr int kSweepThreads = 1024;
+constexpr int kSweepBlock = 16;
 
 __device__ __forceinline__ int64_t tri(int p) { return (int64_t)p * (p + 1) / 2; }
 
+// Blocked form of the reference's right-looking sweep with the identical per-entry
+// operation sequence: every h_pq still receives  h_pq - l_c(p) l_c(q)  for the
+// accepted steps c in sweep order, with the same two roundings, so the decisions,
+// L and the accepted list are bit-identical to rpcholesky.hpp:174-199.
+//   1. warp 0 runs the 16 decisions of a block on the 16x16 diagonal block only
+//      (a decision needs h_ii, which depends only on in-block l values);
+//   2. all threads form the accepted columns below the block (panel) row by row;
+//   3. all threads apply the block's accepted rank-1 updates to the trailing
+//      triangle, in acceptance order per entry.
+// Three CTA barriers per 16 steps instead of two per step.
 __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     const double* __restrict__ H, int b, uint64_t seed, uint64_t draw0,
     const double* __restrict__ prop, RecordLayout lay, int* __restrict__ pos,
     int64_t* __restrict__ acc_ids, double* __restrict__ lcol, double* __restrict__ lacc_cm,
     SweepOut* out, double* hp_global) {
   extern __shared__ double sm[];
-  __shared__ int s_m;
+  __shared__ int s_m, s_nacc, s_acc[kSweepBlock];
+  __shared__ double s_root[kSweepBlock];
   __shared__ int s_pos[256];
-  double* lcur = sm;
-  double* rdraw = sm + b;
-  double* udiag = sm + 2 * b;
-  double* hp = hp_global ? hp_global : sm + 3 * b;
+  double* rdraw = sm;
+  double* udiag = sm + b;
+  double* lblk = sm + 2 * b;                       // [kSweepBlock][kSweepBlock] in-block l values
+  double* lpan = lblk + kSweepBlock * kSweepBlock;  // [kSweepBlock][b] panel l values
+  double* hp = hp_global ? hp_global : lpan + kSweepBlock * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kSweepThreads / 32;
   for (int p = warp; p < b; p += nwarps)
@@ -106,26 +120,65 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   }
   if (tid == 0) s_m = 0;
   __syncthreads();
-  for (int i = 0; i < b; ++i) {
-    const double hii = hp[tri(i) + i];
-    if (!(__dmul_rn(udiag[i], rdraw[i]) < hii)) continue;  // uniform across the CTA
-    const double root = __dsqrt_rn(hii);
-    const int m = s_m;
-    for (int j = i + tid; j < b; j += kSweepThreads) {
-      const double lj = __ddiv_rn(hp[tri(j) + i], root);
-      lcur[j] = lj;
-      lcol[(int64_t)m * b + j] = lj;
+  for (int i0 = 0; i0 < b; i0 += kSweepBlock) {
+    const int i1 = min(b, i0 + kSweepBlock);
+    // ---- 1. decisions on the diagonal block (warp 0) ----
+    if (warp == 0) {
+      int nacc = 0;
+      const int p = i0 + lane;  // this lane's row inside the block
+      for (int i = i0; i < i1; ++i) {
+        const double hii = hp[tri(i) + i];
+        if (!(__dmul_rn(udiag[i], rdraw[i]) < hii)) continue;  // uniform in the warp
+        const double root = __dsqrt_rn(hii);
+        if (lane < kSweepBlock && p >= i && p < i1)
+          lblk[nacc * kSweepBlock + (p - i0)] = __ddiv_rn(hp[tri(p) + i], root);
+        __syncwarp();
+        if (lane < kSweepBlock && p > i && p < i1) {
+          const double lp = lblk[nacc * kSweepBlock + (p - i0)];
+          for (int q = i + 1; q <= p; ++q)
+            hp[tri(p) + q] = __dsub_rn(hp[tri(p) + q], __dmul_rn(lp, lblk[nacc * kSweepBlock + (q - i0)]));
+        }
+        if (lane == 0) {
+          s_acc[nacc] = i;
+          s_root[nacc] = root;
+        }
+        __syncwarp();
+        ++nacc;
+      }
+      if (lane == 0) s_nacc = nacc;
     }
     __syncthreads();
-    for (int p = i + 1 + warp; p < b; p += nwarps) {
-      const double lp = lcur[p];
-      const int64_t base = tri(p);
-      for (int q = i + 1 + lane; q <= p; q += 32)
-        hp[base + q] = __dsub_rn(hp[base + q], __dmul_rn(lp, lcur[q]));
-    }
-    if (tid == 0) {
-      s_pos[m] = i;
-      s_m = m + 1;
+    const int nacc = s_nacc;
+    const int m0 = s_m;
+    if (nacc > 0) {
+      // ---- 2. panel: l_c(p) for rows p >= i1, accepted c in order ----
+      for (int p = i1 + tid; p < b; p += kSweepThreads) {
+        for (int k = 0; k < nacc; ++k) {
+          const int c = s_acc[k];
+          double t = hp[tri(p) + c];
+          for (int k2 = 0; k2 < k; ++k2)
+            t = __dsub_rn(t, __dmul_rn(lpan[k2 * b + p], lblk[k2 * kSweepBlock + (c - i0)]));
+          lpan[k * b + p] = __ddiv_rn(t, s_root[k]);
+        }
+      }
+      __syncthreads();
+      // global L columns (c-th acceptance): rows in the block and below
+      for (int idx = tid; idx < nacc * b; idx += kSweepThreads) {
+        const int k = idx / b, j = idx % b, c = s_acc[k];
+        if (j < c) continue;
+        lcol[(int64_t)(m0 + k) * b + j] = j < i1 ? lblk[k * kSweepBlock + (j - i0)] : lpan[k * b + j];
+      }
+      // ---- 3. trailing update, acceptance order per entry ----
+      for (int p = i1 + warp; p < b; p += nwarps) {
+        const int64_t base = tri(p);
+        for (int q = i1 + lane; q <= p; q += 32) {
+          double h = hp[base + q];
+          for (int k = 0; k < nacc; ++k) h = __dsub_rn(h, __dmul_rn(lpan[k * b + p], lpan[k * b + q]));
+          hp[base + q] = h;
+        }
+      }
+      if (tid < nacc) s_pos[m0 + tid] = s_acc[tid];
+      if (tid == 0) s_m = m0 + nacc;
     }
     __syncthreads();
   }
@@ -146,45 +199,77 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
                   RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
                   SweepOut* out, double* scratch_hp, cudaStream_t st) {
   const size_t packed = (size_t)b * (b + 1) / 2;
-  size_t smem = (size_t)3 * b * sizeof(double);
+  size_t smem = sizeof(double) * (2 * (size_t)b + kSweepBlock * kSweepBlock + kSweepBlock * (size_t)b);
   double* hpg = nullptr;
-  if (smem + packed * sizeof(double) <= 200 * 1024) {
+  if (smem + packed * sizeof(double) <= 210 * 1024) {
     smem += packed * sizeof(double);
   } else {
     hpg = scratch_hp;  // global (L2-resident) fallback for large blocks
   }
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024);
     attr = true;
   }
   sweep_kernel<<<1, kSweepThreads, smem, st>>>(H, b, seed, draw0, prop, lay, pos, acc_ids, lcol,
                                                 lacc_cm, out, hpg);
 }
 
-// One CTA per column c of L^{-1}: forward substitution L x = e_c, axpy form.
-__global__ void __launch_bounds__(256) linv_kernel(const double* __restrict__ lacc_cm, int m,
-                                                   int nb, int64_t ldl, int koff,
-                                                   double* __restrict__ linv_rm) {
-  extern __shared__ double rhs[];
-  const int c = blockIdx.x, tid = threadIdx.x;
-  for (int a = tid; a < m; a += 256) rhs[a] = (a == c) ? 1.0 : 0.0;
-  __syncthreads();
-  for (int t = c; t < m; ++t) {
-    const double xt = __ddiv_rn(rhs[t], lacc_cm[(int64_t)t * m + t]);
+// L^{-1} by forward substitution L x = e_c, one warp per column c (8 columns per
+// CTA), with the lower triangle of L staged in shared memory (packed by rows when
+// it fits, else read from L2).  No CTA-wide barriers inside the substitution.
+constexpr int kLinvWarps = 8;
+__global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __restrict__ lacc_cm,
+                                                               int m, int nb, int64_t ldl, int koff,
+                                                               int in_smem,
+                                                               double* __restrict__ linv_rm) {
+  extern __shared__ double sL[];  // column-major m x m copy (lower part) when in_smem
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const double* L = lacc_cm;
+  if (in_smem) {
+    for (int i = tid; i < m * m; i += blockDim.x) sL[i] = lacc_cm[i];
     __syncthreads();
-    for (int a = t + 1 + tid; a < m; a += 256)
-      rhs[a] = fma(-lacc_cm[(int64_t)t * m + a], xt, rhs[a]);
-    if (tid == 0) rhs[t] = xt;
-    __syncthreads();
+    L = sL;
   }
-  for (int a = tid; a < nb; a += 256)
-    linv_rm[(int64_t)perm_row(a) * ldl + c + koff] = (a >= c && a < m) ? rhs[a] : 0.0;
+  const int c = blockIdx.x * kLinvWarps + warp;
+  if (c >= m) return;
+  // lane owns rows a = lane + 32 q
+  double x[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) x[q] = (lane + 32 * q == c) ? 1.0 : 0.0;
+  for (int t = c; t < m; ++t) {
+    const int ql = t >> 5, ll = t & 31;
+    double xt_own = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (q == ql) xt_own = x[q];
+    const double xt = __ddiv_rn(__shfl_sync(0xffffffffu, xt_own, ll), L[(int64_t)t * m + t]);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int a = lane + 32 * q;
+      if (a == t) x[q] = xt;
+      else if (a > t && a < m) x[q] = fma(-L[(int64_t)t * m + a], xt, x[q]);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const int a = lane + 32 * q;
+    if (a < nb) linv_rm[(int64_t)perm_row(a) * ldl + c + koff] = (a >= c && a < m) ? x[q] : 0.0;
+  }
 }
 
 void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
                  cudaStream_t st) {
-  if (m > 0) linv_kernel<<<m, 256, m * sizeof(double), st>>>(lacc_cm, m, nb, ldl, koff, linv_rm);
+  if (m <= 0) return;
+  const size_t bytes = sizeof(double) * (size_t)m * m;
+  const int in_smem = bytes <= 200 * 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  linv_kernel<<<(m + kLinvWarps - 1) / kLinvWarps, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(
+      lacc_cm, m, nb, ldl, koff, in_smem, linv_rm);
 }
 
 }  // namespace rpcb

@@ -16,10 +16,11 @@
 // and l1 distances run on the FP64 CUDA cores from the same staged X tiles in
 // ascending coordinate order (bit-identical distances to the reference's sums).
 //
-// Execution: 8 consumer warps + 1 producer warp.  The producer's elected lane
+// Execution: persistent CTAs (one per SM) of 8 warps walk row tiles; thread 0
 // streams [rows][16] fp64 tiles with 2D TMA (cp.async.bulk.tensor, 128B swizzle)
-// into an S-stage ring guarded by full/empty mbarriers; consumers run
-// mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operand rows are permuted inside 8-row
+// into an S-stage ring guarded by full/empty mbarriers, running ahead across tile
+// boundaries (the next tile's first tiles load during this tile's epilogue); all
+// warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operand rows are permuted inside 8-row
 // groups (perm8, common.cuh) so every fragment load is bank-conflict free.
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -33,10 +34,10 @@
 
 namespace rpcb {
 
-template <int NCW_, int WC, int NFW>
+template <int WC, int NFW>
 struct UCfg {
-  static constexpr int NCW = NCW_;          // consumer warps
-  static constexpr int NT = 32 * (NCW + 1); // + producer warp
+  static constexpr int NCW = 8;             // warps (all consumers; thread 0 also issues TMA)
+  static constexpr int NT = 32 * NCW;
   static constexpr int WR = NCW / WC;
   static constexpr int BM = 16 * WR;        // tile rows
   static constexpr int NF = WC * NFW;       // 8-column fragments
@@ -45,13 +46,9 @@ struct UCfg {
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = NB * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int MISC = NB * 16 + WC * BM * 8 + BM * 8 + (2 * S + 2) * 8;
+  static constexpr int MISC = NB * 16 + WC * BM * 8 + BM * 8 + (2 * S) * 8;
   static constexpr int SMEM = S * STAGE + MISC + 1024;
 };
-
-__device__ __forceinline__ double lds64(const unsigned char* base, uint32_t off) {
-  return *reinterpret_cast<const double*>(base + off);
-}
 
 // Compact exp for the kernel-column epilogue (arguments are <= 0 here):
 // Cody-Waite reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor polynomial
@@ -83,26 +80,27 @@ __device__ __forceinline__ double exp_compact(double x) {
   return q * s1 * s2;
 }
 
-template <int NCW_, int WC, int NFW, bool GRAM>
-__global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
+template <int WC, int NFW, bool GRAM>
+__global__ void __launch_bounds__(UCfg<WC, NFW>::NT, 1)
     update_kernel(UpdateParams p, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmF,
                   const __grid_constant__ CUtensorMap tmFS, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmL) {
-  using C = UCfg<NCW_, WC, NFW>;
+  using C = UCfg<WC, NFW>;
   constexpr int BM = C::BM, S = C::S, NCW = C::NCW;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* stages = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1024-byte aligned ring (128B-swizzle atoms).  Offsets stay relative to the
+  // __shared__ array so every fragment load is an LDS with an immediate offset.
+  const uint32_t align = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
+  unsigned char* stages = smem_raw + align;
   double* s_sqnS = reinterpret_cast<double*>(stages + S * C::STAGE);
   double* s_idS = s_sqnS + C::NB;
   double* s_rown = s_idS + C::NB;  // [WC][BM]
   double* s_rowg2 = s_rown + WC * BM;
   uint64_t* full = reinterpret_cast<uint64_t*>(s_rowg2 + BM);
   uint64_t* empty = full + S;
-  uint64_t* gready = empty + S;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t tile_row0 = (int64_t)blockIdx.x * BM;
   const int m = p.m, kcur = p.kcur;
   const int nX = p.dchunks;
   const int nFk = (kcur + 15) >> 4;
@@ -111,15 +109,23 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
   // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
   const int koff = kcur & 1;
   const int nL = p.columns_only ? 0 : (m + koff + 15) >> 4;
-  const int total = nX + nFk + nL;
+  const int T = nX + nFk + nL;               // chunks per tile
+  const int ntiles = (int)((p.n_loc + BM - 1) / BM);
+  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  const int total = my_tiles * T;            // chunks this CTA consumes (persistent)
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
     }
-    mbar_init(gready, NCW);
     mbar_fence_init();
+    tma_prefetch_desc(&tmX);
+    tma_prefetch_desc(&tmXS);
+    tma_prefetch_desc(&tmF);
+    tma_prefetch_desc(&tmFS);
+    tma_prefetch_desc(&tmG);
+    tma_prefetch_desc(&tmL);
   }
   for (int n = tid; n < C::NB; n += C::NT) {
     s_sqnS[n] = p.sqnS[n];
@@ -127,50 +133,42 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
   }
   __syncthreads();
 
-  if (warp == NCW) {  // ---------------- producer warp ----------------------
-    if (lane == 0) {
-      tma_prefetch_desc(&tmX);
-      tma_prefetch_desc(&tmXS);
-      tma_prefetch_desc(&tmF);
-      tma_prefetch_desc(&tmFS);
-      tma_prefetch_desc(&tmG);
-      tma_prefetch_desc(&tmL);
-      const int r0 = (int)tile_row0;
-      for (int c = 0; c < total; ++c) {
-        const int s = c % S;
-        if (c >= S) mbar_wait(&empty[s], ((c / S) & 1) ^ 1);
-        if (c == nX + nFk) mbar_wait(gready, 0);  // phase-2 A operand parked in F
-        unsigned char* As = stages + s * C::STAGE;
-        unsigned char* Bs = As + C::A_BYTES;
-        mbar_arrive_expect_tx(&full[s], C::STAGE);
-        if (c < nX) {
-          tma_load_2d(As, &tmX, 16 * c, r0, &full[s]);
-          tma_load_2d(Bs, &tmXS, 16 * c, 0, &full[s]);
-        } else if (c < nX + nFk) {
-          tma_load_2d(As, &tmF, 16 * (c - nX), r0, &full[s]);
-          tma_load_2d(Bs, &tmFS, 16 * (c - nX), 0, &full[s]);
-        } else {
-          tma_load_2d(As, &tmG, kcur - koff + 16 * (c - nX - nFk), r0, &full[s]);
-          tma_load_2d(Bs, &tmL, 16 * (c - nX - nFk), 0, &full[s]);
-        }
+  // ---- producer (thread 0): issue chunk `issued` when its stage is free and, for
+  // phase-2 chunks of tile k, once that tile's G is parked (parked > k).
+  int issued = 0;      // meaningful in thread 0 only
+  int parked = 0;      // tiles whose G has been parked (CTA-uniform)
+  auto pump = [&](int done_w0) {
+    if (tid != 0) return;
+    while (issued < total && issued < done_w0 + S) {
+      const int k = issued / T, c = issued - k * T;
+      if (c >= nX + nFk && parked <= k) break;
+      const int s = issued % S;
+      if (issued >= S) mbar_wait(&empty[s], ((issued / S) & 1) ^ 1);
+      unsigned char* As = stages + s * C::STAGE;
+      unsigned char* Bs = As + C::A_BYTES;
+      const int r0 = (int)((blockIdx.x + (int64_t)k * gridDim.x) * BM);
+      mbar_arrive_expect_tx(&full[s], C::STAGE);
+      if (c < nX) {
+        tma_load_2d(As, &tmX, 16 * c, r0, &full[s]);
+        tma_load_2d(Bs, &tmXS, 16 * c, 0, &full[s]);
+      } else if (c < nX + nFk) {
+        tma_load_2d(As, &tmF, 16 * (c - nX), r0, &full[s]);
+        tma_load_2d(Bs, &tmFS, 16 * (c - nX), 0, &full[s]);
+      } else {
+        tma_load_2d(As, &tmG, kcur - koff + 16 * (c - nX - nFk), r0, &full[s]);
+        tma_load_2d(Bs, &tmL, 16 * (c - nX - nFk), 0, &full[s]);
       }
+      ++issued;
     }
-    return;
-  }
+  };
+  pump(0);
 
-  // ------------------------------ consumer warps ------------------------------
   const int g = lane >> 2, t = lane & 3;
   const int wr = warp / WC, wc = warp % WC;
   const int pg = perm8(g);
   int arow[2];  // tile rows of this lane's A-fragment rows
 #pragma unroll
   for (int fr = 0; fr < 2; ++fr) arow[fr] = wr * 16 + 8 * fr + pg;
-
-  double acc[2][NFW][2];
-#pragma unroll
-  for (int fr = 0; fr < 2; ++fr)
-#pragma unroll
-    for (int q = 0; q < NFW; ++q) acc[fr][q][0] = acc[fr][q][1] = 0.0;
 
   // Swizzled byte offsets of this lane's fragment element (row & 7 == pg, k = 4s + t)
   // inside any 8-row group: identical for the A and B operands, so every fragment
@@ -179,40 +177,45 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
 #pragma unroll
   for (int s = 0; s < 4; ++s) foff[s] = swz_off(pg, 4 * s + t);
   const uint32_t a_base = (uint32_t)(wr * 16) * 128u;
+  const uint32_t b_base = (uint32_t)(wc * NFW) * 1024u;
+
+  double acc[2][NFW][2];
 
   // q_lo: first fragment that can be non-zero (phase 2 skips the zero upper triangle
   // of L^{-T}; phase 1 passes 0).
-  auto mma_stage = [&](const unsigned char* As, const unsigned char* Bs, int q_lo) {
-    const unsigned char* Aw = As + a_base;
-    const unsigned char* Bw = Bs + (uint32_t)(wc * NFW) * 1024u;
+  auto mma_stage = [&](uint32_t st_off, int q_lo) {
+    const unsigned char* Aw = stages + st_off + a_base;
+    const unsigned char* Bw = stages + st_off + C::A_BYTES + b_base;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
       double a[2];
 #pragma unroll
-      for (int fr = 0; fr < 2; ++fr) a[fr] = lds64(Aw + fr * 1024, foff[s]);
+      for (int fr = 0; fr < 2; ++fr) a[fr] = *reinterpret_cast<const double*>(Aw + fr * 1024 + foff[s]);
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
         if (q < q_lo) continue;
-        const double bv = lds64(Bw + q * 1024, foff[s]);
+        const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[fr], bv);
       }
     }
   };
 
-  auto dist_stage = [&](const unsigned char* As, const unsigned char* Bs) {
+  auto dist_stage = [&](uint32_t st_off) {
+    const unsigned char* As = stages + st_off;
+    const unsigned char* Bs = As + C::A_BYTES;
     const bool l1 = p.kind == kL1;
-#pragma unroll 4
+#pragma unroll 1
     for (int j = 0; j < 16; ++j) {
       double xr[2];
 #pragma unroll
-      for (int fr = 0; fr < 2; ++fr) xr[fr] = lds64(As, swz_off(arow[fr], j));
+      for (int fr = 0; fr < 2; ++fr) xr[fr] = *reinterpret_cast<const double*>(As + swz_off(arow[fr], j));
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
         const int Q = wc * NFW + q;
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const double xs = lds64(Bs, swz_off(8 * Q + perm8(2 * t + v), j));
+          const double xs = *reinterpret_cast<const double*>(Bs + swz_off(8 * Q + perm8(2 * t + v), j));
 #pragma unroll
           for (int fr = 0; fr < 2; ++fr) {
             const double df = __dsub_rn(xr[fr], xs);
@@ -224,155 +227,154 @@ __global__ void __launch_bounds__(UCfg<NCW_, WC, NFW>::NT, 1)
     }
   };
 
-  auto transform = [&]() {  // acc (Gram dot / distance) -> -A(R, S)
-    // exponent = D * (-0.5 / sigma^2) (Gaussian) or D * (-1 / sigma) (l1): one multiply
-    // instead of the reference's division, <= 1 ulp apart (kernel values agree to 1e-15).
-    const double escale = (!GRAM && p.kind == kL1) ? -1.0 / p.sigma : -0.5 / (p.sigma * p.sigma);
+  int cons = 0;  // chunks consumed by this warp so far (CTA-uniform in practice)
+  auto consume = [&](auto&& body) {
+    const int s = cons % S;
+    mbar_wait(&full[s], (cons / S) & 1);
+    __syncwarp();
+    body((uint32_t)(s * C::STAGE));
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++cons;
+    if (warp == 0) pump(cons);
+  };
+
+#pragma unroll 1
+  for (int k = 0; k < my_tiles; ++k) {
+    const int tile = (int)blockIdx.x + k * (int)gridDim.x;
+    const int64_t tile_row0 = (int64_t)tile * BM;
 #pragma unroll
-    for (int fr = 0; fr < 2; ++fr) {
-      const int64_t grow = tile_row0 + arow[fr];
-      const bool rin = grow < p.n_loc;
-      const double sqr = rin ? p.sqn[grow] : 0.0;
-      const double gid = (double)(p.row0 + grow);
+    for (int fr = 0; fr < 2; ++fr)
 #pragma unroll
-      for (int q = 0; q < NFW; ++q) {
+      for (int q = 0; q < NFW; ++q) acc[fr][q][0] = acc[fr][q][1] = 0.0;
+
+    // ---- phase 1a: kernel-column distances / Gram products (X tiles) -------------
+#pragma unroll 1
+    for (int c = 0; c < nX; ++c) {
+      if constexpr (GRAM) consume([&](uint32_t so) { mma_stage(so, 0); });
+      else consume([&](uint32_t so) { dist_stage(so); });
+    }
+    // ---- acc (Gram dot / distance) -> -A(R, S) ------------------------------------
+    {
+      // exponent = D * (-0.5 / sigma^2) (Gaussian) or D * (-1 / sigma) (l1): one multiply
+      // instead of the reference's division, <= 1 ulp apart (kernel values agree to 1e-15).
+      const double escale = (!GRAM && p.kind == kL1) ? -1.0 / p.sigma : -0.5 / (p.sigma * p.sigma);
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int col = 8 * (wc * NFW + q) + 2 * t + v;
-          double val = 0.0;
-          if (col < m && rin) {
-            const double a = acc[fr][q][v];
-            double dd = a;
-            if (GRAM) {
-              dd = __dadd_rn(__dadd_rn(-2.0 * a, sqr), s_sqnS[col]);
-              if (dd < 0.0) dd = 0.0;
-              if (gid == s_idS[col]) dd = 0.0;
+      for (int fr = 0; fr < 2; ++fr) {
+        const int64_t grow = tile_row0 + arow[fr];
+        const bool rin = grow < p.n_loc;
+        const double sqr = rin ? p.sqn[grow] : 0.0;
+        const double gid = (double)(p.row0 + grow);
+#pragma unroll
+        for (int q = 0; q < NFW; ++q) {
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = 8 * (wc * NFW + q) + 2 * t + v;
+            double val = 0.0;
+            if (col < m && rin) {
+              double dd = acc[fr][q][v];
+              if (GRAM) {
+                dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr), s_sqnS[col]);
+                if (dd < 0.0) dd = 0.0;
+                if (gid == s_idS[col]) dd = 0.0;
+              }
+              val = exp_compact(dd * escale);
             }
-            val = exp_compact(dd * escale);
+            acc[fr][q][v] = -val;
           }
-          acc[fr][q][v] = -val;
         }
       }
     }
-  };
-
-  // ---- phase 1a: kernel-column distances (X tiles) ------------------------------
+    // ---- phase 1b: residual GEMM F(R,:) F(S,:)^T (F tiles) ---------------------------
 #pragma unroll 1
-  for (int c = 0; c < nX; ++c) {
-    const int s = c % S;
-    mbar_wait(&full[s], (c / S) & 1);
-    __syncwarp();
-    const unsigned char* As = stages + s * C::STAGE;
-    if constexpr (GRAM) mma_stage(As, As + C::A_BYTES, 0);
-    else dist_stage(As, As + C::A_BYTES);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-  transform();
-  // ---- phase 1b: residual GEMM F(R,:) F(S,:)^T (F tiles) ---------------------------
-#pragma unroll 1
-  for (int c = nX; c < nX + nFk; ++c) {
-    const int s = c % S;
-    mbar_wait(&full[s], (c / S) & 1);
-    __syncwarp();
-    const unsigned char* As = stages + s * C::STAGE;
-    mma_stage(As, As + C::A_BYTES, 0);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
+    for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0); });
 
-  if (p.columns_only) {  // standalone K5: A(R, S) -> column-major output
+    if (p.columns_only) {  // standalone K5: A(R, S) -> column-major output
+#pragma unroll
+      for (int fr = 0; fr < 2; ++fr) {
+        const int64_t grow = tile_row0 + arow[fr];
+        if (grow >= p.n_loc) continue;
+#pragma unroll
+        for (int q = 0; q < NFW; ++q)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = 8 * (wc * NFW + q) + 2 * t + v;
+            if (col < m) p.cols_out[(int64_t)col * p.ld_out + grow] = -acc[fr][q][v];
+          }
+      }
+      continue;
+    }
+
+    // ---- park G = -acc in F(R, kcur:kcur+m) for phase 2 --------------------------
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr) {
       const int64_t grow = tile_row0 + arow[fr];
-      if (grow >= p.n_loc) continue;
+      double* frow = p.F + grow * p.ldf + kcur;
 #pragma unroll
       for (int q = 0; q < NFW; ++q)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const int col = 8 * (wc * NFW + q) + 2 * t + v;
-          if (col < m) p.cols_out[(int64_t)col * p.ld_out + grow] = -acc[fr][q][v];
+          if (col < m && grow < p.n_loc) frow[col] = -acc[fr][q][v];
+          acc[fr][q][v] = 0.0;
         }
     }
-    return;
-  }
+    fence_proxy_async_global();
+    __syncthreads();
+    parked = k + 1;
+    if (warp == 0) pump(cons);
 
-  // ---- park G = -acc in F(R, kcur:kcur+m) for phase 2 --------------------------
-#pragma unroll
-  for (int fr = 0; fr < 2; ++fr) {
-    const int64_t grow = tile_row0 + arow[fr];
-    if (grow >= p.n_loc) continue;
-    double* frow = p.F + grow * p.ldf + kcur;
-#pragma unroll
-    for (int q = 0; q < NFW; ++q)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int col = 8 * (wc * NFW + q) + 2 * t + v;
-        if (col < m) frow[col] = -acc[fr][q][v];
-        acc[fr][q][v] = 0.0;
-      }
-  }
-  fence_proxy_async_global();
-  __syncwarp();
-  if (lane == 0) mbar_arrive(gready);
-
-  // ---- phase 2: G L^{-T} ------------------------------------------------------------
+    // ---- phase 2: G L^{-T} ------------------------------------------------------------
 #pragma unroll 1
-  for (int c = nX + nFk; c < total; ++c) {
-    const int s = c % S;
-    mbar_wait(&full[s], (c / S) & 1);
-    __syncwarp();
-    const unsigned char* As = stages + s * C::STAGE;
-    // chunk j covers G columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
-    // so fragments whose 8 columns all lie below 16j - koff contribute nothing.
-    const int j = c - nX - nFk;
-    const int q_lo = max(0, (16 * j - koff) / 8 - wc * NFW);
-    mma_stage(As, As + C::A_BYTES, q_lo);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
-
-  // ---- epilogue ------------------------------------------------------------------
-  double rs[2] = {0.0, 0.0};
-#pragma unroll
-  for (int fr = 0; fr < 2; ++fr) {
-    const int64_t grow = tile_row0 + arow[fr];
-    const bool rin = grow < p.n_loc;
-    double* frow = p.F + grow * p.ldf + kcur;
-#pragma unroll
-    for (int q = 0; q < NFW; ++q)
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int col = 8 * (wc * NFW + q) + 2 * t + v;
-        if (col < m && rin) {
-          const double val = acc[fr][q][v];
-          frow[col] = val;
-          rs[fr] = fma(val, val, rs[fr]);
-        }
-      }
-    rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 1);
-    rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 2);
-    if (t == 0) s_rown[wc * BM + arow[fr]] = rs[fr];
-  }
-  named_bar_sync(1, 32 * NCW);
-  if (tid < BM) {
-    const int64_t grow = tile_row0 + tid;
-    double s2 = 0.0;
-#pragma unroll
-    for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + tid]);
-    if (grow < p.n_loc) {
-      const double un = __dsub_rn(p.u[grow], s2);
-      p.u[grow] = un < 0.0 ? 0.0 : un;
-    } else {
-      s2 = 0.0;
+    for (int j = 0; j < nL; ++j) {
+      // chunk j covers G columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
+      // so fragments whose 8 columns all lie below 16j - koff contribute nothing.
+      const int q_lo = max(0, (16 * j - koff) / 8 - wc * NFW);
+      consume([&](uint32_t so) { mma_stage(so, q_lo); });
     }
-    s_rowg2[tid] = s2;
-  }
-  named_bar_sync(1, 32 * NCW);
-  if (tid == 0) {
-    double s = 0.0;
-    for (int r = 0; r < BM; ++r) s = __dadd_rn(s, s_rowg2[r]);
-    p.tile_g2[blockIdx.x] = s;
+
+    // ---- epilogue ------------------------------------------------------------------
+    double rs[2] = {0.0, 0.0};
+#pragma unroll
+    for (int fr = 0; fr < 2; ++fr) {
+      const int64_t grow = tile_row0 + arow[fr];
+      const bool rin = grow < p.n_loc;
+      double* frow = p.F + grow * p.ldf + kcur;
+#pragma unroll
+      for (int q = 0; q < NFW; ++q)
+#pragma unroll
+        for (int v = 0; v < 2; ++v) {
+          const int col = 8 * (wc * NFW + q) + 2 * t + v;
+          if (col < m && rin) {
+            const double val = acc[fr][q][v];
+            frow[col] = val;
+            rs[fr] = fma(val, val, rs[fr]);
+          }
+        }
+      rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 1);
+      rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 2);
+      if (t == 0) s_rown[wc * BM + arow[fr]] = rs[fr];
+    }
+    __syncthreads();
+    if (tid < BM) {
+      const int64_t grow = tile_row0 + tid;
+      double s2 = 0.0;
+#pragma unroll
+      for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + tid]);
+      if (grow < p.n_loc) {
+        const double un = __dsub_rn(p.u[grow], s2);
+        p.u[grow] = un < 0.0 ? 0.0 : un;
+      } else {
+        s2 = 0.0;
+      }
+      s_rowg2[tid] = s2;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      double s2 = 0.0;
+      for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
+      p.tile_g2[tile] = s2;
+    }
   }
 }
 
@@ -408,12 +410,23 @@ static bool make_map(CUtensorMap* m, const double* base, uint64_t inner, uint64_
   return r == CUDA_SUCCESS;
 }
 
-template <int NCW, int WC, int NFW, bool GRAM>
+static int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int WC, int NFW, bool GRAM>
 static int launch_t(const UpdateParams& p, cudaStream_t st) {
-  using C = UCfg<NCW, WC, NFW>;
+  using C = UCfg<WC, NFW>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(update_kernel<NCW, WC, NFW, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(update_kernel<WC, NFW, GRAM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::SMEM) != cudaSuccess)
       return -2;
     attr = true;
@@ -426,12 +439,14 @@ static int launch_t(const UpdateParams& p, cudaStream_t st) {
             make_map(&mG, p.F, p.kcur + p.m, p.n_loc, p.ldf, C::BM) &&
             make_map(&mL, p.linv, p.ldl, C::NB, p.ldl, C::NB);
   if (!ok) return -3;
-  const unsigned grid = (unsigned)((p.n_loc + C::BM - 1) / C::BM);
-  if (grid) update_kernel<NCW, WC, NFW, GRAM><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
+  // persistent: one CTA per SM, tiles strided by the grid (p.tile_g2 is per tile)
+  const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+  if (grid) update_kernel<WC, NFW, GRAM><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
   return C::BM;
 }
 
-// 8 consumer warps + 1 TMA producer warp.  m <= 128: one warp column (BM = 128,
+// 8 warps (thread 0 also issues the TMA loads).  m <= 128: one warp column (BM = 128,
 // warp tile 16 x NB); m <= 256: two warp columns (BM = 64).
 int update_tile_rows(int m) {
   const int nf = (m + 7) / 8;
@@ -444,7 +459,7 @@ int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
 #define RPCB_CASE(W, N) \
   case N:               \
-    return p.kind == kGaussGram ? launch_t<8, W, N, true>(p, st) : launch_t<8, W, N, false>(p, st);
+    return p.kind == kGaussGram ? launch_t<W, N, true>(p, st) : launch_t<W, N, false>(p, st);
   if (nf <= 16) {
     switch (nf) {
       RPCB_CASE(1, 1) RPCB_CASE(1, 2) RPCB_CASE(1, 3) RPCB_CASE(1, 4) RPCB_CASE(1, 5)
