@@ -289,6 +289,9 @@ def main():
             "rank_final": k_final, "rounds": len(m_seq), "accepted_per_round": m_seq,
             "relative_trace_error": trace_err,
             "device_factorize_ms": timing["factorize_ms"],
+            "host_ms": {k: round(timing[k], 3) for k in ("host_total_ms", "host_setup_ms",
+                                                         "host_loop_ms", "host_final_ms",
+                                                         "upload_ms")},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "kernel": "update_kernel (fused K5 kernel columns + K6 FP64 DMMA GEMM + L^-T + diag update)",

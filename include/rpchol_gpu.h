@@ -135,6 +135,10 @@ typedef struct {
   double update_bytes;     /* algorithmic HBM bytes of those launches */
   int64_t update_launches; /* update-kernel launches */
   int64_t kernel_launches; /* all kernels launched by the factorization */
+  double host_total_ms;    /* host wall time of the whole call */
+  double host_setup_ms;    /* ... allocation, upload, packing, validation */
+  double host_loop_ms;     /* ... the round loop */
+  double host_final_ms;    /* ... finalisation (chol gather, bookkeeping) */
 } rpc_timing;
 int rpc_result_timing(const rpc_result* r, rpc_timing* t);
 void rpc_result_free(rpc_result* r);

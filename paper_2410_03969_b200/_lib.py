@@ -57,6 +57,10 @@ class TimingC(C.Structure):
         ("update_bytes", C.c_double),
         ("update_launches", C.c_int64),
         ("kernel_launches", C.c_int64),
+        ("host_total_ms", C.c_double),
+        ("host_setup_ms", C.c_double),
+        ("host_loop_ms", C.c_double),
+        ("host_final_ms", C.c_double),
     ]
 
 

@@ -158,7 +158,6 @@ class CholeskyResult:
     _ctx: Context
     n: int
     pivots: np.ndarray
-    chol_factor: np.ndarray
     proposed: list
     accepted: list
     rank_exhausted: bool
@@ -167,10 +166,21 @@ class CholeskyResult:
     relative_trace_error: float
     timing: dict = field(default_factory=dict)
     _factor: np.ndarray | None = None
+    _chol: np.ndarray | None = None
 
     @property
     def rank(self) -> int:
         return int(self.pivots.size)
+
+    @property
+    def chol_factor(self) -> np.ndarray:
+        """k x k lower-triangular F(pivots, :) (rpcholesky.hpp:140-145)."""
+        if self._chol is None:
+            k = self.rank
+            self._chol = np.zeros((k, k), order="F")
+            L.check(L.load().rpc_result_chol_copy(self._handle, self._chol.ctypes.data),
+                    self._ctx.handle)
+        return self._chol
 
     def factor_into(self, out: np.ndarray, layout: str = "F") -> np.ndarray:
         lay = L.RPC_COL_MAJOR if layout == "F" else L.RPC_ROW_MAJOR
@@ -210,8 +220,6 @@ def _wrap_result(h: C.c_void_p, ctx: Context) -> CholeskyResult:
     k = lib.rpc_result_rank(h)
     piv = np.zeros(k, np.int64)
     lib.rpc_result_pivots(h, piv.ctypes.data)
-    chol = np.zeros((k, k), order="F")
-    lib.rpc_result_chol_copy(h, chol.ctypes.data)
     b = lib.rpc_result_block_size(h)
     proposed, accepted = [], []
     for r in range(lib.rpc_result_num_rounds(h)):
@@ -224,7 +232,7 @@ def _wrap_result(h: C.c_void_p, ctx: Context) -> CholeskyResult:
     t = L.TimingC()
     lib.rpc_result_timing(h, C.byref(t))
     timing = {f: getattr(t, f) for f, _ in L.TimingC._fields_}
-    return CholeskyResult(h, ctx, n, piv, chol, proposed, accepted,
+    return CholeskyResult(h, ctx, n, piv, proposed, accepted,
                           bool(lib.rpc_result_rank_exhausted(h)), int(lib.rpc_result_surplus(h)),
                           float(lib.rpc_result_captured_sq(h)),
                           float(lib.rpc_result_relative_trace_error(h)), timing)

@@ -206,7 +206,7 @@ struct rpc_result {
   int64_t surplus = 0;
   double captured_sq = 0.0;
   double fro2 = 0.0;
-  std::vector<double> chol;  // kcur x kcur column-major
+  DBuf chol_dev;             // kcur x kcur column-major lower triangle (device)
   rpc_timing timing{};
 };
 
@@ -285,7 +285,7 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
   const int64_t i = blockIdx.x;
   const int64_t lr = piv[i] - row0;
   if (lr < 0 || lr >= n_loc) return;
-  for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[i * k + j] = F[lr * ldf + j];
+  for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[j * k + i] = F[lr * ldf + j];
 }
 
 // The factorization proper.  `src` points to this process's shard rows (device
@@ -313,6 +313,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   lay.foff = 2 + dpad;
   lay.rec = 2 + dpad + ldf;
 
+  using clk = std::chrono::steady_clock;
+  const auto h0 = clk::now();
+  auto ms_since = [](clk::time_point a) {
+    return std::chrono::duration<double, std::milli>(clk::now() - a).count();
+  };
   res->ctx = ctx;
   res->n = n;
   res->d = d;
@@ -427,9 +432,13 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   bool pending_g2 = false;
   std::vector<Ev> upd_ev;
   upd_ev.reserve(8);
+  std::vector<std::pair<int, int64_t>> upd_info;
+  std::vector<double> upd_flops;
   double update_ms = 0.0, flops = 0.0, bytes = 0.0;
   int64_t upd_launches = 0;
 
+  const double setup_ms = ms_since(h0);
+  const auto h1 = clk::now();
   CK(cudaEventRecord(ev_t0.e, st));
   for (int64_t round = 0;; ++round) {
     if (cfg.mode == RPC_FIXED_ROUNDS ? round >= cfg.rounds : kcur >= cfg.target_rank) break;
@@ -560,7 +569,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         launches += 2;
         ++upd_launches;
         const double N = (double)s.n_loc;
-        flops += 2.0 * N * m * kcur + N * (double)m * m + 2.0 * N * m * d;
+        const double fl = 2.0 * N * m * kcur + N * (double)m * m + 2.0 * N * m * d;
+        flops += fl;
+        upd_info.emplace_back(m, kcur);
+        upd_flops.push_back(fl);
         bytes += 8.0 * (N * kcur + N * m + N * d + 2.0 * N);
       }
       pending_g2 = true;
@@ -571,6 +583,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     res->accepted.push_back(std::move(ac));
   }
   CK(cudaEventRecord(ev_t1.e, st));
+  const double loop_ms = ms_since(h1);
+  const auto h2 = clk::now();
   // ---- finalize ----------------------------------------------------------------
   if (pending_g2) {  // last round's ||G||^2 (no further scan consumed it)
     allgather(ctx, g2_all.as<double>(), L.cpr);
@@ -589,39 +603,47 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   // chunk order per round, so no extra pass over the N x k factor is needed.
   res->fro2 = captured_sq;
   // chol_factor = lower(F(pivots, :)) (rpcholesky.hpp:140-145): owners gather pivot rows
-  res->chol.assign((size_t)kcur * kcur, 0.0);
+  // into a device-resident column-major k x k buffer; copied out on request.
   if (kcur > 0) {
-    DBuf piv(ctx, sizeof(int64_t) * kcur), cb(ctx, sizeof(double) * kcur * kcur);
+    DBuf piv(ctx, sizeof(int64_t) * kcur);
+    res->chol_dev = DBuf(ctx, sizeof(double) * kcur * kcur);
     CK(cudaMemcpyAsync(piv.p, res->pivots.data(), sizeof(int64_t) * kcur, cudaMemcpyHostToDevice, st));
-    CK(cudaMemsetAsync(cb.p, 0, sizeof(double) * kcur * kcur, st));
+    CK(cudaMemsetAsync(res->chol_dev.p, 0, sizeof(double) * kcur * kcur, st));
     for (Shard& s : res->shards) {
       if (s.n_loc == 0) continue;
       chol_gather_kernel<<<(unsigned)kcur, 128, 0, st>>>(s.F.as<double>(), ldf, s.row0, s.n_loc,
-                                                          piv.as<int64_t>(), kcur, cb.as<double>());
+                                                          piv.as<int64_t>(), kcur,
+                                                          res->chol_dev.as<double>());
       ++launches;
     }
     if (ctx->world > 1)  // each pivot row lives on exactly one rank: sum the zeros away
-      NK(ncclAllReduce(cb.p, cb.p, (size_t)kcur * kcur, ncclDouble, ncclSum, ctx->comm, st));
-    std::vector<double> rm((size_t)kcur * kcur);
-    CK(cudaMemcpyAsync(rm.data(), cb.p, sizeof(double) * kcur * kcur, cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    for (int64_t i = 0; i < kcur; ++i)
-      for (int64_t j = 0; j <= i; ++j) res->chol[j * kcur + i] = rm[i * kcur + j];
+      NK(ncclAllReduce(res->chol_dev.p, res->chol_dev.p, (size_t)kcur * kcur, ncclDouble, ncclSum,
+                       ctx->comm, st));
+    CK(cudaStreamSynchronize(st));  // piv returns to the pool
   }
   float ms = 0.f;
   CK(cudaEventElapsedTime(&ms, ev_t0.e, ev_t1.e));
   tm.factorize_ms = ms;
   CK(cudaEventElapsedTime(&ms, ev_up0.e, ev_up1.e));
   tm.upload_ms = ms;
+  const bool dbg_timing = std::getenv("RPC_DEBUG_TIMING") != nullptr;
   for (size_t i = 0; i + 1 < upd_ev.size(); i += 2) {
     CK(cudaEventElapsedTime(&ms, upd_ev[i].e, upd_ev[i + 1].e));
     update_ms += ms;
+    if (dbg_timing && i / 2 < upd_info.size())
+      std::fprintf(stderr, "[rpc] update %zu: m=%d kcur=%lld  %.3f ms  %.2f TF/s\n", i / 2,
+                   upd_info[i / 2].first, (long long)upd_info[i / 2].second, ms,
+                   upd_flops[i / 2] / (ms * 1e-3) / 1e12);
   }
   tm.update_ms = update_ms;
   tm.update_flops = flops;
   tm.update_bytes = bytes;
   tm.update_launches = upd_launches;
   tm.kernel_launches = launches;
+  tm.host_setup_ms = setup_ms;
+  tm.host_loop_ms = loop_ms;
+  tm.host_final_ms = ms_since(h2);
+  tm.host_total_ms = ms_since(h0);
   // release the point copies; F, u stay with the result
   for (Shard& s : res->shards) {
     s.X.release();
@@ -783,8 +805,15 @@ int rpc_result_pivots(const rpc_result* r, int64_t* out) {
 
 int rpc_result_chol_copy(const rpc_result* r, double* out) {
   if (!r || (!out && r->kcur)) return RPC_EINVAL;
-  std::copy(r->chol.begin(), r->chol.end(), out);
-  return RPC_OK;
+  if (r->kcur == 0) return RPC_OK;
+  rpc_ctx* ctx = r->ctx;
+  return guarded(ctx, [&] {
+    std::lock_guard<std::mutex> lk(ctx->mu);
+    CK(cudaSetDevice(ctx->device));
+    CK(cudaMemcpyAsync(out, r->chol_dev.p, sizeof(double) * r->kcur * r->kcur,
+                       cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+  });
 }
 
 int rpc_result_round(const rpc_result* r, int64_t round, int64_t* proposed, int64_t* accepted,
@@ -866,6 +895,7 @@ void rpc_result_free(rpc_result* r) {
     std::lock_guard<std::mutex> lk(r->ctx->mu);
     cudaStreamSynchronize(r->ctx->stream);
     r->shards.clear();  // buffers return to the ctx pool
+    r->chol_dev.release();
   }
   delete r;
 }

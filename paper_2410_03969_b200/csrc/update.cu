@@ -201,6 +201,29 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, 1)
     }
   };
 
+  // Phase-2 variant: the four k-steps' A fragments are loaded once, then each B
+  // fragment column block is either skipped whole (upper triangle of L^{-T}) or
+  // accumulated over all four k-steps — one uniform branch per fragment per chunk.
+  auto mma_stage_tri = [&](uint32_t st_off, int q_lo) {
+    const unsigned char* Aw = stages + st_off + a_base;
+    const unsigned char* Bw = stages + st_off + C::A_BYTES + b_base;
+    double a[4][2];
+#pragma unroll
+    for (int s = 0; s < 4; ++s)
+#pragma unroll
+      for (int fr = 0; fr < 2; ++fr) a[s][fr] = *reinterpret_cast<const double*>(Aw + fr * 1024 + foff[s]);
+#pragma unroll
+    for (int q = 0; q < NFW; ++q) {
+      if (q < q_lo) continue;
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[s][fr], bv);
+      }
+    }
+  };
+
   auto dist_stage = [&](uint32_t st_off) {
     const unsigned char* As = stages + st_off;
     const unsigned char* Bs = As + C::A_BYTES;
@@ -330,7 +353,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, 1)
       // chunk j covers G columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
       // so fragments whose 8 columns all lie below 16j - koff contribute nothing.
       const int q_lo = max(0, (16 * j - koff) / 8 - wc * NFW);
-      consume([&](uint32_t so) { mma_stage(so, q_lo); });
+      consume([&](uint32_t so) { mma_stage_tri(so, q_lo); });
     }
 
     // ---- epilogue ------------------------------------------------------------------
