@@ -87,6 +87,14 @@ const char* rpc_last_error(const rpc_ctx* ctx);
  * this process's shard `local` (0 unless virtual). */
 int rpc_shard_rows(const rpc_ctx* ctx, int64_t n, int local, int64_t* row0, int64_t* nrows);
 
+/* Host-only shard plan (no device needed): N points over n_shards global shards.
+ * Rows are cut at multiples of the 4096-row scan chunk, so the chunk grid, and with
+ * it every reduction order, is independent of the shard count (p-invariance).
+ * Shard s owns rows [row0, row0+nrows) = global chunks [chunk0, chunk0+nchunks);
+ * every shard reserves chunks_per_shard slots in the per-round allgathers. */
+int rpc_plan_shards(int64_t n, int n_shards, int shard, int64_t* row0, int64_t* nrows,
+                    int* chunk0, int* nchunks, int* chunks_per_shard);
+
 /* ---- the hot path: accelerated_rpcholesky over a kernel oracle ----------- */
 /* X: host N x d points (layout + leading dimension ldx).  Every rank passes the
  * same full X; each uploads only its own rows. */

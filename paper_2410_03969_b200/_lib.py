@@ -22,7 +22,7 @@ RPC_FLAG_REPLAY_SCAN = 1
 # Every symbol include/rpchol_gpu.h declares (checked by tests/test_boundary.py).
 EXPORTS = [
     "rpc_create", "rpc_create_virtual", "rpc_nccl_unique_id", "rpc_create_nccl", "rpc_destroy",
-    "rpc_last_error", "rpc_shard_rows", "rpc_accelerated_rpcholesky",
+    "rpc_last_error", "rpc_shard_rows", "rpc_plan_shards", "rpc_accelerated_rpcholesky",
     "rpc_accelerated_rpcholesky_device", "rpc_result_n", "rpc_result_rank", "rpc_result_pivots",
     "rpc_result_factor_copy", "rpc_result_chol_copy", "rpc_result_residual_diag_copy",
     "rpc_result_num_rounds", "rpc_result_block_size", "rpc_result_round",
@@ -84,6 +84,8 @@ def load() -> C.CDLL:
         "rpc_destroy": (None, [vp]),
         "rpc_last_error": (C.c_char_p, [vp]),
         "rpc_shard_rows": (C.c_int, [vp, i64, C.c_int, pi64, pi64]),
+        "rpc_plan_shards": (C.c_int, [i64, C.c_int, C.c_int, pi64, pi64, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.POINTER(C.c_int)]),
         "rpc_accelerated_rpcholesky": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
                                                  RunConfigC, C.POINTER(vp)]),
         "rpc_accelerated_rpcholesky_device": (C.c_int, [vp, vp, i64, i64, i64, C.c_int,

@@ -93,6 +93,16 @@ class Context:
         return r0.value, nr.value
 
 
+def plan_shards(n: int, n_shards: int, shard: int) -> dict:
+    """Host-only shard plan of the C-ABI (rpc_plan_shards); needs no GPU."""
+    r0, nr = C.c_int64(), C.c_int64()
+    c0, nc, cpr = C.c_int(), C.c_int(), C.c_int()
+    L.check(L.load().rpc_plan_shards(n, n_shards, shard, C.byref(r0), C.byref(nr), C.byref(c0),
+                                     C.byref(nc), C.byref(cpr)))
+    return {"row0": r0.value, "nrows": nr.value, "chunk0": c0.value, "nchunks": nc.value,
+            "chunks_per_shard": cpr.value}
+
+
 def nccl_unique_id() -> bytes:
     buf = C.create_string_buffer(128)
     L.check(L.load().rpc_nccl_unique_id(buf))

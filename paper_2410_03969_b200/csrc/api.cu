@@ -738,6 +738,19 @@ void rpc_destroy(rpc_ctx* ctx) {
   delete ctx;
 }
 
+int rpc_plan_shards(int64_t n, int n_shards, int shard, int64_t* row0, int64_t* nrows,
+                    int* chunk0, int* nchunks, int* chunks_per_shard) {
+  if (n < 1 || n_shards < 1 || shard < 0 || shard >= n_shards)
+    return fail(nullptr, RPC_EINVAL, "rpc_plan_shards: bad arguments");
+  const Layout L = make_layout(n, n_shards);
+  if (row0) *row0 = L.row0(shard);
+  if (nrows) *nrows = L.rows(shard);
+  if (chunk0) *chunk0 = shard * L.cpr;
+  if (nchunks) *nchunks = L.chunks(shard);
+  if (chunks_per_shard) *chunks_per_shard = L.cpr;
+  return RPC_OK;
+}
+
 int rpc_shard_rows(const rpc_ctx* ctx, int64_t n, int local, int64_t* row0, int64_t* nrows) {
   if (!ctx || local < 0 || local >= ctx->nvirt || n < 0) return RPC_EINVAL;
   const Layout L = make_layout(n, ctx->nshards());
