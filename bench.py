@@ -44,11 +44,7 @@ def env_rank():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
-
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-              "clocks_event_reasons.sw_power_cap")
+    """SM clocks and throttle reasons sampled (NVML, every 10 ms) during the timed region."""
 
     def __init__(self, device: int):
         self.device = device
@@ -57,16 +53,27 @@ class ClockSampler:
         self._t = None
 
     def _run(self):
-        while not self._stop.is_set():
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+                    "sw_power_cap": 0x4}
+            while not self._stop.is_set():
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((sm, mx, [k for k, b in bits.items() if r & b]))
+                self._stop.wait(0.01)
+        except Exception as e:  # NVML unavailable: fall back to one nvidia-smi reading
             try:
                 out = subprocess.run(["nvidia-smi", "-i", str(self.device),
-                                      f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits"],
+                                      "--query-gpu=clocks.sm,clocks.max.sm", "--format=csv,noheader,nounits"],
                                      capture_output=True, text=True, timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
+                sm, mx = [float(v) for v in out.split(",")]
+                self.samples.append((sm, mx, ["nvml_unavailable:" + type(e).__name__]))
             except Exception:
                 pass
-            self._stop.wait(0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -80,13 +87,9 @@ class ClockSampler:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4)
-                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+        return {"sm_mhz": statistics.median(s[0] for s in self.samples),
+                "sm_max_mhz": max(s[1] for s in self.samples),
+                "reasons": sorted({r for s in self.samples for r in s[2]}),
                 "samples": len(self.samples)}
 
 
@@ -253,6 +256,7 @@ def main():
     achieved = flops / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else 0.0
     tr = ncu_traffic(w.name)
     traffic = tr["bytes_per_launch_mean"] if tr else None
+    traffic_note = tr.get("note") if tr else None
 
     # kernel-col GB/s: standalone K5 on this run's accepted blocks (rank 0 only)
     col_gbs = None
@@ -323,6 +327,7 @@ def main():
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
                          "kernel": "update_kernel (fused K5 kernel columns + K6 FP64 DMMA GEMM + L^-T + diag update)",
+                         "traffic_note": traffic_note,
                          "peak_source": peak_src,
                          "per_launch_flops": flops / max(1, timing["update_launches"]),
                          "update_ms_per_step": upd_ms,

@@ -433,6 +433,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   std::vector<Ev> upd_ev;
   upd_ev.reserve(8);
   std::vector<std::pair<int, int64_t>> upd_info;
+  const bool dbg_phase = std::getenv("RPC_DEBUG_PHASES") != nullptr;
+  DBuf phase_clk(ctx, dbg_phase ? sizeof(unsigned long long) * 8 * 4096 : 8);
   std::vector<double> upd_flops;
   double update_ms = 0.0, flops = 0.0, bytes = 0.0;
   int64_t upd_launches = 0;
@@ -501,6 +503,15 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                  hp.as<double>(), st);
     dbg(st, "sweep");
     launches += 3;
+    // L^{-1} and the accepted-pivot operands only need the sweep's device-side outputs:
+    // queue them before the status read so they run while the host waits.
+    CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+    launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, (int)(kcur & 1),
+                    linv.as<double>(), st);
+    launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, (int)kcur, (int)dpad,
+                           xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
+                           idS.as<double>(), st, &d_sweep->m);
+    launches += 2;
     CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),
@@ -524,13 +535,6 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     if (m > 0) {
       if (kcur + m > cap)
         raise(RPC_ENUMERIC, "accelerated_rpcholesky: factor capacity exceeded (duplicate pivot)");
-      CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
-      launch_linv(lacc.as<double>(), m, (int)nbl, ldl, (int)(kcur & 1), linv.as<double>(), st);
-      launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), m, 256, (int)kcur, (int)dpad,
-                             xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
-                             idS.as<double>(), st);
-      dbg(st, "linv+gather");
-      launches += 2;
       CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
       for (Shard& s : res->shards) {
         if (s.n_loc == 0) continue;
@@ -555,13 +559,36 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.ldl = ldl;
         up.sigma = kspec.sigma;
         up.kind = kind;
+        up.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
         up.tile_g2 = s.tile_g2.as<double>();
+        if (dbg_phase) {
+          CK(cudaMemsetAsync(phase_clk.p, 0, phase_clk.bytes, st));
+          up.phase_clk = phase_clk.as<unsigned long long>();
+        }
         upd_ev.emplace_back();
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
         const int bm = launch_update(up, st);
         CK(cudaEventRecord(upd_ev.back().e, st));
         dbg(st, "update");
+        if (dbg_phase) {
+          std::vector<unsigned long long> h(phase_clk.bytes / 8);
+          CK(cudaMemcpyAsync(h.data(), phase_clk.p, phase_clk.bytes, cudaMemcpyDeviceToHost, st));
+          CK(cudaStreamSynchronize(st));
+          double sum[8] = {0};
+          int nb = 0;
+          for (size_t b = 0; b < h.size() / 8; ++b) {
+            if (!h[b * 8 + 5]) continue;
+            ++nb;
+            for (int q = 0; q < 8; ++q) sum[q] += (double)h[b * 8 + q];
+          }
+          std::fprintf(stderr,
+                       "[rpc] phases m=%d kcur=%lld (Mcycles/CTA): X %.3f drain %.3f sqn %.3f exp %.3f F %.3f "
+                       "park %.3f trsm %.3f epi %.3f\n",
+                       m, (long long)kcur, sum[0] / nb / 1e6, sum[6] / nb / 1e6, sum[7] / nb / 1e6,
+                       sum[1] / nb / 1e6,
+                       sum[2] / nb / 1e6, sum[3] / nb / 1e6, sum[4] / nb / 1e6, sum[5] / nb / 1e6);
+        }
         if (bm < 0) raise(RPC_ECUDA, "update kernel launch failed (code " + std::to_string(bm) + ")");
         const int64_t ntiles = (s.n_loc + bm - 1) / bm;
         launch_tile_to_chunk(s.tile_g2.as<double>(), (int)ntiles, kChunk / bm, s.nchunks,
@@ -986,6 +1013,7 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.ldl = 16;
       up.sigma = kspec.sigma;
       up.kind = kind;
+      up.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
       up.tile_g2 = tile.as<double>();
       up.columns_only = 1;
       up.cols_out = outd.as<double>();

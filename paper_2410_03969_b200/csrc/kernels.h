@@ -77,6 +77,10 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
 // matching the update kernel's 16-byte-aligned phase-2 tiles).
 void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
                  cudaStream_t st);
+// Same with the accepted count read on the device (*m_dev <= m_max): launched right after
+// the sweep, before the host learns m.
+void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb, int64_t ldl,
+                     int koff, double* linv_rm, cudaStream_t st);
 
 // ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
 struct UpdateParams {
@@ -90,9 +94,12 @@ struct UpdateParams {
   int m;
   const double* linv; int64_t ldl;             // L^{-1} rows perm_row(a), [256][ldl]
   double sigma; int kind;
+  double escale;            // -0.5/sigma^2 (Gaussian) or -1/sigma (l1), host-computed
   double* tile_g2;                              // [n_tiles] per-CTA ||G||^2 partial (row order)
   // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
   int columns_only; double* cols_out; int64_t ld_out;
+  // RPC_DEBUG_TIMING: per-CTA cycle counters per phase ([grid][8] u64), or null
+  unsigned long long* phase_clk;
 };
 // Row-tile height used for m accepted columns (128 or 64), or -1 if m unsupported.
 int update_tile_rows(int m);
@@ -102,7 +109,8 @@ int launch_update(const UpdateParams& p, cudaStream_t st);
 // proposal records into the update kernel's operand buffers (rows at perm_row(n), n < nb).
 void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,
                             int kcur, int dpad, double* xs, double* fs, int64_t ldfs,
-                            double* sqnS, double* idS, cudaStream_t st);
+                            double* sqnS, double* idS, cudaStream_t st,
+                            const int* m_dev = nullptr);
 // per-chunk sum of per-tile partials (tile = rows_per_tile rows)
 void launch_tile_to_chunk(const double* tile_g2, int n_tiles, int tiles_per_chunk,
                           int n_chunks_local, double* chunk_g2, cudaStream_t st);

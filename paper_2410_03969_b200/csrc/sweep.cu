@@ -81,7 +81,7 @@ void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d,
   hblock_kernel<<<dim3(nb, nb), dim3(16, 16), 0, st>>>(prop, lay, b, d, kcur, kind, sigma, H);
 }
 
-constexpr int kSweepThreads = 1024;
+constexpr int kSweepThreads = 512;
 constexpr int kSweepBlock = 16;
 
 __device__ __forceinline__ int64_t tri(int p) { return (int64_t)p * (p + 1) / 2; }
@@ -122,27 +122,33 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   __syncthreads();
   for (int i0 = 0; i0 < b; i0 += kSweepBlock) {
     const int i1 = min(b, i0 + kSweepBlock);
-    // ---- 1. decisions on the diagonal block (warp 0) ----
+    // ---- 1. decisions on the diagonal block (warp 0, registers + shuffles) ----
     if (warp == 0) {
       int nacc = 0;
-      const int p = i0 + lane;  // this lane's row inside the block
-      for (int i = i0; i < i1; ++i) {
-        const double hii = hp[tri(i) + i];
-        if (!(__dmul_rn(udiag[i], rdraw[i]) < hii)) continue;  // uniform in the warp
+      const int p = i0 + lane;               // this lane's row inside the block
+      const bool live = lane < kSweepBlock && p < i1;
+      double row[kSweepBlock];               // h(p, i0 + q), q <= p - i0
+#pragma unroll
+      for (int q = 0; q < kSweepBlock; ++q)
+        row[q] = (live && i0 + q <= p) ? hp[tri(p) + i0 + q] : 0.0;
+#pragma unroll
+      for (int ii = 0; ii < kSweepBlock; ++ii) {
+        const int i = i0 + ii;
+        if (i >= i1) break;
+        const double hii = __shfl_sync(0xffffffffu, row[ii], ii);  // lane ii holds h(i, i)
+        if (!(__dmul_rn(udiag[i], rdraw[i]) < hii)) continue;       // uniform in the warp
         const double root = __dsqrt_rn(hii);
-        if (lane < kSweepBlock && p >= i && p < i1)
-          lblk[nacc * kSweepBlock + (p - i0)] = __ddiv_rn(hp[tri(p) + i], root);
-        __syncwarp();
-        if (lane < kSweepBlock && p > i && p < i1) {
-          const double lp = lblk[nacc * kSweepBlock + (p - i0)];
-          for (int q = i + 1; q <= p; ++q)
-            hp[tri(p) + q] = __dsub_rn(hp[tri(p) + q], __dmul_rn(lp, lblk[nacc * kSweepBlock + (q - i0)]));
+        const double lp = (live && p >= i) ? __ddiv_rn(row[ii], root) : 0.0;
+        if (live && p >= i) lblk[nacc * kSweepBlock + (p - i0)] = lp;
+#pragma unroll
+        for (int q = 0; q < kSweepBlock; ++q) {
+          const double lq = __shfl_sync(0xffffffffu, lp, q);
+          if (q > ii && live && i0 + q <= p) row[q] = __dsub_rn(row[q], __dmul_rn(lp, lq));
         }
         if (lane == 0) {
           s_acc[nacc] = i;
           s_root[nacc] = root;
         }
-        __syncwarp();
         ++nacc;
       }
       if (lane == 0) s_nacc = nacc;
@@ -220,35 +226,44 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
 // it fits, else read from L2).  No CTA-wide barriers inside the substitution.
 constexpr int kLinvWarps = 8;
 __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __restrict__ lacc_cm,
-                                                               int m, int nb, int64_t ldl, int koff,
+                                                               int m_host, const int* m_dev,
+                                                               int nb, int64_t ldl, int koff,
                                                                int in_smem,
                                                                double* __restrict__ linv_rm) {
-  extern __shared__ double sL[];  // column-major m x m copy (lower part) when in_smem
+  extern __shared__ double smem_l[];  // column-major m x m copy when it fits
+  const int m = m_dev ? *m_dev : m_host;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const double* L = lacc_cm;
-  if (in_smem) {
-    for (int i = tid; i < m * m; i += blockDim.x) sL[i] = lacc_cm[i];
-    __syncthreads();
-    L = sL;
-  }
   const int c = blockIdx.x * kLinvWarps + warp;
+  if ((int)blockIdx.x * kLinvWarps >= m) return;  // whole CTA beyond m (device-side m)
+  const double* sL = lacc_cm;
+  if (in_smem) {
+    for (int i = tid; i < m * m; i += blockDim.x) smem_l[i] = lacc_cm[i];
+    __syncthreads();
+    sL = smem_l;
+  }
   if (c >= m) return;
-  // lane owns rows a = lane + 32 q
-  double x[8];
+  // lane owns rows a = lane + 32 q; reciprocals of its diagonal entries up front so the
+  // serial substitution chain has no divisions.
+  double x[8], rd[8];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) x[q] = (lane + 32 * q == c) ? 1.0 : 0.0;
+  for (int q = 0; q < 8; ++q) {
+    const int a = lane + 32 * q;
+    x[q] = (a == c) ? 1.0 : 0.0;
+    rd[q] = a < m ? 1.0 / sL[(int64_t)a * m + a] : 0.0;
+  }
   for (int t = c; t < m; ++t) {
     const int ql = t >> 5, ll = t & 31;
     double xt_own = 0.0;
 #pragma unroll
     for (int q = 0; q < 8; ++q)
-      if (q == ql) xt_own = x[q];
-    const double xt = __ddiv_rn(__shfl_sync(0xffffffffu, xt_own, ll), L[(int64_t)t * m + t]);
+      if (q == ql) xt_own = x[q] * rd[q];
+    const double xt = __shfl_sync(0xffffffffu, xt_own, ll);
+    const double* Lt = sL + (int64_t)t * m;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int a = lane + 32 * q;
       if (a == t) x[q] = xt;
-      else if (a > t && a < m) x[q] = fma(-L[(int64_t)t * m + a], xt, x[q]);
+      else if (a > t && a < m) x[q] = fma(-Lt[a], xt, x[q]);
     }
   }
 #pragma unroll
@@ -258,18 +273,32 @@ __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __r
   }
 }
 
-void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
-                 cudaStream_t st) {
-  if (m <= 0) return;
-  const size_t bytes = sizeof(double) * (size_t)m * m;
-  const int in_smem = bytes <= 200 * 1024;
+static void linv_attr() {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(linv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
+}
+
+void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
+                 cudaStream_t st) {
+  if (m <= 0) return;
+  linv_attr();
+  const size_t bytes = sizeof(double) * (size_t)m * m;
+  const int in_smem = bytes <= 200 * 1024;
   linv_kernel<<<(m + kLinvWarps - 1) / kLinvWarps, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(
-      lacc_cm, m, nb, ldl, koff, in_smem, linv_rm);
+      lacc_cm, m, nullptr, nb, ldl, koff, in_smem, linv_rm);
+}
+
+void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb, int64_t ldl,
+                     int koff, double* linv_rm, cudaStream_t st) {
+  if (m_max <= 0) return;
+  linv_attr();
+  const size_t bytes = sizeof(double) * (size_t)m_max * m_max;
+  const int in_smem = bytes <= 200 * 1024;
+  linv_kernel<<<(m_max + kLinvWarps - 1) / kLinvWarps, 32 * kLinvWarps, in_smem ? bytes : 0,
+                st>>>(lacc_cm, 0, m_dev, nb, ldl, koff, in_smem, linv_rm);
 }
 
 }  // namespace rpcb

@@ -10,20 +10,18 @@ namespace rpcb {
 int launch_update_wc1(const UpdateParams& p, int nf, cudaStream_t st);
 int launch_update_wc2(const UpdateParams& p, int nfw, cudaStream_t st);
 
-// Fragment count nf = ceil(m / 8).  Even nf <= 16: two warp columns, BM = 64, two
-// co-resident CTAs per SM (one CTA's per-tile fixed work overlaps the other's DMMA
-// main loop).  Odd nf <= 16: one warp column, BM = 128 (no padded column).
-// 16 < nf <= 32: two warp columns, BM = 64, one CTA per SM.
+// Fragment count nf = ceil(m / 8).  nf <= 16: two ping-pong warp groups per CTA, each
+// with 64-row tiles and a single warp column (no padded columns).  16 < nf <= 32: one
+// group of 8 warps, two warp columns, 64-row tiles.
 int update_tile_rows(int m) {
   const int nf = std::max(1, (m + 7) / 8);
-  if (nf <= 16) return (nf % 2 == 0) ? 64 : 128;
   if (nf <= 32) return 64;
   return -1;
 }
 
 int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
-  if (nf <= 16) return (nf % 2 == 0) ? launch_update_wc2(p, nf / 2, st) : launch_update_wc1(p, nf, st);
+  if (nf <= 16) return launch_update_wc1(p, nf, st);
   if (nf <= 32) return launch_update_wc2(p, (nf + 1) / 2, st);
   return -1;
 }
@@ -31,11 +29,13 @@ int launch_update(const UpdateParams& p, cudaStream_t st) {
 // Accepted-pivot operands for the update: rows stored at perm_row(n) of
 // [256][ld] buffers (zero rows beyond m, zero columns [kcur, round16(kcur))).
 __global__ void gather_accepted_kernel(const double* __restrict__ prop, RecordLayout lay,
-                                       const int* __restrict__ pos, int m, int kcur, int kpad,
+                                       const int* __restrict__ pos, int m_host,
+                                       const int* __restrict__ m_dev, int kcur, int kpad,
                                        int dpad, double* __restrict__ xs, double* __restrict__ fs,
                                        int64_t ldfs, double* __restrict__ sqnS,
                                        double* __restrict__ idS) {
   const int n = blockIdx.x;
+  const int m = m_dev ? *m_dev : m_host;
   const int dst = perm_row(n);
   double* xr = xs + (int64_t)dst * dpad;
   double* fr = fs + (int64_t)dst * ldfs;
@@ -59,10 +59,10 @@ __global__ void gather_accepted_kernel(const double* __restrict__ prop, RecordLa
 
 void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,
                             int kcur, int dpad, double* xs, double* fs, int64_t ldfs,
-                            double* sqnS, double* idS, cudaStream_t st) {
+                            double* sqnS, double* idS, cudaStream_t st, const int* m_dev) {
   const int kpad = std::min<int64_t>(ldfs, ((kcur + 15) / 16) * 16);
-  gather_accepted_kernel<<<nb, 256, 0, st>>>(prop, lay, pos, m, kcur, kpad, dpad, xs, fs, ldfs,
-                                             sqnS, idS);
+  gather_accepted_kernel<<<nb, 256, 0, st>>>(prop, lay, pos, m, m_dev, kcur, kpad, dpad, xs, fs,
+                                             ldfs, sqnS, idS);
 }
 
 }  // namespace rpcb

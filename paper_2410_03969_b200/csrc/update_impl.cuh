@@ -35,73 +35,90 @@
 
 namespace rpcb {
 
-template <int WC, int NFW>
+// G independent warp groups per CTA ("ping-pong"): each group of 8/G warps owns its
+// own stage ring, barriers and tile sequence, so one group's non-DMMA work (exp
+// transform, park, epilogue) overlaps the other group's DMMA main loop, while the
+// CTA keeps the 255-register budget of 256 threads.
+template <int WC, int NFW, int G>
 struct UCfg {
-  static constexpr int NCW = 8;             // warps (all consumers; thread 0 also issues TMA)
-  static constexpr int NT = 32 * NCW;
+  static constexpr int NT = 256;            // threads per CTA
+  static constexpr int NCW = 8 / G;         // warps per group (thread 0 of a group issues TMA)
+  static constexpr int GT = 32 * NCW;       // threads per group
   static constexpr int WR = NCW / WC;
-  static constexpr int BM = 16 * WR;        // tile rows
+  static constexpr int BM = 16 * WR;        // tile rows (per group tile)
   static constexpr int NF = WC * NFW;       // 8-column fragments
   static constexpr int NB = 8 * NF;         // tile columns (m padded)
   static constexpr int S = 4;               // pipeline stages
   static constexpr int A_BYTES = BM * 128;
   static constexpr int B_BYTES = NB * 128;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int MISC = NB * 16 + WC * BM * 8 + BM * 8 + (2 * S) * 8;
-  static constexpr int SMEM = S * STAGE + MISC + 1024;
+  static constexpr int GMISC = WC * BM * 8 + BM * 8 + (2 * S) * 8;  // per group
+  static constexpr int MISC = NB * 16 + 64 * 8 + G * GMISC;
+  static constexpr int SMEM = G * S * STAGE + MISC + 1024;
 };
 
-// Compact exp for the kernel-column epilogue (arguments are <= 0 here):
-// Cody-Waite reduction x = n ln2 + r, |r| <= ln2/2, degree-13 Taylor polynomial
-// (truncation < 5e-18 relative), exact power-of-two scaling in two steps so
-// results down to the subnormal range stay correct.  ~1 ulp, branch-free.
-__device__ __forceinline__ double exp_compact(double x) {
-  x = fmax(x, -745.5);
-  const double n = rint(x * 1.4426950408889634);
-  double r = fma(n, -6.93147180369123816490e-01, x);
-  r = fma(n, -1.90821492927058770002e-10, r);
-  double q = 1.6059043836821613e-10;          // 1/13!
-  q = fma(q, r, 2.0876756987868100e-09);      // 1/12!
-  q = fma(q, r, 2.5052108385441720e-08);      // 1/11!
-  q = fma(q, r, 2.7557319223985893e-07);      // 1/10!
-  q = fma(q, r, 2.7557319223985888e-06);      // 1/9!
-  q = fma(q, r, 2.4801587301587302e-05);      // 1/8!
-  q = fma(q, r, 1.9841269841269841e-04);      // 1/7!
-  q = fma(q, r, 1.3888888888888889e-03);      // 1/6!
-  q = fma(q, r, 8.3333333333333332e-03);      // 1/5!
-  q = fma(q, r, 4.1666666666666664e-02);      // 1/4!
-  q = fma(q, r, 1.6666666666666666e-01);      // 1/3!
-  q = fma(q, r, 0.5);
-  q = fma(q, r, 1.0);
-  q = fma(q, r, 1.0);
-  const int ni = (int)n;
-  const int k1 = ni >> 1, k2 = ni - k1;
-  const double s1 = __longlong_as_double((long long)(k1 + 1023) << 52);
-  const double s2 = __longlong_as_double((long long)(k2 + 1023) << 52);
-  return q * s1 * s2;
+// exp for the kernel-column epilogue: x = (64 n + j) ln2/64 + r with |r| <= ln2/128,
+// exp(x) = 2^n * T[j] * (1 + expm1(r)), T[j] = 2^(j/64) from a shared-memory table,
+// expm1 by a degree-5 polynomial (truncation < 4e-17 relative).  ~1 ulp; about half
+// the FP64 work and dependency depth of a plain Cody-Waite + degree-13 Taylor.
+// Scaling by 2^n in two exact steps keeps subnormal results (x >= -745.5).
+__constant__ double kExpC[8] = {92.332482616893656,        // 64 / ln 2
+                                -1.0830424696249145e-02,   // -ln2/64 (high)
+                                -3.6235106466348430e-19,   // -ln2/64 (low)
+                                8.3333333333333333e-03, 4.1666666666666667e-02,
+                                1.6666666666666667e-01, 0.5, -745.5};
+
+// No FP64<->int conversion instructions (slow paths on this part): k = rint(x 64/ln2)
+// comes out of the low mantissa bits of x * 64/ln2 + 1.5 * 2^52 (one rounding, ties
+// to even, exact for |k| < 2^51).
+__device__ __forceinline__ double exp_tab(double x, const double* __restrict__ tab) {
+  constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  x = fmax(x, kExpC[7]);
+  const double ks = fma(x, kExpC[0], kShift);
+  const int k = __double2loint(ks);
+  const double kd = ks - kShift;
+  double r = fma(kd, kExpC[1], x);
+  r = fma(kd, kExpC[2], r);
+  double q = fma(r, kExpC[3], kExpC[4]);
+  q = fma(q, r, kExpC[5]);
+  q = fma(q, r, kExpC[6]);
+  q = fma(q * r, r, r);                                      // expm1(r)
+  const double t = tab[k & 63];
+  const int n = k >> 6;                                      // floor(k / 64)
+  const int n1 = n >> 1, n2 = n - n1;
+  const double s1 = __hiloint2double((n1 + 1023) << 20, 0);
+  const double s2 = __hiloint2double((n2 + 1023) << 20, 0);
+  return fma(t, q, t) * s1 * s2;
 }
 
-template <int WC, int NFW, bool GRAM, int MINB>
-__global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
+template <int WC, int NFW, bool GRAM, int MINB, int G>
+__global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     update_kernel(UpdateParams p, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmF,
                   const __grid_constant__ CUtensorMap tmFS, const __grid_constant__ CUtensorMap tmG,
                   const __grid_constant__ CUtensorMap tmL) {
-  using C = UCfg<WC, NFW>;
-  constexpr int BM = C::BM, S = C::S, NCW = C::NCW;
+  using C = UCfg<WC, NFW, G>;
+  constexpr int BM = C::BM, S = C::S, NCW = C::NCW, GT = C::GT;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms).  Offsets stay relative to the
   // __shared__ array so every fragment load is an LDS with an immediate offset.
   const uint32_t align = (1024u - (smem_u32(smem_raw) & 1023u)) & 1023u;
-  unsigned char* stages = smem_raw + align;
-  double* s_sqnS = reinterpret_cast<double*>(stages + S * C::STAGE);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int grp = (tid >> 5) / NCW;          // warp group
+  const int warp = (tid >> 5) % NCW;         // warp within the group
+  const int gtid = tid % GT;                 // thread within the group
+  unsigned char* stages = smem_raw + align + grp * S * C::STAGE;
+  double* s_sqnS = reinterpret_cast<double*>(smem_raw + align + G * S * C::STAGE);
   double* s_idS = s_sqnS + C::NB;
-  double* s_rown = s_idS + C::NB;  // [WC][BM]
+  double* s_exp2 = s_idS + C::NB;  // 2^(j/64), j = 0..63
+  unsigned char* gmisc = reinterpret_cast<unsigned char*>(s_exp2 + 64) + grp * C::GMISC;
+  double* s_rown = reinterpret_cast<double*>(gmisc);  // [WC][BM]
   double* s_rowg2 = s_rown + WC * BM;
   uint64_t* full = reinterpret_cast<uint64_t*>(s_rowg2 + BM);
   uint64_t* empty = full + S;
+  auto gsync = [&]() { named_bar_sync(1 + grp, GT); };
+  __shared__ volatile int s_go;  // ping-pong stagger: group 1 starts once group 0 passed its first exp
 
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int m = p.m, kcur = p.kcur;
   const int nX = p.dchunks;
   const int nFk = (kcur + 15) >> 4;
@@ -112,10 +129,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
   const int nL = p.columns_only ? 0 : (m + koff + 15) >> 4;
   const int T = nX + nFk + nL;               // chunks per tile
   const int ntiles = (int)((p.n_loc + BM - 1) / BM);
-  const int my_tiles = blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
-  const int total = my_tiles * T;            // chunks this CTA consumes (persistent)
+  const int vb = (int)blockIdx.x * G + grp, vgrid = (int)gridDim.x * G;  // virtual block per group
+  const int my_tiles = vb < ntiles ? (ntiles - 1 - vb) / vgrid + 1 : 0;
+  const int total = my_tiles * T;            // chunks this group consumes (persistent)
 
-  if (tid == 0) {
+  if (gtid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NCW);
@@ -132,14 +150,16 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
     s_sqnS[n] = p.sqnS[n];
     s_idS[n] = p.idS[n];
   }
+  if (tid < 64) s_exp2[tid] = exp2((double)tid / 64.0);
+  if (tid == 0) s_go = (G == 1);
   __syncthreads();
 
-  // ---- producer (thread 0): issue chunk `issued` when its stage is free and, for
+  // ---- producer (thread 0 of the group): issue chunk `issued` when its stage is free and, for
   // phase-2 chunks of tile k, once that tile's G is parked (parked > k).
   int issued = 0;      // meaningful in thread 0 only
   int parked = 0;      // tiles whose G has been parked (CTA-uniform)
   auto pump = [&](int done_w0) {
-    if (tid != 0) return;
+    if (gtid != 0) return;
     while (issued < total && issued < done_w0 + S) {
       const int k = issued / T, c = issued - k * T;
       if (c >= nX + nFk && parked <= k) break;
@@ -147,7 +167,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
       if (issued >= S) mbar_wait(&empty[s], ((issued / S) & 1) ^ 1);
       unsigned char* As = stages + s * C::STAGE;
       unsigned char* Bs = As + C::A_BYTES;
-      const int r0 = (int)((blockIdx.x + (int64_t)k * gridDim.x) * BM);
+      const int r0 = (int)((vb + (int64_t)k * vgrid) * BM);
       mbar_arrive_expect_tx(&full[s], C::STAGE);
       if (c < nX) {
         tma_load_2d(As, &tmX, 16 * c, r0, &full[s]);
@@ -162,6 +182,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
       ++issued;
     }
   };
+  if (G > 1 && grp == 1) {  // offset group 1 so the two groups' non-DMMA phases interleave
+    if (gtid == 0)
+      while (!s_go) __nanosleep(200);
+    named_bar_sync(1 + grp, GT);
+  }
   pump(0);
 
   const int g = lane >> 2, t = lane & 3;
@@ -251,6 +276,15 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
     }
   };
 
+  // Optional phase timing (warp 0 lane 0 clocks; debug only).
+  unsigned long long tclk = clock64();
+  auto mark = [&](int ph) {
+    if (p.phase_clk && tid == 0) {
+      const unsigned long long now = clock64();
+      p.phase_clk[(size_t)blockIdx.x * 8 + ph] += now - tclk;
+      tclk = now;
+    }
+  };
   int cons = 0;  // chunks consumed by this warp so far (CTA-uniform in practice)
   auto consume = [&](auto&& body) {
     const int s = cons % S;
@@ -265,7 +299,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
 
 #pragma unroll 1
   for (int k = 0; k < my_tiles; ++k) {
-    const int tile = (int)blockIdx.x + k * (int)gridDim.x;
+    const int tile = vb + k * vgrid;
     const int64_t tile_row0 = (int64_t)tile * BM;
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr)
@@ -278,37 +312,66 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
       if constexpr (GRAM) consume([&](uint32_t so) { mma_stage(so, 0); });
       else consume([&](uint32_t so) { dist_stage(so); });
     }
+    mark(0);
+    if (p.phase_clk) {  // debug: wait for every outstanding DMMA before timing the transform
+      double s = 0.0;
+#pragma unroll
+      for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+        for (int q = 0; q < NFW; ++q) s += acc[fr][q][0] + acc[fr][q][1];
+      if (s == 1.2345e300) p.phase_clk[0] = 1;
+      mark(6);
+    }
     // ---- acc (Gram dot / distance) -> -A(R, S) ------------------------------------
+    // Rolled over the warp's column fragments: each pass transforms fragment 0 and
+    // rotates the accumulator array by one fragment, so the code stays small
+    // (one fragment's epilogue) while acc never leaves registers.
     {
       // exponent = D * (-0.5 / sigma^2) (Gaussian) or D * (-1 / sigma) (l1): one multiply
       // instead of the reference's division, <= 1 ulp apart (kernel values agree to 1e-15).
-      const double escale = (!GRAM && p.kind == kL1) ? -1.0 / p.sigma : -0.5 / (p.sigma * p.sigma);
+      const double escale = p.escale;
+      double sqr[2], gid[2];
+      bool rin[2];
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) {
         const int64_t grow = tile_row0 + arow[fr];
-        const bool rin = grow < p.n_loc;
-        const double sqr = rin ? p.sqn[grow] : 0.0;
-        const double gid = (double)(p.row0 + grow);
+        rin[fr] = grow < p.n_loc;
+        sqr[fr] = rin[fr] ? p.sqn[grow] : 0.0;
+        gid[fr] = (double)(p.row0 + grow);
+      }
+      mark(7);
+#pragma unroll 1
+      for (int it = 0; it < NFW; ++it) {
 #pragma unroll
-        for (int q = 0; q < NFW; ++q) {
+        for (int v = 0; v < 2; ++v) {
+          const int col = 8 * (wc * NFW + it) + 2 * t + v;
+          const double sqc = s_sqnS[col], idc = s_idS[col];
 #pragma unroll
-          for (int v = 0; v < 2; ++v) {
-            const int col = 8 * (wc * NFW + q) + 2 * t + v;
-            double val = 0.0;
-            if (col < m && rin) {
-              double dd = acc[fr][q][v];
-              if (GRAM) {
-                dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr), s_sqnS[col]);
-                if (dd < 0.0) dd = 0.0;
-                if (gid == s_idS[col]) dd = 0.0;
-              }
-              val = exp_compact(dd * escale);
+          for (int fr = 0; fr < 2; ++fr) {
+            double dd = acc[fr][0][v];
+            if (GRAM) {
+              dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr[fr]), sqc);
+              dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
             }
-            acc[fr][q][v] = -val;
+            const double val = exp_tab(dd * escale, s_exp2);
+            acc[fr][0][v] = (col < m && rin[fr]) ? -val : 0.0;
           }
+        }
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr) {
+          const double t0 = acc[fr][0][0], t1 = acc[fr][0][1];
+#pragma unroll
+          for (int q = 0; q + 1 < NFW; ++q) {
+            acc[fr][q][0] = acc[fr][q + 1][0];
+            acc[fr][q][1] = acc[fr][q + 1][1];
+          }
+          acc[fr][NFW - 1][0] = t0;
+          acc[fr][NFW - 1][1] = t1;
         }
       }
     }
+    if (G > 1 && grp == 0 && k == 0 && gtid == 0) s_go = 1;
+    mark(1);
     // ---- phase 1b: residual GEMM F(R,:) F(S,:)^T (F tiles) ---------------------------
 #pragma unroll 1
     for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0); });
@@ -329,6 +392,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
       continue;
     }
 
+    mark(2);
     // ---- park G = -acc in F(R, kcur:kcur+m) for phase 2 --------------------------
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr) {
@@ -344,10 +408,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
         }
     }
     fence_proxy_async_global();
-    __syncthreads();
+    gsync();
     parked = k + 1;
     if (warp == 0) pump(cons);
 
+    mark(3);
     // ---- phase 2: G L^{-T} ------------------------------------------------------------
 #pragma unroll 1
     for (int j = 0; j < nL; ++j) {
@@ -357,6 +422,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
       consume([&](uint32_t so) { mma_stage_tri(so, q_lo); });
     }
 
+    mark(4);
     // ---- epilogue ------------------------------------------------------------------
     double rs[2] = {0.0, 0.0};
 #pragma unroll
@@ -379,26 +445,27 @@ __global__ void __launch_bounds__(UCfg<WC, NFW>::NT, MINB)
       rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 2);
       if (t == 0) s_rown[wc * BM + arow[fr]] = rs[fr];
     }
-    __syncthreads();
-    if (tid < BM) {
-      const int64_t grow = tile_row0 + tid;
+    gsync();
+    if (gtid < BM) {
+      const int64_t grow = tile_row0 + gtid;
       double s2 = 0.0;
 #pragma unroll
-      for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + tid]);
+      for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + gtid]);
       if (grow < p.n_loc) {
         const double un = __dsub_rn(p.u[grow], s2);
         p.u[grow] = un < 0.0 ? 0.0 : un;
       } else {
         s2 = 0.0;
       }
-      s_rowg2[tid] = s2;
+      s_rowg2[gtid] = s2;
     }
-    __syncthreads();
-    if (tid == 0) {
+    gsync();
+    if (gtid == 0) {
       double s2 = 0.0;
       for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
       p.tile_g2[tile] = s2;
     }
+    mark(5);
   }
 }
 
@@ -445,12 +512,12 @@ inline int num_sms() {
   return n;
 }
 
-template <int WC, int NFW, bool GRAM, int MINB>
+template <int WC, int NFW, bool GRAM, int MINB, int G>
 int launch_t(const UpdateParams& p, cudaStream_t st) {
-  using C = UCfg<WC, NFW>;
+  using C = UCfg<WC, NFW, G>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(update_kernel<WC, NFW, GRAM, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(update_kernel<WC, NFW, GRAM, MINB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::SMEM) != cudaSuccess)
       return -2;
     attr = true;
@@ -465,9 +532,9 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
   if (!ok) return -3;
   // persistent: one CTA per SM, tiles strided by the grid (p.tile_g2 is per tile)
   const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
-  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, (int64_t)MINB * num_sms());
+  const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)MINB * num_sms());
   if (grid)
-    update_kernel<WC, NFW, GRAM, MINB><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
+    update_kernel<WC, NFW, GRAM, MINB, G><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
   return C::BM;
 }
 
