@@ -508,10 +508,12 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
     launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, (int)(kcur & 1),
                     linv.as<double>(), st);
-    launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, (int)kcur, (int)dpad,
+    launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, 0, (int)dpad,
                            xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
                            idS.as<double>(), st, &d_sweep->m);
-    launches += 2;
+    launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), prop.as<double>(), lay, pos.as<int>(),
+                  &d_sweep->m, b, (int)kcur, fs.as<double>(), ldf, st);
+    launches += 3;
     CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),

@@ -105,6 +105,12 @@ struct UpdateParams {
 int update_tile_rows(int m);
 // Launch; returns the tile height, or < 0 on failure (-1 unsupported m, -2 smem attr, -3 TMA map).
 int launch_update(const UpdateParams& p, cudaStream_t st);
+// B'[perm_row(n)][k] = -(L^{-1} F_S)[n][k] for k < kcur (the residual GEMM's B operand with
+// the triangular solve folded in); linv_rm as written by launch_linv*, F_S rows from the
+// proposal records of the accepted positions.  *m_dev = accepted count (<= m_max).
+void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* prop,
+                   RecordLayout lay, const int* pos, const int* m_dev, int m_max, int kcur,
+                   double* bp, int64_t ldbp, cudaStream_t st);
 // Gathers the accepted pivots' X rows, F rows (first kcur columns), norms and ids from the
 // proposal records into the update kernel's operand buffers (rows at perm_row(n), n < nb).
 void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,

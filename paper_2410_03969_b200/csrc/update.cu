@@ -65,4 +65,53 @@ void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos
                                              ldfs, sqnS, idS);
 }
 
+// Tiled C[8 x 128] = L^{-1}[8 rows, :m] * F_S[:m, 128 columns]; each output summed over
+// c ascending (deterministic), negated.
+__global__ void __launch_bounds__(256) bprime_kernel(const double* __restrict__ linv_rm,
+                                                     int64_t ldl, int koff,
+                                                     const double* __restrict__ prop,
+                                                     RecordLayout lay, const int* __restrict__ pos,
+                                                     const int* __restrict__ m_dev, int kcur,
+                                                     double* __restrict__ bp, int64_t ldbp) {
+  __shared__ double sL[8][257];
+  __shared__ double sF[16][129];
+  const int m = *m_dev;
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int n = blockIdx.y * 8 + ty;
+  const int k0 = blockIdx.x * 128;
+  for (int i = threadIdx.x; i < 8 * m; i += 256) {
+    const int r = i / m, c = i % m;
+    sL[r][c] = linv_rm[(int64_t)perm_row(blockIdx.y * 8 + r) * ldl + c + koff];
+  }
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int c0 = 0; c0 < m; c0 += 16) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < 16 * 128; i += 256) {
+      const int cc = i >> 7, kk = i & 127;
+      const int c = c0 + cc, k = k0 + kk;
+      sF[cc][kk] = (c < m && k < kcur) ? prop[(int64_t)pos[c] * lay.rec + lay.foff + k] : 0.0;
+    }
+    __syncthreads();
+    const int cend = min(16, m - c0);
+    for (int cc = 0; cc < cend; ++cc) {
+      const double l = sL[ty][c0 + cc];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[j] = fma(l, sF[cc][tx + 32 * j], acc[j]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int k = k0 + tx + 32 * j;
+    if (k < kcur) bp[(int64_t)perm_row(n) * ldbp + k] = -acc[j];
+  }
+}
+
+void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* prop,
+                   RecordLayout lay, const int* pos, const int* m_dev, int m_max, int kcur,
+                   double* bp, int64_t ldbp, cudaStream_t st) {
+  if (kcur <= 0 || m_max <= 0) return;
+  dim3 grid((unsigned)((kcur + 127) / 128), (unsigned)((m_max + 7) / 8));
+  bprime_kernel<<<grid, 256, 0, st>>>(linv_rm, ldl, koff, prop, lay, pos, m_dev, kcur, bp, ldbp);
+}
+
 }  // namespace rpcb

@@ -3,12 +3,12 @@
 //
 // For the accepted pivots S (m columns) of a round it computes, without ever
 // materialising the N x m kernel panel in HBM:
-//   phase 1  acc  = -A(R, S)                      (K5: kernel columns, fused)
-//            acc += F(R, :kcur) F(S, :kcur)^T     (K6: FP64 DMMA GEMM)
-//            G    = -acc = A(R,S) - F F_S^T       (rpcholesky.hpp:378-383)
-//            G is parked in its final place F(R, kcur:kcur+m) (L2-resident)
-//   phase 2  G   <- G L^{-T}: DMMA GEMM whose A operand is G streamed back by TMA
-//            (right_solve_lower_transposed, rpcholesky.hpp:147-151, 384)
+//   phase 0  A(R, S) kernel columns in registers (K5, fused), parked in its final
+//            place F(R, kcur:kcur+m) (L2-resident)
+//   phase 1  acc  = F(R, :kcur) B'^T,  B' = -L^{-1} F(S, :kcur)   (K6: FP64 DMMA GEMM)
+//   phase 2  acc += A(R, S) L^{-T}: DMMA GEMM whose A operand is streamed back by TMA
+//            so acc = A L^{-T} - F (L^{-1} F_S)^T = (A - F F_S^T) L^{-T}
+//            (rpcholesky.hpp:378-384: residual GEMM + right_solve_lower_transposed)
 //   epilogue F(R, kcur:kcur+m) = G ; u(R) = max(u - rowwise||G||^2, 0) ;
 //            per-tile ||G||_F^2 partial                  (rpcholesky.hpp:385-388)
 // Kernel columns (oracle.hpp:71-90, kernels.hpp:60-64): the Gaussian Gram term
@@ -372,10 +372,6 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     }
     if (G > 1 && grp == 0 && k == 0 && gtid == 0) s_go = 1;
     mark(1);
-    // ---- phase 1b: residual GEMM F(R,:) F(S,:)^T (F tiles) ---------------------------
-#pragma unroll 1
-    for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0); });
-
     if (p.columns_only) {  // standalone K5: A(R, S) -> column-major output
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) {
@@ -392,8 +388,9 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       continue;
     }
 
-    mark(2);
-    // ---- park G = -acc in F(R, kcur:kcur+m) for phase 2 --------------------------
+    // ---- park A(R, S) in F(R, kcur:kcur+m): phase 2 streams it back as the A operand
+    // of A L^{-T}.  Parking right after the transform lets the TMA round trip hide
+    // behind the residual GEMM instead of stalling the end of the tile.
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr) {
       const int64_t grow = tile_row0 + arow[fr];
@@ -411,12 +408,17 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     gsync();
     parked = k + 1;
     if (warp == 0) pump(cons);
+    mark(2);
+    // ---- phase 1b: acc = F(R,:) B'^T with B' = -L^{-1} F(S,:)  (K = kcur) -------------
+    //   G L^{-T} = (A - F F_S^T) L^{-T} = A L^{-T} + F (-L^{-1} F_S)^T
+#pragma unroll 1
+    for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0); });
 
     mark(3);
-    // ---- phase 2: G L^{-T} ------------------------------------------------------------
+    // ---- phase 2: acc += A L^{-T}  (K = m, A streamed back from F) --------------------
 #pragma unroll 1
     for (int j = 0; j < nL; ++j) {
-      // chunk j covers G columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
+      // chunk j covers A columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
       // so fragments whose 8 columns all lie below 16j - koff contribute nothing.
       const int q_lo = max(0, (16 * j - koff) / 8 - wc * NFW);
       consume([&](uint32_t so) { mma_stage_tri(so, q_lo); });
