@@ -485,8 +485,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.lay = lay;
       sp.records = recv.as<double>() + (size_t)s.gidx * b * lay.rec;
       sp.owner = owner.as<int>();
+      // every shard runs the sampler, including shards without rows: it also fills the
+      // replicated owner[] table that the proposal selection reads
       if (replay) launch_replay_sample(sp, cumsum.as<double>(), st);
-      else if (s.n_loc > 0) launch_sample(sp, st);
+      else launch_sample(sp, st);
       dbg(st, "sample");
       ++launches;
     }

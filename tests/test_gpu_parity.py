@@ -270,8 +270,8 @@ def test_invalid_arguments(ctx):
 
 
 # --------------------------------------------------------------- sharding
-@pytest.mark.parametrize("p", [2, 3, 5])
-def test_virtual_shards_p_invariance(p):
+@pytest.mark.parametrize("p", [2, 3, 5, 7])
+def test_virtual_shards_p_invariance(p):  # p = 7: shards 5 and 6 own no rows
     x = wl.gen_c1(20000, 10, 0)
     cfg = api.RunConfig.until_rank(200, 40, 0)
     ko = api.KernelOracle(x, api.KernelSpec("gaussian", math.sqrt(10.0)))
