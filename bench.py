@@ -110,15 +110,16 @@ def ncu_traffic(config_name):
         return None
 
 
-def cpu_sample(w, threads: int, n_sample: int):
+def cpu_sample(w, threads: int, n_sample: int, lowmem: bool = False):
     """Oracle restatement (oracle/, test infrastructure) on N' = n_sample points of
     the same workload; returns (seconds at N', extrapolated seconds at N)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as po
     x = w.points(n_sample)
     o = po.Oracle(x=x, kernel=w.kernel, sigma=w.sigma, n_threads=threads)
+    fn = po.accelerated_rpcholesky_lowmem if lowmem else po.accelerated_rpcholesky
     t0 = time.perf_counter()
-    po.accelerated_rpcholesky(o, block_size=w.b, target_rank=w.k, seed=w.seed)
+    fn(o, block_size=w.b, target_rank=w.k, seed=w.seed)
     dt = time.perf_counter() - t0
     return dt, dt * (w.n / n_sample)
 
@@ -171,6 +172,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="N' for the CPU sample (0=auto)")
+    ap.add_argument("--variant", default="standard", choices=["standard", "lowmem"],
+                    help="lowmem: accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485)")
     args = ap.parse_args()
 
     from paper_2410_03969_b200 import workloads
@@ -182,6 +185,10 @@ def main():
                 "n": w.n, "d": w.d, "k": w.k, "b": w.b, "kernel": w.kernel,
                 "parallelism": f"row-shard{world}" if world > 1 else "single-gpu",
                 "l2": "inputs larger than L2 (F alone is >= 1.8 GB at C2-C5)"}
+    lowmem = args.variant == "lowmem"
+    if lowmem:
+        cfg_json["variant"] = "lowmem (no N x k factor; A(R, S_all) regenerated per round)"
+        cfg_json["l2"] = "X and u larger than L2 at C2-C5; the kernel block never leaves the SM"
 
     if args.impl == "reference":
         if rank != 0:
@@ -226,8 +233,8 @@ def main():
         torch.cuda.synchronize()
 
     def one_step():
-        return api.accelerated_rpcholesky_device(x_dev.data_ptr(), w.n, w.d, w.d, L.RPC_ROW_MAJOR,
-                                                 spec, cfg, ctx)
+        fn = api.accelerated_rpcholesky_lowmem_device if lowmem else api.accelerated_rpcholesky_device
+        return fn(x_dev.data_ptr(), w.n, w.d, w.d, L.RPC_ROW_MAJOR, spec, cfg, ctx)
 
     for _ in range(args.warmup):
         one_step().free()
@@ -254,13 +261,13 @@ def main():
     flops = timing["update_flops"]
     peak, peak_src = fp64_peak()
     achieved = flops / (upd_ms * 1e-3) / 1e12 if upd_ms > 0 else 0.0
-    tr = ncu_traffic(w.name)
+    tr = ncu_traffic(w.name + ("_lowmem" if lowmem else ""))
     traffic = tr["bytes_per_launch_mean"] if tr else None
     traffic_note = tr.get("note") if tr else None
 
     # kernel-col GB/s: standalone K5 on this run's accepted blocks (rank 0 only)
     col_gbs = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not lowmem:
         rr = one_step()
         ko = api.KernelOracle(x, spec)
         tot_ms, cols_total = 0.0, 0
@@ -277,20 +284,29 @@ def main():
     e2e = None
     if not args.no_e2e:
         xh = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
-        fout = torch.empty((nr * max(k_final, 1) + 16,), dtype=torch.float64).pin_memory().numpy()
+        fout = torch.empty((nr * max(k_final, 1) + k_final * k_final + nr + 16,),
+                           dtype=torch.float64).pin_memory().numpy()
         ko = api.KernelOracle(xh, spec)
         e2e_times = []
         for i in range(1 + min(args.steps, 3)):
             barrier()
             t0 = time.perf_counter()
-            res = api.accelerated_rpcholesky(ko, cfg, ctx)
-            kk = res.rank
-            lib = L.load()
-            # rows owned by this rank, column-major with ld = nr
             import ctypes as C
-            buf = np.ndarray((nr, kk), dtype=np.float64, buffer=fout, order="F")
-            L.check(lib.rpc_result_factor_copy(res._handle, C.c_void_p(buf.ctypes.data - r0 * 8),
-                                               nr, L.RPC_COL_MAJOR), ctx.handle)
+            lib = L.load()
+            if lowmem:  # LowMemResult: chol_factor + residual diagonal out
+                res = api.accelerated_rpcholesky_lowmem(ko, cfg, ctx)
+                kk = res.rank
+                L.check(lib.rpc_result_chol_copy(res._handle, C.c_void_p(fout.ctypes.data)),
+                        ctx.handle)
+                L.check(lib.rpc_result_residual_diag_copy(
+                    res._handle, C.c_void_p(fout.ctypes.data + 8 * (kk * kk - r0))), ctx.handle)
+            else:
+                res = api.accelerated_rpcholesky(ko, cfg, ctx)
+                kk = res.rank
+                # rows owned by this rank, column-major with ld = nr
+                buf = np.ndarray((nr, kk), dtype=np.float64, buffer=fout, order="F")
+                L.check(lib.rpc_result_factor_copy(res._handle, C.c_void_p(buf.ctypes.data - r0 * 8),
+                                                   nr, L.RPC_COL_MAJOR), ctx.handle)
             barrier()
             dt = time.perf_counter() - t0
             res.free()
@@ -299,14 +315,15 @@ def main():
         tt = torch.tensor([statistics.median(e2e_times)], dtype=torch.float64, device=dev)
         if dist is not None:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        d2h = (k_final * k_final * 8 + nr * 8 + k_final * 8) if lowmem else \
+            (nr * k_final * 8 + k_final * 8 + k_final * k_final * 8)
         e2e = {"value": float(tt.item()), "unit": "s",
-               "h2d_bytes_per_step": int(nr * w.d * 8),
-               "d2h_bytes_per_step": int(nr * k_final * 8 + k_final * 8 + k_final * k_final * 8)}
+               "h2d_bytes_per_step": int(nr * w.d * 8), "d2h_bytes_per_step": int(d2h)}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        n_sample = args.cpu_sample or min(w.n, 100_000)
-        dt, ext = cpu_sample(w, n_cores, n_sample)
+        n_sample = args.cpu_sample or min(w.n, 10_000 if lowmem else 100_000)
+        dt, ext = cpu_sample(w, n_cores, n_sample, lowmem)
         cpu = {"value": ext, "unit": "s", "cores": n_cores, "kind": "port",
                "sample": f"oracle restatement on the first N'={n_sample} rows of {w.name}, same "
                          f"k/b/seed, {dt:.2f} s measured, x N/N' to the full N"}
@@ -326,7 +343,9 @@ def main():
                                                          "upload_ms")},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak if peak else None, "traffic": traffic,
-                         "kernel": "update_kernel (fused K5 kernel columns + K6 FP64 DMMA GEMM + L^-T + diag update)",
+                         "kernel": ("lowmem_kernel (A(R, S_all) regenerated in SMEM + FP64 DMMA GEMM with "
+                                    "the new L^-1 rows + diag update)") if lowmem else
+                                   "update_kernel (fused K5 kernel columns + K6 FP64 DMMA GEMM + L^-T + diag update)",
                          "traffic_note": traffic_note,
                          "peak_source": peak_src,
                          "per_launch_flops": flops / max(1, timing["update_launches"]),

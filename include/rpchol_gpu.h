@@ -109,6 +109,22 @@ int rpc_accelerated_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t
                                       int64_t ldx, int layout, rpc_kernel_spec kernel,
                                       rpc_run_config cfg, rpc_result** out);
 
+/* ---- low-memory variant ------------------------------------------------- */
+/* accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485; LowMemResult 114-119):
+ * same pivots, trace and stopping rules as the standard call; keeps O(N + k^2)
+ * state (X, u, pivots, L, L^{-1}) and never stores the N x k factor.  The result
+ * handle answers rank / pivots / chol_copy / residual_diag_copy / round /
+ * rank_exhausted / surplus / captured_sq; rpc_result_factor_copy fails with
+ * RPC_EINVAL and rpc_result_factor_device returns NULL.  This build: d <= 128. */
+int rpc_accelerated_rpcholesky_lowmem(rpc_ctx* ctx, const double* x, int64_t n, int64_t d,
+                                      int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                      rpc_run_config cfg, rpc_result** out);
+int rpc_accelerated_rpcholesky_lowmem_device(rpc_ctx* ctx, const double* x_dev, int64_t n,
+                                             int64_t d, int64_t ldx, int layout,
+                                             rpc_kernel_spec kernel, rpc_run_config cfg,
+                                             rpc_result** out);
+int rpc_result_is_lowmem(const rpc_result* r);
+
 /* ---- result (CholeskyResult, rpcholesky.hpp:106-110) --------------------- */
 int64_t rpc_result_n(const rpc_result* r);
 int64_t rpc_result_rank(const rpc_result* r); /* factor columns = |pivots| */

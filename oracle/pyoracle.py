@@ -95,6 +95,8 @@ def lib() -> C.CDLL:
                                           C.POINTER(C.c_int64), C.c_void_p]
         L.rpo_accelerated_rpcholesky_bounded.argtypes = [C.POINTER(_Oracle), C.POINTER(_Cfg),
                                                          C.c_int64, C.POINTER(_Res)]
+        L.rpo_accelerated_rpcholesky_lowmem.argtypes = [C.POINTER(_Oracle), C.POINTER(_Cfg),
+                                                        C.POINTER(_Res)]
         L.rpo_result_free.argtypes = [C.POINTER(_Res)]
         L.rpo_relative_trace_error.restype = C.c_double
         L.rpo_relative_trace_error.argtypes = [C.POINTER(_Oracle), C.c_void_p, C.c_int64,
@@ -207,20 +209,17 @@ class Result:
 
     @property
     def rank(self) -> int:
-        return self.factor.shape[1]
+        return len(self.pivots)
 
 
-def accelerated_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "until_rank",
-                           rounds: int = 0, target_rank: int = 0, seed: int = 0,
-                           stop_tol: float = 0.0, max_rounds: int = -1) -> Result:
-    cfg = _Cfg(block_size, MODES[mode], rounds, target_rank, seed, stop_tol)
-    res = _Res()
-    _check(lib().rpo_accelerated_rpcholesky_bounded(C.byref(oracle._o), C.byref(cfg),
-                                                    max_rounds, C.byref(res)))
+def _unpack(res) -> Result:
     try:
         n, k, b, nr = res.n, res.rank, res.block_size, res.n_rounds
-        factor = np.ctypeslib.as_array(res.factor, shape=(k * n,)).reshape(n, k, order="F").copy() \
-            if k else np.zeros((n, 0), order="F")
+        if not res.factor:
+            factor = None  # LowMemResult
+        else:
+            factor = np.ctypeslib.as_array(res.factor, shape=(k * n,)).reshape(n, k, order="F").copy() \
+                if k else np.zeros((n, 0), order="F")
         pivots = np.ctypeslib.as_array(res.pivots, shape=(k,)).copy() if k else np.zeros(0, np.int64)
         chol = np.ctypeslib.as_array(res.chol, shape=(k * k,)).reshape(k, k, order="F").copy() \
             if k else np.zeros((0, 0))
@@ -237,6 +236,26 @@ def accelerated_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "unti
                       bool(res.rank_exhausted), int(res.surplus), float(res.captured_sq))
     finally:
         lib().rpo_result_free(C.byref(res))
+
+
+def accelerated_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "until_rank",
+                           rounds: int = 0, target_rank: int = 0, seed: int = 0,
+                           stop_tol: float = 0.0, max_rounds: int = -1) -> Result:
+    cfg = _Cfg(block_size, MODES[mode], rounds, target_rank, seed, stop_tol)
+    res = _Res()
+    _check(lib().rpo_accelerated_rpcholesky_bounded(C.byref(oracle._o), C.byref(cfg),
+                                                    max_rounds, C.byref(res)))
+    return _unpack(res)
+
+
+def accelerated_rpcholesky_lowmem(oracle: Oracle, *, block_size: int, mode: str = "until_rank",
+                                  rounds: int = 0, target_rank: int = 0, seed: int = 0,
+                                  stop_tol: float = 0.0) -> Result:
+    """rpcholesky.hpp:408-485; Result.factor is None (LowMemResult)."""
+    cfg = _Cfg(block_size, MODES[mode], rounds, target_rank, seed, stop_tol)
+    res = _Res()
+    _check(lib().rpo_accelerated_rpcholesky_lowmem(C.byref(oracle._o), C.byref(cfg), C.byref(res)))
+    return _unpack(res)
 
 
 def relative_trace_error(oracle: Oracle, factor: np.ndarray) -> float:

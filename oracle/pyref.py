@@ -32,6 +32,7 @@ def lib():
         L.ref_last_error.restype = C.c_char_p
         L.ref_accelerated_kernel.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, i64, C.c_int, i64,
                                              i64, C.c_uint64, d, C.POINTER(po._Res)]
+        L.ref_lowmem_kernel.argtypes = L.ref_accelerated_kernel.argtypes
         L.ref_accelerated_dense.argtypes = [vp, i64, i64, C.c_int, i64, i64, C.c_uint64, d,
                                             C.POINTER(po._Res)]
         L.ref_relative_trace_error_kernel.restype = d
@@ -53,7 +54,8 @@ def _check(rc):
 def _unpack(res) -> po.Result:
     try:
         n, k, b, nr = res.n, res.rank, res.block_size, res.n_rounds
-        f = np.ctypeslib.as_array(res.factor, shape=(max(n * k, 1),))[: n * k].reshape(n, k, order="F").copy()
+        f = (np.ctypeslib.as_array(res.factor, shape=(max(n * k, 1),))[: n * k]
+             .reshape(n, k, order="F").copy() if res.factor else None)
         piv = np.ctypeslib.as_array(res.pivots, shape=(max(k, 1),))[:k].copy()
         chol = np.ctypeslib.as_array(res.chol, shape=(max(k * k, 1),))[: k * k].reshape(k, k, order="F").copy()
         resid = np.ctypeslib.as_array(res.residual_diag, shape=(n,)).copy()
@@ -78,6 +80,20 @@ def accelerated_rpcholesky_kernel(x, kernel, sigma, *, block_size, mode="until_r
     _check(lib().ref_accelerated_kernel(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm,
                                         block_size, po.MODES[mode], rounds, target_rank, seed,
                                         stop_tol, C.byref(res)))
+    return _unpack(res)
+
+
+def accelerated_rpcholesky_lowmem_kernel(x, kernel, sigma, *, block_size, mode="until_rank",
+                                         rounds=0, target_rank=0, seed=0, stop_tol=0.0,
+                                         dist=None) -> po.Result:
+    """accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485); .factor is None."""
+    xf = np.asfortranarray(x, dtype=np.float64)
+    kind = po.KERNELS[kernel]
+    dm = po.DIST[dist or ("direct" if kind == 1 else "gram")]
+    res = po._Res()
+    _check(lib().ref_lowmem_kernel(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm,
+                                   block_size, po.MODES[mode], rounds, target_rank, seed,
+                                   stop_tol, C.byref(res)))
     return _unpack(res)
 
 

@@ -124,6 +124,38 @@ int ref_accelerated_dense(const double* a, int64_t n, int64_t b, int mode, int64
   }
 }
 
+// accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485): factor = NULL, rank = |pivots|.
+int ref_lowmem_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                      int64_t b, int mode, int64_t rounds, int64_t k, uint64_t seed,
+                      double stop_tol, Res* out) {
+  try {
+    auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+    auto r = rpchol::accelerated_rpcholesky_lowmem(oracle, make_cfg(b, mode, rounds, k, seed, stop_tol));
+    std::memset(out, 0, sizeof *out);
+    out->n = n;
+    out->rank = (int64_t)r.pivots.size();
+    std::vector<int64_t> piv(r.pivots.begin(), r.pivots.end());
+    out->pivots = dup(piv.data(), piv.size());
+    out->chol = dup(r.chol_factor.data(), (size_t)(r.chol_factor.rows() * r.chol_factor.cols()));
+    out->residual_diag = dup(r.residual_diag.data(), (size_t)r.residual_diag.size());
+    out->n_rounds = (int64_t)r.trace.rounds.size();
+    out->block_size = b;
+    std::vector<int64_t> prop, cnt;
+    for (const auto& rr : r.trace.rounds) {
+      prop.insert(prop.end(), rr.proposed.begin(), rr.proposed.end());
+      cnt.push_back((int64_t)rr.accepted.size());
+    }
+    out->proposed = dup(prop.data(), prop.size());
+    out->accepted_count = dup(cnt.data(), cnt.size());
+    out->rank_exhausted = r.trace.rank_exhausted ? 1 : 0;
+    out->surplus = r.trace.surplus;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
 double ref_relative_trace_error_kernel(const double* x, int64_t n, int64_t d, int kind,
                                        double sigma, int dist, const double* factor, int64_t k) {
   auto oracle = make_kernel(x, n, d, kind, sigma, dist);

@@ -527,6 +527,231 @@ int rpo_accelerated_rpcholesky(const rpo_oracle* o, const rpo_run_config* cfg, r
   return rpo_accelerated_rpcholesky_bounded(o, cfg, -1, res);
 }
 
+/* ---- rpcholesky.hpp:408-485  accelerated_rpcholesky_lowmem ---------- */
+/* Forward substitution L y = w in place for nc columns (L: k x k column-major lower,
+ * w: k x nc column-major with leading dimension ldw) — triangularView<Lower>::solveInPlace. */
+static void lower_solve_inplace(const double* l, int64_t k, double* w, int64_t ldw, int64_t nc) {
+  for (int64_t c = 0; c < nc; ++c) {
+    double* y = w + c * ldw;
+    for (int64_t i = 0; i < k; ++i) {
+      double s = y[i];
+      for (int64_t j = 0; j < i; ++j) s -= l[j * k + i] * y[j];
+      y[i] = s / l[i * k + i];
+    }
+  }
+}
+
+int rpo_accelerated_rpcholesky_lowmem(const rpo_oracle* o, const rpo_run_config* cfg,
+                                      rpo_result* res) {
+  memset(res, 0, sizeof *res);
+  const int64_t n = o->n;
+  const int64_t b = cfg->block_size;
+  const int nt = o->n_threads;
+  if (b < 1) return fail(RPO_EINVAL, "accelerated_rpcholesky_lowmem: block size must be >= 1");
+  if (cfg->mode == RPO_MODE_FIXED_ROUNDS && cfg->rounds < 1)
+    return fail(RPO_EINVAL, "RunConfig: t, b must be >= 1");
+  if (cfg->mode == RPO_MODE_UNTIL_RANK && cfg->target_rank < 1)
+    return fail(RPO_EINVAL, "RunConfig: k, b must be >= 1");
+  double* u = (double*)malloc(sizeof(double) * (size_t)n);
+  double* cumsum = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!u || !cumsum) {
+    free(u);
+    free(cumsum);
+    return fail(RPO_ENOMEM, "out of memory");
+  }
+  diag_of(o, u);
+  double trace_a = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (u[i] < 0.0) u[i] = 0.0;
+    trace_a += u[i];
+  }
+  if (!(trace_a > 0.0)) {
+    free(u);
+    free(cumsum);
+    return fail(RPO_EINVAL, "accelerated_rpcholesky_lowmem: trace must be > 0");
+  }
+  int64_t cap = cfg->mode == RPO_MODE_FIXED_ROUNDS ? cfg->rounds * b : cfg->target_rank + b;
+  if (cap > n) cap = n;
+  if (cap < 1) cap = 1;
+  const int64_t nchunks = (n + b - 1) / b;
+  double* l = (double*)calloc((size_t)(cap * cap), sizeof(double)); /* k x k, ld = k (repacked) */
+  double* lnext = (double*)calloc((size_t)(cap * cap), sizeof(double));
+  int64_t* pivots = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int64_t* s_all = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int64_t* proposed = (int64_t*)malloc(sizeof(int64_t) * (size_t)b);
+  double* h = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  double* w_prop = (double*)malloc(sizeof(double) * (size_t)(cap * b));
+  double* w_acc = (double*)malloc(sizeof(double) * (size_t)(cap * b));
+  int64_t* acc_ids = (int64_t*)malloc(sizeof(int64_t) * (size_t)b);
+  int64_t* acc_pos = (int64_t*)malloc(sizeof(int64_t) * (size_t)b);
+  double* lsel = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  double* chunk_g2 = (double*)malloc(sizeof(double) * (size_t)nchunks);
+  int64_t rounds_cap = 16;
+  int64_t* all_prop = (int64_t*)malloc(sizeof(int64_t) * (size_t)(rounds_cap * b));
+  int64_t* all_cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)rounds_cap);
+  int rc = RPO_OK;
+  if (!l || !lnext || !pivots || !s_all || !proposed || !h || !w_prop || !w_acc || !acc_ids ||
+      !acc_pos || !lsel || !chunk_g2 || !all_prop || !all_cnt) {
+    rc = fail(RPO_ENOMEM, "out of memory");
+    goto done;
+  }
+  int64_t kold = 0;
+  double captured_sq = 0.0;
+  uint64_t draw = 0;
+  int64_t round;
+  for (round = 0; !run_finished(cfg, round, kold); ++round) {
+    double usum = 0.0;
+    for (int64_t i = 0; i < n; ++i) usum += u[i];
+    if (!(usum > 0.0)) { /* 423-426 */
+      res->rank_exhausted = 1;
+      break;
+    }
+    if (cfg->stop_tol > 0.0 && (trace_a - captured_sq) <= cfg->stop_tol * trace_a) break;
+    rpo_cumulative_sums(u, n, cumsum);
+    for (int64_t j = 0; j < b; ++j) {
+      rc = rpo_sample_discrete(cumsum, n, rpo_u01(rpo_splitmix64_draw(cfg->seed, draw++)),
+                               &proposed[j]);
+      if (rc) goto done;
+    }
+    /* h = A(S', S') - W_prop^T W_prop, W_prop = L^{-1} A(S, S')  (438-445) */
+    if ((rc = rpo_submatrix(o, proposed, b, proposed, b, h))) goto done;
+    if (kold > 0) {
+      if ((rc = rpo_submatrix(o, pivots, kold, proposed, b, w_prop))) goto done;
+      lower_solve_inplace(l, kold, w_prop, kold, b);
+      for (int64_t j = 0; j < b; ++j)
+        for (int64_t i = 0; i < b; ++i) {
+          double s2 = 0.0;
+          for (int64_t t = 0; t < kold; ++t) s2 += w_prop[i * kold + t] * w_prop[j * kold + t];
+          h[j * b + i] -= s2;
+        }
+    }
+    int64_t m = 0;
+    if ((rc = rpo_rejection_sweep(h, b, proposed, cfg->seed, draw, acc_ids, acc_pos, &m, lsel)))
+      goto done;
+    draw += (uint64_t)b;
+    if (m > 0) {
+      if (kold + m > cap) {
+        rc = fail(RPO_ENUMERIC, "accelerated_rpcholesky_lowmem: pivot capacity exceeded");
+        goto done;
+      }
+      /* W_acc = W_prop(:, positions)  (449-455) */
+      for (int64_t j = 0; j < m; ++j)
+        for (int64_t t = 0; t < kold; ++t) w_acc[j * kold + t] = w_prop[acc_pos[j] * kold + t];
+      const int64_t kn = kold + m;
+      for (int64_t t = 0; t < kold; ++t) s_all[t] = pivots[t];
+      for (int64_t j = 0; j < m; ++j) s_all[kold + j] = acc_ids[j];
+      /* diagonal update in row chunks of b (457-468) */
+#pragma omp parallel num_threads(nt)
+      {
+        double* a_chunk = (double*)malloc(sizeof(double) * (size_t)(b * kn));
+        double* y = (double*)malloc(sizeof(double) * (size_t)(kold * b + 1));
+        double* g = (double*)malloc(sizeof(double) * (size_t)(b * m));
+        int64_t* rows = (int64_t*)malloc(sizeof(int64_t) * (size_t)b);
+#pragma omp for schedule(static)
+        for (int64_t ch = 0; ch < nchunks; ++ch) {
+          const int64_t r0 = ch * b;
+          const int64_t ht = (r0 + b <= n) ? b : n - r0;
+          for (int64_t a = 0; a < ht; ++a) rows[a] = r0 + a;
+          rpo_submatrix(o, rows, ht, s_all, kn, a_chunk); /* ht x kn, ld = ht */
+          for (int64_t j = 0; j < m; ++j)
+            for (int64_t a = 0; a < ht; ++a) g[j * ht + a] = a_chunk[(kold + j) * ht + a];
+          if (kold > 0) {
+            /* y = A(S_old, R) solved against L; g -= y^T W_acc */
+            for (int64_t a = 0; a < ht; ++a)
+              for (int64_t t = 0; t < kold; ++t) y[a * kold + t] = a_chunk[t * ht + a];
+            lower_solve_inplace(l, kold, y, kold, ht);
+            for (int64_t j = 0; j < m; ++j)
+              for (int64_t a = 0; a < ht; ++a) {
+                double s2 = 0.0;
+                for (int64_t t = 0; t < kold; ++t) s2 += y[a * kold + t] * w_acc[j * kold + t];
+                g[j * ht + a] -= s2;
+              }
+          }
+          right_solve_lt(lsel, m, g, ht, 1);
+          double gs = 0.0;
+          for (int64_t a = 0; a < ht; ++a) {
+            double s2 = 0.0;
+            for (int64_t j = 0; j < m; ++j) s2 += g[j * ht + a] * g[j * ht + a];
+            u[r0 + a] -= s2;
+          }
+          for (int64_t j = 0; j < m; ++j)
+            for (int64_t a = 0; a < ht; ++a) gs += g[j * ht + a] * g[j * ht + a];
+          chunk_g2[ch] = gs;
+        }
+        free(a_chunk);
+        free(y);
+        free(g);
+        free(rows);
+      }
+      for (int64_t ch = 0; ch < nchunks; ++ch) captured_sq += chunk_g2[ch];
+      /* l_next = [[l, 0], [W_acc^T, L_sel]]  (470-475) */
+      memset(lnext, 0, sizeof(double) * (size_t)(kn * kn));
+      for (int64_t c = 0; c < kold; ++c)
+        for (int64_t r = 0; r < kold; ++r) lnext[c * kn + r] = l[c * kold + r];
+      for (int64_t c = 0; c < kold; ++c)
+        for (int64_t j = 0; j < m; ++j) lnext[c * kn + kold + j] = w_acc[j * kold + c];
+      for (int64_t c = 0; c < m; ++c)
+        for (int64_t j = 0; j < m; ++j) lnext[(kold + c) * kn + kold + j] = lsel[c * m + j];
+      double* tmp = l;
+      l = lnext;
+      lnext = tmp;
+      for (int64_t j = 0; j < m; ++j) pivots[kold + j] = acc_ids[j];
+      kold = kn;
+    }
+    for (int64_t i = 0; i < n; ++i)
+      if (u[i] < 0.0) u[i] = 0.0; /* 478 */
+    if (round >= rounds_cap) {
+      rounds_cap *= 2;
+      int64_t* np = (int64_t*)realloc(all_prop, sizeof(int64_t) * (size_t)(rounds_cap * b));
+      int64_t* nc = (int64_t*)realloc(all_cnt, sizeof(int64_t) * (size_t)rounds_cap);
+      if (!np || !nc) {
+        rc = fail(RPO_ENOMEM, "out of memory");
+        goto done;
+      }
+      all_prop = np;
+      all_cnt = nc;
+    }
+    memcpy(all_prop + round * b, proposed, sizeof(int64_t) * (size_t)b);
+    all_cnt[round] = m;
+  }
+  res->n = n;
+  res->rank = kold;
+  res->block_size = b;
+  res->n_rounds = round;
+  res->factor = NULL; /* LowMemResult has no factor (114-119) */
+  res->pivots = pivots;
+  pivots = NULL;
+  res->chol = l;
+  l = NULL;
+  res->residual_diag = u;
+  u = NULL;
+  res->proposed = all_prop;
+  all_prop = NULL;
+  res->accepted_count = all_cnt;
+  all_cnt = NULL;
+  if (cfg->mode == RPO_MODE_UNTIL_RANK && kold > cfg->target_rank) res->surplus = kold - cfg->target_rank;
+  res->captured_sq = captured_sq;
+done:
+  free(u);
+  free(cumsum);
+  free(l);
+  free(lnext);
+  free(pivots);
+  free(s_all);
+  free(proposed);
+  free(h);
+  free(w_prop);
+  free(w_acc);
+  free(acc_ids);
+  free(acc_pos);
+  free(lsel);
+  free(chunk_g2);
+  free(all_prop);
+  free(all_cnt);
+  if (rc) rpo_result_free(res);
+  return rc;
+}
+
 void rpo_result_free(rpo_result* res) {
   free(res->factor);
   free(res->pivots);

@@ -108,6 +108,10 @@ int rpo_accelerated_rpcholesky(const rpo_oracle* o, const rpo_run_config* cfg,
 /* Run only rounds [0, max_rounds) — bounded CPU-baseline samples. */
 int rpo_accelerated_rpcholesky_bounded(const rpo_oracle* o, const rpo_run_config* cfg,
                                        int64_t max_rounds, rpo_result* res);
+/* accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485): res->factor is NULL, res->chol
+ * is the k x k L of the pivot block, res->rank = |pivots|. */
+int rpo_accelerated_rpcholesky_lowmem(const rpo_oracle* o, const rpo_run_config* cfg,
+                                      rpo_result* res);
 void rpo_result_free(rpo_result* res);
 double rpo_relative_trace_error(const rpo_oracle* o, const double* factor, int64_t n,
                                 int64_t k);

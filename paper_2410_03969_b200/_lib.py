@@ -29,6 +29,8 @@ EXPORTS = [
     "rpc_result_rank_exhausted", "rpc_result_surplus", "rpc_result_captured_sq",
     "rpc_result_relative_trace_error", "rpc_result_factor_device", "rpc_result_timing",
     "rpc_result_free", "rpc_kernel_columns", "rpc_sample_discrete", "rpc_rejection_sweep",
+    "rpc_accelerated_rpcholesky_lowmem", "rpc_accelerated_rpcholesky_lowmem_device",
+    "rpc_result_is_lowmem",
 ]
 
 
@@ -90,6 +92,12 @@ def load() -> C.CDLL:
                                                  RunConfigC, C.POINTER(vp)]),
         "rpc_accelerated_rpcholesky_device": (C.c_int, [vp, vp, i64, i64, i64, C.c_int,
                                                         KernelSpecC, RunConfigC, C.POINTER(vp)]),
+        "rpc_accelerated_rpcholesky_lowmem": (C.c_int, [vp, vp, i64, i64, i64, C.c_int,
+                                                        KernelSpecC, RunConfigC, C.POINTER(vp)]),
+        "rpc_accelerated_rpcholesky_lowmem_device": (C.c_int, [vp, vp, i64, i64, i64, C.c_int,
+                                                               KernelSpecC, RunConfigC,
+                                                               C.POINTER(vp)]),
+        "rpc_result_is_lowmem": (C.c_int, [vp]),
         "rpc_result_n": (i64, [vp]),
         "rpc_result_rank": (i64, [vp]),
         "rpc_result_pivots": (C.c_int, [vp, vp]),

@@ -274,6 +274,36 @@ def accelerated_rpcholesky_device(x_dev_ptr: int, n: int, d: int, ld: int, layou
     return _wrap_result(h, ctx)
 
 
+def accelerated_rpcholesky_lowmem(oracle: KernelOracle, cfg: RunConfig,
+                                  ctx: Context | None = None) -> CholeskyResult:
+    """rpchol::accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485) on the GPU.
+
+    Returns the LowMemResult fields (rpcholesky.hpp:114-119): pivots, chol_factor,
+    residual_diag and the trace; `factor` is not stored (reading it raises ValueError).
+    """
+    if not isinstance(oracle, KernelOracle):
+        raise ValueError("accelerated_rpcholesky_lowmem (B200): only KernelOracle inputs are supported")
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    h = C.c_void_p()
+    L.check(L.load().rpc_accelerated_rpcholesky_lowmem(ctx.handle, x.ctypes.data, x.shape[0],
+                                                       x.shape[1], ld, lay, oracle._c_spec(),
+                                                       cfg.to_c(), C.byref(h)), ctx.handle)
+    return _wrap_result(h, ctx)
+
+
+def accelerated_rpcholesky_lowmem_device(x_dev_ptr: int, n: int, d: int, ld: int, layout: int,
+                                         spec: KernelSpec, cfg: RunConfig, ctx: Context,
+                                         distance_mode: str | None = None) -> CholeskyResult:
+    """Low-memory variant with this process's shard rows already on the device."""
+    o = KernelOracle(np.zeros((1, 1)), spec, distance_mode)
+    h = C.c_void_p()
+    L.check(L.load().rpc_accelerated_rpcholesky_lowmem_device(
+        ctx.handle, C.c_void_p(x_dev_ptr), n, d, ld, layout, o._c_spec(), cfg.to_c(), C.byref(h)),
+        ctx.handle)
+    return _wrap_result(h, ctx)
+
+
 def relative_trace_error(oracle: KernelOracle, result: CholeskyResult) -> float:
     """rpcholesky.hpp:577-583, evaluated from the device-resident factor."""
     return result.relative_trace_error

@@ -203,6 +203,7 @@ struct rpc_result {
   std::vector<int64_t> pivots;
   std::vector<std::vector<int64_t>> proposed, accepted;
   bool exhausted = false;
+  bool lowmem = false;       // accelerated_rpcholesky_lowmem: no factor is kept
   int64_t surplus = 0;
   double captured_sq = 0.0;
   double fro2 = 0.0;
@@ -290,11 +291,18 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 
 // The factorization proper.  `src` points to this process's shard rows (device
 // memory when src_on_device, else host memory of the full X).
+//
+// lowmem: accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485) — the same proposals,
+// sweep and stopping rules, but no N x k factor: the proposals' factor rows come from
+// A(S', S) L^{-T}, and the diagonal update regenerates A(R, S_all) inside the update
+// kernel (lowmem_impl.cuh).  State: X, u, pivot records, L and L^{-1} (k x k).
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
-                       rpc_run_config cfg, rpc_result* res) {
+                       rpc_run_config cfg, rpc_result* res, bool lowmem = false) {
   int kind = 0;
   validate(n, d, kspec, cfg, kind);
+  if (lowmem && round_up(d, 16) > 128)
+    raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: this build supports d <= 128");
   if (layout != RPC_COL_MAJOR && layout != RPC_ROW_MAJOR) raise(RPC_EINVAL, "unknown layout");
   const bool replay = (cfg.flags & RPC_FLAG_REPLAY_SCAN) != 0;
   if (replay && ctx->nshards() != 1)
@@ -323,6 +331,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   res->d = d;
   res->ldf = ldf;
   res->b = b;
+  res->lowmem = lowmem;
   rpc_timing& tm = res->timing;
   int64_t launches = 0;
 
@@ -343,7 +352,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     const int64_t nl = std::max<int64_t>(s.n_loc, 1);
     s.X = DBuf(ctx, sizeof(double) * nl * dpad);
     s.sqn = DBuf(ctx, sizeof(double) * nl);
-    s.F = DBuf(ctx, sizeof(double) * nl * ldf);
+    if (!lowmem) s.F = DBuf(ctx, sizeof(double) * nl * ldf);
     s.u = DBuf(ctx, sizeof(double) * nl);
     s.tile_g2 = DBuf(ctx, sizeof(double) * (nl / 64 + 2));
     max_tiles = std::max<int64_t>(max_tiles, nl / 64 + 2);
@@ -407,6 +416,20 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   DBuf shard_c0(ctx, sizeof(int) * (P + 1));
   DBuf cumsum;
   if (replay) cumsum = DBuf(ctx, sizeof(double) * n);
+  // low-memory state (replicated): pivot records, L and L^{-1} row-major [cap][ldf],
+  // per-round scratch K(S', S), F_S and F_S L^{-1}
+  const int64_t prec = 2 + dpad;
+  DBuf piv, Lrm, Linv, Kp, fsl, T1;
+  if (lowmem) {
+    piv = DBuf(ctx, sizeof(double) * cap * prec);
+    Lrm = DBuf(ctx, sizeof(double) * cap * ldf);
+    Linv = DBuf(ctx, sizeof(double) * cap * ldf);
+    Kp = DBuf(ctx, sizeof(double) * b * ldf);
+    fsl = DBuf(ctx, sizeof(double) * b * ldf);
+    T1 = DBuf(ctx, sizeof(double) * b * ldf);
+    CK(cudaMemsetAsync(Lrm.p, 0, Lrm.bytes, st));
+    CK(cudaMemsetAsync(Linv.p, 0, Linv.bytes, st));
+  }
   {
     std::vector<int> c0(P + 1);
     for (int s = 0; s <= P; ++s) c0[s] = s * L.cpr;
@@ -466,11 +489,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.u = s.u.as<double>();
       sp.X = s.X.as<double>();
       sp.sqn = s.sqn.as<double>();
-      sp.F = s.F.as<double>();
+      sp.F = lowmem ? nullptr : s.F.as<double>();
       sp.n_loc = s.n_loc;
       sp.dpad = dpad;
       sp.ldf = ldf;
-      sp.kcur = (int)kcur;
+      sp.kcur = lowmem ? 0 : (int)kcur;  // lowmem: factor rows are formed after selection
       sp.row0 = s.row0;
       sp.chunk0 = s.chunk0;
       sp.n_chunks_local = s.nchunks;
@@ -493,9 +516,18 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       ++launches;
     }
     allgather(ctx, recv.as<double>(), (size_t)b * lay.rec);
-    const int64_t words = 2 + dpad + kcur;
+    const int64_t words = 2 + dpad + (lowmem ? 0 : kcur);
     launch_select(recv.as<double>(), (int64_t)b * lay.rec, owner.as<int>(), b, lay.rec, words,
                   prop.as<double>(), st);
+    if (lowmem && kcur > 0) {
+      // F(S', :) = A(S', S) L^{-T}  (= W_prop^T of rpcholesky.hpp:441-444)
+      launch_kprop(prop.as<double>(), lay, b, piv.as<double>(), prec, (int)kcur, (int)d, kind,
+                   kspec.sigma, Kp.as<double>(), ldf, st);
+      launch_gemm(b, (int)kcur, (int)kcur, 1.0, Kp.as<double>(), ldf, 0, Linv.as<double>(), ldf, 1,
+                  0.0, prop.as<double>() + lay.foff, lay.rec, st);
+      launches += 2;
+      dbg(st, "lowmem fprop");
+    }
     // -- K3: H block; K4: rejection sweep (replicated on every shard)
     launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
                   Hbuf.as<double>(), st);
@@ -508,14 +540,17 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // L^{-1} and the accepted-pivot operands only need the sweep's device-side outputs:
     // queue them before the status read so they run while the host waits.
     CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
-    launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, (int)(kcur & 1),
+    launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, lowmem ? 0 : (int)(kcur & 1),
                     linv.as<double>(), st);
-    launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, 0, (int)dpad,
-                           xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
-                           idS.as<double>(), st, &d_sweep->m);
-    launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), prop.as<double>(), lay, pos.as<int>(),
-                  &d_sweep->m, b, (int)kcur, fs.as<double>(), ldf, st);
-    launches += 3;
+    ++launches;
+    if (!lowmem) {
+      launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, 0, (int)dpad,
+                             xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
+                             idS.as<double>(), st, &d_sweep->m);
+      launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), prop.as<double>(), lay, pos.as<int>(),
+                    &d_sweep->m, b, (int)kcur, fs.as<double>(), ldf, st);
+      launches += 2;
+    }
     CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
                        cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),
@@ -540,8 +575,65 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       if (kcur + m > cap)
         raise(RPC_ENUMERIC, "accelerated_rpcholesky: factor capacity exceeded (duplicate pivot)");
       CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
+      if (lowmem) {
+        // L_new = [[L, 0], [F_S, L_sel]]; L_new^{-1} rows [kcur, kcur+m) =
+        // [-L_sel^{-1} (F_S L^{-1}) | L_sel^{-1}]   (rpcholesky.hpp:470-475)
+        launch_lowmem_append(prop.as<double>(), lay, pos.as<int>(), m, (int)kcur, prec,
+                             lacc.as<double>(), linv.as<double>(), ldl, piv.as<double>(),
+                             fsl.as<double>(), ldf, Lrm.as<double>(), Linv.as<double>(), ldf, st);
+        ++launches;
+        if (kcur > 0) {
+          launch_gemm(m, (int)kcur, (int)kcur, 1.0, fsl.as<double>(), ldf, 0, Linv.as<double>(),
+                      ldf, 0, 0.0, T1.as<double>(), ldf, st);
+          launch_gemm(m, (int)kcur, m, -1.0, Linv.as<double>() + kcur * ldf + kcur, ldf, 0,
+                      T1.as<double>(), ldf, 0, 0.0, Linv.as<double>() + kcur * ldf, ldf, st);
+          launches += 2;
+        }
+        dbg(st, "lowmem append");
+        for (Shard& s : res->shards) {
+          if (s.n_loc == 0) continue;
+          LowmemParams lp{};
+          lp.X = s.X.as<double>();
+          lp.dpad = dpad;
+          lp.dchunks = (int)(dpad / 16);
+          lp.d = (int)d;
+          lp.sqn = s.sqn.as<double>();
+          lp.u = s.u.as<double>();
+          lp.n_loc = s.n_loc;
+          lp.row0 = s.row0;
+          lp.piv = piv.as<double>();
+          lp.prec = prec;
+          lp.W = Linv.as<double>() + kcur * ldf;
+          lp.ldw = ldf;
+          lp.m = m;
+          lp.kold = (int)kcur;
+          lp.knew = (int)(kcur + m);
+          lp.kind = kind;
+          lp.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
+          lp.tile_g2 = s.tile_g2.as<double>();
+          upd_ev.emplace_back();
+          upd_ev.emplace_back();
+          CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
+          const int bm = launch_lowmem(lp, st);
+          CK(cudaEventRecord(upd_ev.back().e, st));
+          dbg(st, "lowmem update");
+          if (bm < 0)
+            raise(RPC_ECUDA, "low-memory update launch failed (code " + std::to_string(bm) + ")");
+          const int64_t ntiles = (s.n_loc + bm - 1) / bm;
+          launch_tile_to_chunk(s.tile_g2.as<double>(), (int)ntiles, kChunk / bm, s.nchunks,
+                               g2_all.as<double>() + s.chunk0, st);
+          launches += 2;
+          ++upd_launches;
+          const double N = (double)s.n_loc, kn = (double)(kcur + m);
+          const double fl = 2.0 * N * m * kn + (kind == kGaussGram ? 2.0 * N * kn * d : 0.0);
+          flops += fl;
+          upd_info.emplace_back(m, kcur);
+          upd_flops.push_back(fl);
+          bytes += 8.0 * (N * d + 2.0 * N);
+        }
+      }
       for (Shard& s : res->shards) {
-        if (s.n_loc == 0) continue;
+        if (s.n_loc == 0 || lowmem) continue;
         UpdateParams up{};
         up.X = s.X.as<double>();
         up.dpad = dpad;
@@ -635,7 +727,12 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   res->fro2 = captured_sq;
   // chol_factor = lower(F(pivots, :)) (rpcholesky.hpp:140-145): owners gather pivot rows
   // into a device-resident column-major k x k buffer; copied out on request.
-  if (kcur > 0) {
+  if (kcur > 0 && lowmem) {
+    res->chol_dev = DBuf(ctx, sizeof(double) * kcur * kcur);
+    launch_lowmem_chol(Lrm.as<double>(), ldf, (int)kcur, res->chol_dev.as<double>(), st);
+    ++launches;
+    CK(cudaStreamSynchronize(st));
+  } else if (kcur > 0) {
     DBuf piv(ctx, sizeof(int64_t) * kcur);
     res->chol_dev = DBuf(ctx, sizeof(double) * kcur * kcur);
     CK(cudaMemcpyAsync(piv.p, res->pivots.data(), sizeof(int64_t) * kcur, cudaMemcpyHostToDevice, st));
@@ -827,6 +924,51 @@ int rpc_accelerated_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t
   return RPC_OK;
 }
 
+int rpc_accelerated_rpcholesky_lowmem(rpc_ctx* ctx, const double* x, int64_t n, int64_t d,
+                                      int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                      rpc_run_config cfg, rpc_result** out) {
+  if (!ctx || !out) return fail(ctx, RPC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *out = nullptr;
+  rpc_result* r = new_result();
+  int rc = guarded(ctx, [&] {
+    if (!x && n > 0) raise(RPC_EINVAL, "null point matrix");
+    if (ldx < (layout == RPC_ROW_MAJOR ? d : n)) raise(RPC_EINVAL, "leading dimension too small");
+    if (cfg.block_size < 1)
+      raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: block size must be >= 1");
+    run_factorization(ctx, x, false, n, d, ldx, layout, kernel, cfg, r, true);
+  });
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return RPC_OK;
+}
+
+int rpc_accelerated_rpcholesky_lowmem_device(rpc_ctx* ctx, const double* x_dev, int64_t n,
+                                             int64_t d, int64_t ldx, int layout,
+                                             rpc_kernel_spec kernel, rpc_run_config cfg,
+                                             rpc_result** out) {
+  if (!ctx || !out) return fail(ctx, RPC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *out = nullptr;
+  rpc_result* r = new_result();
+  int rc = guarded(ctx, [&] {
+    if (cfg.block_size < 1)
+      raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: block size must be >= 1");
+    run_factorization(ctx, x_dev, true, n, d, ldx, layout, kernel, cfg, r, true);
+  });
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return RPC_OK;
+}
+
+int rpc_result_is_lowmem(const rpc_result* r) { return r ? (int)r->lowmem : 0; }
+
 int64_t rpc_result_n(const rpc_result* r) { return r ? r->n : 0; }
 int64_t rpc_result_rank(const rpc_result* r) { return r ? r->kcur : 0; }
 int64_t rpc_result_num_rounds(const rpc_result* r) { return r ? (int64_t)r->proposed.size() : 0; }
@@ -871,6 +1013,8 @@ int rpc_result_round(const rpc_result* r, int64_t round, int64_t* proposed, int6
 
 int rpc_result_factor_copy(const rpc_result* r, double* out, int64_t ld, int layout) {
   if (!r) return RPC_EINVAL;
+  if (r->lowmem)
+    return fail(r->ctx, RPC_EINVAL, "low-memory result: the factor is not stored (LowMemResult)");
   rpc_ctx* ctx = r->ctx;
   return guarded(ctx, [&] {
     std::lock_guard<std::mutex> lk(ctx->mu);
@@ -920,7 +1064,7 @@ int rpc_result_residual_diag_copy(const rpc_result* r, double* out) {
 
 const double* rpc_result_factor_device(const rpc_result* r, int64_t* ldf, int64_t* row0,
                                        int64_t* nrows) {
-  if (!r || r->shards.empty()) return nullptr;
+  if (!r || r->shards.empty() || r->lowmem) return nullptr;
   if (ldf) *ldf = r->ldf;
   if (row0) *row0 = r->shards[0].row0;
   if (nrows) *nrows = r->shards[0].n_loc;

@@ -126,6 +126,42 @@ void launch_fsq_chunks(const double* F, int64_t ldf, int64_t n_loc, int k, int n
 // F row-major [n_loc][ldf] columns [c0, c0+nc) -> out col-major [nc][ld_out]
 void launch_f_to_colmajor(const double* F, int64_t ldf, int64_t n_loc, int c0, int nc,
                           double* out, int64_t ld_out, cudaStream_t st);
+// ---- low-memory variant (accelerated_rpcholesky_lowmem, rpcholesky.hpp:408-485) ----
+// State: pivot records piv[k][prec] (id, ||x||^2, x), Linv = L^{-1} of the pivot block
+// ([cap][ldw] row-major, lower), L ([cap][ldw] row-major, lower), u.  No N x k factor.
+// Per round the diagonal update is  u -= rowsq(A(R, S_all) W^T),  W = rows
+// [kold, kold+m) of the new L^{-1}: the kernel block A(R, S_all) is regenerated tile
+// by tile in shared memory and never leaves the SM (lowmem.cu).
+struct LowmemParams {
+  const double* X; int64_t dpad; int dchunks; int d;  // X shard [n_loc][dpad]
+  const double* sqn;                                  // ||x||^2 [n_loc]
+  double* u;                                          // residual diagonal [n_loc]
+  int64_t n_loc; int64_t row0;
+  const double* piv; int64_t prec;                    // pivot records [knew][prec]
+  const double* W; int64_t ldw;                       // W = Linv + kold * ldw, [m][knew]
+  int m, kold, knew;
+  int kind; double escale;
+  double* tile_g2;                                    // [n_tiles] per-tile ||G||^2
+};
+// Returns the tile height (64), or < 0 on failure (-1 unsupported m/d, -2 attr, -3 map).
+int launch_lowmem(const LowmemParams& p, cudaStream_t st);
+// C[M x N] = alpha op(A) op(B) + beta C, row-major fp64 (op = transpose when t* != 0).
+void launch_gemm(int M, int N, int K, double alpha, const double* A, int64_t lda, int ta,
+                 const double* B, int64_t ldb, int tb, double beta, double* C, int64_t ldc,
+                 cudaStream_t st);
+// K[j][i] = A(prop_j, piv_i) for j < b, i < k (kentry.cuh).
+void launch_kprop(const double* prop, RecordLayout lay, int b, const double* piv, int64_t prec,
+                  int k, int d, int kind, double sigma, double* K, int64_t ldk, cudaStream_t st);
+// Appends the m accepted pivots: piv rows, F_S = prop F rows -> fs[m][ldk] and L rows
+// [kold+a] = (F_S[a], L_sel[a]), Linv rows [kold+a][kold..] = L_sel^{-1}[a] (from linv_rm,
+// rows perm_row(a), koff 0).
+void launch_lowmem_append(const double* prop, RecordLayout lay, const int* pos, int m, int kold,
+                          int64_t prec, const double* lacc_cm, const double* linv_rm, int64_t ldl,
+                          double* piv, double* fs, int64_t ldk, double* Lrm, double* Linv,
+                          int64_t ldw, cudaStream_t st);
+// chol (k x k column-major, lower) from the row-major L.
+void launch_lowmem_chol(const double* Lrm, int64_t ldw, int k, double* chol, cudaStream_t st);
+
 // X (host layout already on device as col-major or row-major) -> padded row-major + norms
 // *nonfinite is set to 1 if any input coordinate is NaN/Inf (DataMatrix, data_matrix.hpp:26-28)
 void launch_pack_points(const double* src, int64_t n_loc, int d, int64_t ld_src,
