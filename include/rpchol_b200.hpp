@@ -6,7 +6,8 @@
 //     rpchol::CholeskyResult res = rpchol::b200::accelerated_rpcholesky(oracle, cfg);
 // Same inputs (the reference's own KernelOracle / RunConfig types), same output type
 // (CholeskyResult with factor, pivots, chol_factor, PivotTrace, residual_diag), same
-// exception classes and messages.  The computation runs in librpchol_b200.so through the
+// exception classes and messages.  Likewise accelerated_rpcholesky_lowmem
+// (rpcholesky.hpp:408-485) -> rpchol::b200::accelerated_rpcholesky_lowmem (LowMemResult).  The computation runs in librpchol_b200.so through the
 // C-ABI of rpchol_gpu.h.  Only KernelOracle inputs are accepted: any other PsdOracle
 // throws std::invalid_argument (there is no CPU fallback).
 //
@@ -60,21 +61,24 @@ inline Device& default_device() {
   return dev;
 }
 
-/// accelerated_rpcholesky (rpcholesky.hpp:338-401) for kernel oracles, on B200.
-inline CholeskyResult accelerated_rpcholesky(const PsdOracle& oracle, const RunConfig& cfg,
-                                             Device& dev = default_device()) {
+namespace detail {
+
+using ResultPtr = std::unique_ptr<rpc_result, void (*)(rpc_result*)>;
+using Entry = int (*)(rpc_ctx*, const double*, int64_t, int64_t, int64_t, int, rpc_kernel_spec,
+                      rpc_run_config, rpc_result**);
+
+// Runs `entry` (standard or low-memory) on a KernelOracle; throws like the reference.
+inline ResultPtr run(const PsdOracle& oracle, const RunConfig& cfg, Device& dev, Entry entry,
+                     const char* who) {
   const auto* ko = dynamic_cast<const KernelOracle*>(&oracle);
-  if (!ko) {
-    throw std::invalid_argument(
-        "accelerated_rpcholesky (B200): only KernelOracle inputs are supported");
-  }
+  if (!ko) throw std::invalid_argument(std::string(who) + " (B200): only KernelOracle inputs are supported");
   const Eigen::MatrixXd& x = ko->data().points();  // N x d, column-major
   rpc_kernel_spec ks;
   switch (ko->kernel().kind) {
     case KernelKind::Gaussian: ks.kind = RPC_KERNEL_GAUSSIAN; break;
     case KernelKind::L1Laplace: ks.kind = RPC_KERNEL_L1LAPLACE; break;
     default:
-      throw std::invalid_argument("accelerated_rpcholesky (B200): unsupported kernel kind " +
+      throw std::invalid_argument(std::string(who) + " (B200): unsupported kernel kind " +
                                   kernel_kind_name(ko->kernel().kind));
   }
   ks.sigma = ko->kernel().bandwidth;
@@ -89,10 +93,54 @@ inline CholeskyResult accelerated_rpcholesky(const PsdOracle& oracle, const RunC
   rc.stop_tol = cfg.stop_tol;
   rc.flags = 0;
   rpc_result* raw = nullptr;
-  if (int st = rpc_accelerated_rpcholesky(dev.get(), x.data(), x.rows(), x.cols(), x.rows(),
-                                          RPC_COL_MAJOR, ks, rc, &raw))
+  if (int st = entry(dev.get(), x.data(), x.rows(), x.cols(), x.rows(), RPC_COL_MAJOR, ks, rc, &raw))
     throw_status(st, rpc_last_error(dev.get()));
-  std::unique_ptr<rpc_result, void (*)(rpc_result*)> r(raw, rpc_result_free);
+  return ResultPtr(raw, rpc_result_free);
+}
+
+inline IndexList pivots_of(rpc_result* r) {
+  const int64_t k = rpc_result_rank(r);
+  std::vector<int64_t> buf(static_cast<std::size_t>(k));
+  if (k > 0) rpc_result_pivots(r, buf.data());
+  return IndexList(buf.begin(), buf.end());
+}
+
+inline Eigen::MatrixXd chol_of(rpc_result* r) {
+  const Eigen::Index k = rpc_result_rank(r);
+  Eigen::MatrixXd c(k, k);
+  if (k > 0) rpc_result_chol_copy(r, c.data());
+  return c;
+}
+
+inline Eigen::VectorXd residual_of(rpc_result* r) {
+  Eigen::VectorXd u(rpc_result_n(r));
+  rpc_result_residual_diag_copy(r, u.data());
+  return u;
+}
+
+inline PivotTrace trace_of(rpc_result* r) {
+  PivotTrace t;
+  const int64_t b = rpc_result_block_size(r);
+  std::vector<int64_t> prop(static_cast<std::size_t>(b)), acc(static_cast<std::size_t>(b));
+  for (int64_t i = 0; i < rpc_result_num_rounds(r); ++i) {
+    int64_t na = 0;
+    rpc_result_round(r, i, prop.data(), acc.data(), &na);
+    RoundRecord rec;
+    rec.proposed.assign(prop.begin(), prop.end());
+    rec.accepted.assign(acc.begin(), acc.begin() + na);
+    t.rounds.push_back(std::move(rec));
+  }
+  t.rank_exhausted = rpc_result_rank_exhausted(r) != 0;
+  t.surplus = rpc_result_surplus(r);
+  return t;
+}
+
+}  // namespace detail
+
+/// accelerated_rpcholesky (rpcholesky.hpp:338-401) for kernel oracles, on B200.
+inline CholeskyResult accelerated_rpcholesky(const PsdOracle& oracle, const RunConfig& cfg,
+                                             Device& dev = default_device()) {
+  auto r = detail::run(oracle, cfg, dev, rpc_accelerated_rpcholesky, "accelerated_rpcholesky");
   const Eigen::Index n = rpc_result_n(r.get());
   const Eigen::Index k = rpc_result_rank(r.get());
   CholeskyResult res;
@@ -101,26 +149,24 @@ inline CholeskyResult accelerated_rpcholesky(const PsdOracle& oracle, const RunC
     if (int st = rpc_result_factor_copy(r.get(), res.approx.factor.data(), n, RPC_COL_MAJOR))
       throw_status(st, rpc_last_error(dev.get()));
   }
-  res.approx.pivots.resize(static_cast<std::size_t>(k));
-  std::vector<int64_t> buf(static_cast<std::size_t>(k));
-  rpc_result_pivots(r.get(), buf.data());
-  for (Eigen::Index i = 0; i < k; ++i) res.approx.pivots[i] = static_cast<Eigen::Index>(buf[i]);
-  res.approx.chol_factor.resize(k, k);
-  if (k > 0) rpc_result_chol_copy(r.get(), res.approx.chol_factor.data());
-  res.residual_diag.resize(n);
-  rpc_result_residual_diag_copy(r.get(), res.residual_diag.data());
-  const int64_t b = rpc_result_block_size(r.get());
-  std::vector<int64_t> prop(static_cast<std::size_t>(b)), acc(static_cast<std::size_t>(b));
-  for (int64_t t = 0; t < rpc_result_num_rounds(r.get()); ++t) {
-    int64_t na = 0;
-    rpc_result_round(r.get(), t, prop.data(), acc.data(), &na);
-    RoundRecord rec;
-    rec.proposed.assign(prop.begin(), prop.end());
-    rec.accepted.assign(acc.begin(), acc.begin() + na);
-    res.trace.rounds.push_back(std::move(rec));
-  }
-  res.trace.rank_exhausted = rpc_result_rank_exhausted(r.get()) != 0;
-  res.trace.surplus = rpc_result_surplus(r.get());
+  res.approx.pivots = detail::pivots_of(r.get());
+  res.approx.chol_factor = detail::chol_of(r.get());
+  res.residual_diag = detail::residual_of(r.get());
+  res.trace = detail::trace_of(r.get());
+  return res;
+}
+
+/// accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485) for kernel oracles, on B200:
+/// O(N + k^2) device state, the N x k factor is never formed.
+inline LowMemResult accelerated_rpcholesky_lowmem(const PsdOracle& oracle, const RunConfig& cfg,
+                                                  Device& dev = default_device()) {
+  auto r = detail::run(oracle, cfg, dev, rpc_accelerated_rpcholesky_lowmem,
+                       "accelerated_rpcholesky_lowmem");
+  LowMemResult res;
+  res.pivots = detail::pivots_of(r.get());
+  res.chol_factor = detail::chol_of(r.get());
+  res.residual_diag = detail::residual_of(r.get());
+  res.trace = detail::trace_of(r.get());
   return res;
 }
 

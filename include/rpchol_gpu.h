@@ -184,6 +184,35 @@ int rpc_rejection_sweep(rpc_ctx* ctx, const double* h, int64_t b, const int64_t*
                         uint64_t seed, uint64_t draw0, int64_t* accepted, int64_t* positions,
                         int64_t* m, double* chol);
 
+/* ---- kernel ridge regression (krr.hpp) ------------------------------------ */
+/* kernel_matvec (krr.hpp:143-162): out (n x nrhs, column-major) = A V for V (n x nrhs,
+ * column-major), A the kernel matrix of X, never formed.  nrhs in [1, 8]; d <= 128. */
+int rpc_kernel_matvec(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                      int layout, rpc_kernel_spec kernel, const double* v, int64_t nrhs,
+                      double* out);
+typedef struct rpc_krr rpc_krr;
+/* fit_krr (krr.hpp:177-224): centred targets, accelerated_rpcholesky preconditioner of
+ * rank min(precond_rank, n) (0 = plain CG; cfg supplies block size and seed; the kernel
+ * uses default_distance_mode, oracle.hpp:39-42), Woodbury preconditioner (krr.hpp:30-70),
+ * PCG on (A + mu I) beta = y to relative residual tol (krr.hpp:87-123).  Errors:
+ * RPC_EINVAL for mu <= 0, tol <= 0, bad shapes; RPC_ENUMERIC if the core factorization
+ * fails.  Single-shard contexts. */
+int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int layout,
+                rpc_kernel_spec kernel, const double* targets, double mu, int64_t precond_rank,
+                rpc_run_config cfg, double tol, int64_t max_iters, rpc_krr** out);
+int64_t rpc_krr_iterations(const rpc_krr* m);  /* PcgReport::iterations */
+int rpc_krr_converged(const rpc_krr* m);       /* PcgReport::converged */
+/* PcgReport::relative_residuals / relative_residuals_unreg (iterations entries each) */
+int rpc_krr_residuals(const rpc_krr* m, double* reg, double* unreg);
+int rpc_krr_coefficients(const rpc_krr* m, double* out); /* KrrModel::coefficients (n) */
+double rpc_krr_target_mean(const rpc_krr* m);            /* KrrModel::target_mean */
+int64_t rpc_krr_precond_rank(const rpc_krr* m);          /* KrrFitResult::preconditioner rank */
+int rpc_krr_precond_pivots(const rpc_krr* m, int64_t* out);
+/* predict (krr.hpp:227-250): out[nq] = sum_i beta_i kappa(x_i, q) + target mean */
+int rpc_krr_predict(const rpc_krr* m, const double* q, int64_t nq, int64_t d, int64_t ldq,
+                    int layout, double* out);
+void rpc_krr_free(rpc_krr* m);
+
 #ifdef __cplusplus
 }
 #endif

@@ -42,6 +42,10 @@ def lib():
         L.ref_rejection_sweep.argtypes = [vp, i64, vp, C.c_uint64, C.c_uint64, vp, vp,
                                           C.POINTER(i64), vp]
         L.ref_result_free.argtypes = [C.POINTER(po._Res)]
+        L.ref_kernel_matvec.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, vp, i64, vp]
+        L.ref_fit_krr.argtypes = [vp, i64, i64, C.c_int, d, vp, d, i64, i64, C.c_uint64, d, i64,
+                                  i64, vp, C.POINTER(d), C.POINTER(i64), C.POINTER(C.c_int), vp,
+                                  vp, vp, C.POINTER(i64), vp, i64, vp]
         _L = L
     return _L
 
@@ -144,3 +148,41 @@ def rejection_sweep(h, proposals, seed, draw0):
                                      acc.ctypes.data, pos.ctypes.data, C.byref(m), chol.ctypes.data))
     k = m.value
     return acc[:k].copy(), pos[:k].copy(), chol[: k * k].reshape(k, k, order="F").copy()
+
+
+def kernel_matvec(x, kernel, sigma, v, dist=None, row_block=1024):
+    """kernel_matvec (krr.hpp:143-162)."""
+    xf = np.asfortranarray(x, dtype=np.float64)
+    kind = po.KERNELS[kernel]
+    dm = po.DIST[dist or ("direct" if kind == 1 else "gram")]
+    vv = np.ascontiguousarray(v, np.float64)
+    out = np.zeros(xf.shape[0])
+    _check(lib().ref_kernel_matvec(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm,
+                                   vv.ctypes.data, row_block, out.ctypes.data))
+    return out
+
+
+def fit_krr(x, targets, kernel, sigma, mu, precond_rank, block_size, seed, tol, max_iters=500,
+            materialize_threshold=8192, query=None):
+    """fit_krr (krr.hpp:177-224) with RunConfig::until_rank(rank, b, seed), then predict on
+    `query` when given.  Returns a dict of the KrrFitResult fields."""
+    xf = np.asfortranarray(x, dtype=np.float64)
+    n, d = xf.shape
+    kind = po.KERNELS[kernel]
+    t = np.ascontiguousarray(targets, np.float64)
+    coef = np.zeros(n)
+    rel, unreg = np.zeros(max(max_iters, 1)), np.zeros(max(max_iters, 1))
+    piv = np.zeros(max(precond_rank, 1) + block_size, np.int64)
+    mean, iters, conv, k = C.c_double(), C.c_int64(), C.c_int(), C.c_int64()
+    qf = np.asfortranarray(query, np.float64) if query is not None else None
+    pred = np.zeros(qf.shape[0]) if qf is not None else np.zeros(1)
+    _check(lib().ref_fit_krr(xf.ctypes.data, n, d, kind, sigma, t.ctypes.data, mu, precond_rank,
+                             block_size, seed, tol, max_iters, materialize_threshold,
+                             coef.ctypes.data, C.byref(mean), C.byref(iters), C.byref(conv),
+                             rel.ctypes.data, unreg.ctypes.data, piv.ctypes.data, C.byref(k),
+                             qf.ctypes.data if qf is not None else None,
+                             qf.shape[0] if qf is not None else 0, pred.ctypes.data))
+    it = iters.value
+    return dict(coefficients=coef, target_mean=mean.value, iterations=it, converged=bool(conv.value),
+                relative_residuals=rel[:it].copy(), relative_residuals_unreg=unreg[:it].copy(),
+                pivots=piv[:k.value].copy(), predictions=pred if qf is not None else None)

@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "rpchol/krr.hpp"
 #include "rpchol/rpcholesky.hpp"
 
 namespace {
@@ -213,6 +214,72 @@ int ref_rejection_sweep(const double* h, int64_t b, const int64_t* proposals, ui
     }
     std::memcpy(chol, sel.chol_factor.data(), sizeof(double) * (size_t)(m * m));
     *m_out = m;
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// kernel_matvec (krr.hpp:143-162) with the oracle's DistanceMode.
+int ref_kernel_matvec(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                      const double* v, int64_t row_block, double* out) {
+  try {
+    Eigen::MatrixXd pts(n, d);
+    std::memcpy(pts.data(), x, sizeof(double) * (size_t)(n * d));
+    rpchol::DataMatrix data(std::move(pts));
+    rpchol::KernelSpec spec(kind == 0 ? rpchol::KernelKind::Gaussian : rpchol::KernelKind::L1Laplace,
+                            sigma);
+    Eigen::VectorXd vv(n);
+    std::memcpy(vv.data(), v, sizeof(double) * (size_t)n);
+    Eigen::VectorXd o = rpchol::kernel_matvec(
+        data, spec, dist == 1 ? rpchol::DistanceMode::GramTrick : rpchol::DistanceMode::Direct, vv,
+        row_block, 1);
+    std::memcpy(out, o.data(), sizeof(double) * (size_t)n);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// fit_krr (krr.hpp:177-224) + predict (227-250) on `query` (nq x d, col-major; may be null).
+// rel / unreg / pivots need max_iters / max_iters / precond_rank entries.
+int ref_fit_krr(const double* x, int64_t n, int64_t d, int kind, double sigma,
+                const double* targets, double mu, int64_t precond_rank, int64_t b, uint64_t seed,
+                double tol, int64_t max_iters, int64_t materialize_threshold, double* coef,
+                double* mean, int64_t* iters, int* converged, double* rel, double* unreg,
+                int64_t* pivots, int64_t* k_out, const double* query, int64_t nq, double* pred) {
+  try {
+    Eigen::MatrixXd pts(n, d);
+    std::memcpy(pts.data(), x, sizeof(double) * (size_t)(n * d));
+    rpchol::DataMatrix data(std::move(pts));
+    rpchol::KernelSpec spec(kind == 0 ? rpchol::KernelKind::Gaussian : rpchol::KernelKind::L1Laplace,
+                            sigma);
+    Eigen::VectorXd t(n);
+    std::memcpy(t.data(), targets, sizeof(double) * (size_t)n);
+    rpchol::KrrOptions opts;
+    opts.max_iters = max_iters;
+    opts.materialize_threshold = materialize_threshold;
+    auto fit = rpchol::fit_krr(data, t, spec, mu, precond_rank,
+                               rpchol::RunConfig::until_rank(std::max<int64_t>(precond_rank, 1), b, seed),
+                               tol, opts);
+    std::memcpy(coef, fit.model.coefficients.data(), sizeof(double) * (size_t)n);
+    *mean = fit.model.target_mean;
+    *iters = fit.report.iterations;
+    *converged = fit.report.converged ? 1 : 0;
+    for (size_t i = 0; i < fit.report.relative_residuals.size(); ++i) {
+      rel[i] = fit.report.relative_residuals[i];
+      unreg[i] = fit.report.relative_residuals_unreg[i];
+    }
+    *k_out = (int64_t)fit.preconditioner.pivots.size();
+    for (size_t i = 0; i < fit.preconditioner.pivots.size(); ++i) pivots[i] = fit.preconditioner.pivots[i];
+    if (query && nq > 0) {
+      Eigen::MatrixXd q(nq, d);
+      std::memcpy(q.data(), query, sizeof(double) * (size_t)(nq * d));
+      Eigen::VectorXd p = rpchol::predict(fit.model, rpchol::DataMatrix(std::move(q)));
+      std::memcpy(pred, p.data(), sizeof(double) * (size_t)nq);
+    }
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

@@ -30,7 +30,9 @@ EXPORTS = [
     "rpc_result_relative_trace_error", "rpc_result_factor_device", "rpc_result_timing",
     "rpc_result_free", "rpc_kernel_columns", "rpc_sample_discrete", "rpc_rejection_sweep",
     "rpc_accelerated_rpcholesky_lowmem", "rpc_accelerated_rpcholesky_lowmem_device",
-    "rpc_result_is_lowmem",
+    "rpc_result_is_lowmem", "rpc_kernel_matvec", "rpc_krr_fit", "rpc_krr_iterations",
+    "rpc_krr_converged", "rpc_krr_residuals", "rpc_krr_coefficients", "rpc_krr_target_mean",
+    "rpc_krr_precond_rank", "rpc_krr_precond_pivots", "rpc_krr_predict", "rpc_krr_free",
 ]
 
 
@@ -98,6 +100,18 @@ def load() -> C.CDLL:
                                                                KernelSpecC, RunConfigC,
                                                                C.POINTER(vp)]),
         "rpc_result_is_lowmem": (C.c_int, [vp]),
+        "rpc_kernel_matvec": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, vp, i64, vp]),
+        "rpc_krr_fit": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, vp, C.c_double, i64,
+                                  RunConfigC, C.c_double, i64, C.POINTER(vp)]),
+        "rpc_krr_iterations": (i64, [vp]),
+        "rpc_krr_converged": (C.c_int, [vp]),
+        "rpc_krr_residuals": (C.c_int, [vp, vp, vp]),
+        "rpc_krr_coefficients": (C.c_int, [vp, vp]),
+        "rpc_krr_target_mean": (C.c_double, [vp]),
+        "rpc_krr_precond_rank": (i64, [vp]),
+        "rpc_krr_precond_pivots": (C.c_int, [vp, vp]),
+        "rpc_krr_predict": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, vp]),
+        "rpc_krr_free": (None, [vp]),
         "rpc_result_n": (i64, [vp]),
         "rpc_result_rank": (i64, [vp]),
         "rpc_result_pivots": (C.c_int, [vp, vp]),

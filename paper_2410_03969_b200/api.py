@@ -13,6 +13,7 @@ there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import weakref
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -75,9 +76,16 @@ class Context:
             L.check(lib.rpc_create(device, C.byref(h)))
         self.handle = h
         self.virtual_shards = virtual_shards
+        self._children = weakref.WeakSet()  # results / models that hold device memory
+
+    def _adopt(self, child):
+        self._children.add(child)
+        return child
 
     def close(self):
         if self.handle:
+            for c in list(self._children):  # release children before the context goes
+                c.free()
             L.load().rpc_destroy(self.handle)
             self.handle = None
 
@@ -160,7 +168,7 @@ class KernelOracle:
         return (out, ms.value) if return_ms else out
 
 
-@dataclass
+@dataclass(eq=False)
 class CholeskyResult:
     """CholeskyResult (rpcholesky.hpp:106-110) with the factor kept on the device
     until `factor` is first read."""
@@ -242,10 +250,11 @@ def _wrap_result(h: C.c_void_p, ctx: Context) -> CholeskyResult:
     t = L.TimingC()
     lib.rpc_result_timing(h, C.byref(t))
     timing = {f: getattr(t, f) for f, _ in L.TimingC._fields_}
-    return CholeskyResult(h, ctx, n, piv, proposed, accepted,
-                          bool(lib.rpc_result_rank_exhausted(h)), int(lib.rpc_result_surplus(h)),
-                          float(lib.rpc_result_captured_sq(h)),
-                          float(lib.rpc_result_relative_trace_error(h)), timing)
+    return ctx._adopt(CholeskyResult(h, ctx, n, piv, proposed, accepted,
+                                     bool(lib.rpc_result_rank_exhausted(h)),
+                                     int(lib.rpc_result_surplus(h)),
+                                     float(lib.rpc_result_captured_sq(h)),
+                                     float(lib.rpc_result_relative_trace_error(h)), timing))
 
 
 def accelerated_rpcholesky(oracle: KernelOracle, cfg: RunConfig,
@@ -336,3 +345,107 @@ def rejection_sample_submatrix(h: np.ndarray, proposals, seed: int, draw0: int,
                                          chol.ctypes.data), ctx.handle)
     k = m.value
     return acc[:k].copy(), pos[:k].copy(), chol[: k * k].reshape(k, k, order="F").copy()
+
+
+# ---------------------------------------------------------------------------
+# Kernel ridge regression (krr.hpp) on the device
+# ---------------------------------------------------------------------------
+def kernel_matvec(oracle: KernelOracle, v: np.ndarray, ctx: Context | None = None) -> np.ndarray:
+    """kernel_matvec (krr.hpp:143-162): A v (or A V for up to 8 columns), A never formed."""
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    v = np.asarray(v, dtype=np.float64)
+    vv = np.asfortranarray(v.reshape(v.shape[0], -1))
+    out = np.zeros(vv.shape, order="F")
+    L.check(L.load().rpc_kernel_matvec(ctx.handle, x.ctypes.data, x.shape[0], x.shape[1], ld, lay,
+                                       oracle._c_spec(), vv.ctypes.data, vv.shape[1],
+                                       out.ctypes.data), ctx.handle)
+    return out.reshape(v.shape)
+
+
+@dataclass
+class PcgReport:
+    """PcgReport (krr.hpp:80-85)."""
+    iterations: int
+    relative_residuals: np.ndarray
+    relative_residuals_unreg: np.ndarray
+    converged: bool
+
+
+class KrrModel:
+    """KrrModel (krr.hpp:125-131): coefficients and training points stay on the device."""
+
+    def __init__(self, handle: C.c_void_p, ctx: Context, n: int, d: int):
+        self._h, self._ctx, self.n, self.d = handle, ctx, n, d
+
+    @property
+    def coefficients(self) -> np.ndarray:
+        out = np.zeros(self.n)
+        L.check(L.load().rpc_krr_coefficients(self._h, out.ctypes.data), self._ctx.handle)
+        return out
+
+    @property
+    def target_mean(self) -> float:
+        return float(L.load().rpc_krr_target_mean(self._h))
+
+    def free(self):
+        if self._h:
+            L.load().rpc_krr_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+@dataclass
+class KrrFitResult:
+    """KrrFitResult (krr.hpp:164-168); `preconditioner_pivots` are the pivots of the
+    accelerated-RPCholesky factor behind the Woodbury preconditioner."""
+    model: KrrModel
+    report: PcgReport
+    preconditioner_pivots: np.ndarray
+
+
+def fit_krr(points: np.ndarray, targets: np.ndarray, spec: KernelSpec, mu: float,
+            precond_rank: int, config: RunConfig, tol: float, max_iters: int = 500,
+            ctx: Context | None = None) -> KrrFitResult:
+    """fit_krr (krr.hpp:177-224) on the GPU: RPCholesky preconditioner + PCG with fused
+    kernel matvecs."""
+    ctx = ctx or default_context()
+    ko = KernelOracle(points, spec)
+    x, lay, ld = ko._host_layout()
+    t = np.ascontiguousarray(targets, dtype=np.float64)
+    if t.shape[0] != x.shape[0]:
+        raise ValueError("fit_krr: targets size mismatch")
+    h = C.c_void_p()
+    lib = L.load()
+    L.check(lib.rpc_krr_fit(ctx.handle, x.ctypes.data, x.shape[0], x.shape[1], ld, lay,
+                            ko._c_spec(), t.ctypes.data, mu, precond_rank, config.to_c(), tol,
+                            max_iters, C.byref(h)), ctx.handle)
+    it = lib.rpc_krr_iterations(h)
+    reg, unreg = np.zeros(max(it, 1)), np.zeros(max(it, 1))
+    lib.rpc_krr_residuals(h, reg.ctypes.data, unreg.ctypes.data)
+    k = lib.rpc_krr_precond_rank(h)
+    piv = np.zeros(max(k, 1), np.int64)
+    lib.rpc_krr_precond_pivots(h, piv.ctypes.data)
+    report = PcgReport(int(it), reg[:it].copy(), unreg[:it].copy(), bool(lib.rpc_krr_converged(h)))
+    return KrrFitResult(ctx._adopt(KrrModel(h, ctx, x.shape[0], x.shape[1])), report, piv[:k].copy())
+
+
+def predict(model: KrrModel, query: np.ndarray) -> np.ndarray:
+    """predict (krr.hpp:227-250): sum_i beta_i kappa(x_i, q) + target mean."""
+    q = np.asarray(query, dtype=np.float64)
+    if q.ndim != 2 or q.shape[1] != model.d:
+        raise ValueError("predict: query dimension mismatch")
+    if q.flags.f_contiguous and not q.flags.c_contiguous:
+        lay, ld = L.RPC_COL_MAJOR, q.shape[0]
+    else:
+        q = np.ascontiguousarray(q)
+        lay, ld = L.RPC_ROW_MAJOR, q.shape[1]
+    out = np.zeros(q.shape[0])
+    L.check(L.load().rpc_krr_predict(model._h, q.ctypes.data, q.shape[0], q.shape[1], ld, lay,
+                                     out.ctypes.data), model._ctx.handle)
+    return out

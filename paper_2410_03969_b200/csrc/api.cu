@@ -13,272 +13,9 @@
 // the shards exchange only: chunk totals (+ previous round ||G||^2 partials),
 // and the b proposal records (id, ||x||^2, x, F row).  The sweep and L^{-1}
 // are computed redundantly and bit-identically on every shard.
-#include <nccl.h>
+#include "runtime.h"
 
-#include <algorithm>
-#include <chrono>
-#include <cmath>
-#include <cstdio>
-#include <cstdlib>
-#include <cstring>
-#include <map>
-#include <mutex>
-#include <stdexcept>
-#include <string>
-#include <vector>
-
-#include "../../include/rpchol_gpu.h"
-#include "common.cuh"
-#include "kernels.h"
-
-using namespace rpcb;
-
-namespace {
-
-struct RpcError {
-  int code;
-  std::string msg;
-};
-
-[[noreturn]] void raise(int code, const std::string& msg) { throw RpcError{code, msg}; }
-
-void cuda_check(cudaError_t e, const char* what) {
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    raise(e == cudaErrorMemoryAllocation ? RPC_ENOMEM : RPC_ECUDA,
-          std::string(what) + ": " + cudaGetErrorString(e));
-  }
-}
-#define CK(x) cuda_check((x), #x)
-
-void nccl_check(ncclResult_t r, const char* what) {
-  if (r != ncclSuccess) raise(RPC_ENCCL, std::string(what) + ": " + ncclGetErrorString(r));
-}
-#define NK(x) nccl_check((x), #x)
-
-thread_local std::string g_last_error;
-
-// RPC_DEBUG_SYNC=1: synchronise and check after every launch (localises faults).
-bool debug_sync() {
-  static const bool on = [] {
-    const char* e = std::getenv("RPC_DEBUG_SYNC");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-void dbg(cudaStream_t st, const char* what) {
-  if (!debug_sync()) return;
-  cudaError_t e = cudaStreamSynchronize(st);
-  if (e == cudaSuccess) e = cudaGetLastError();
-  if (e != cudaSuccess) {
-    cudaGetLastError();
-    throw RpcError{RPC_ECUDA, std::string("after ") + what + ": " + cudaGetErrorString(e)};
-  }
-}
-
-int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
-
-}  // namespace
-
-struct rpc_ctx {
-  int device = 0;
-  cudaStream_t stream = nullptr;
-  int world = 1, rank = 0;
-  ncclComm_t comm = nullptr;
-  int nvirt = 1;
-  std::mutex mu;
-  std::string err;
-  std::multimap<size_t, void*> pool;  // cached device blocks (size -> ptr)
-  void* host_pinned = nullptr;
-  size_t host_pinned_bytes = 0;
-
-  int nshards() const { return world * nvirt; }
-  int first_shard() const { return rank * nvirt; }
-
-  void* dalloc(size_t bytes) {
-    bytes = std::max<size_t>(256, round_up((int64_t)bytes, 256));
-    auto it = pool.lower_bound(bytes);
-    if (it != pool.end() && it->first <= bytes * 2) {
-      void* p = it->second;
-      pool.erase(it);
-      return p;
-    }
-    void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
-    if (e != cudaSuccess) {  // release the cache and retry once
-      cudaGetLastError();
-      trim();
-      CK(cudaMalloc(&p, bytes));
-    }
-    return p;
-  }
-  void dfree(void* p, size_t bytes) {
-    if (!p) return;
-    bytes = std::max<size_t>(256, round_up((int64_t)bytes, 256));
-    pool.emplace(bytes, p);
-  }
-  void trim() {
-    cudaStreamSynchronize(stream);
-    for (auto& kv : pool) cudaFree(kv.second);
-    pool.clear();
-  }
-  void* pinned(size_t bytes) {
-    if (bytes > host_pinned_bytes) {
-      if (host_pinned) cudaFreeHost(host_pinned);
-      host_pinned = nullptr;
-      CK(cudaMallocHost(&host_pinned, bytes));
-      host_pinned_bytes = bytes;
-    }
-    return host_pinned;
-  }
-};
-
-namespace {
-
-// Device buffer owned through the ctx pool.
-struct DBuf {
-  rpc_ctx* ctx = nullptr;
-  void* p = nullptr;
-  size_t bytes = 0;
-  DBuf() = default;
-  DBuf(rpc_ctx* c, size_t b) : ctx(c), bytes(b) { p = b ? c->dalloc(b) : nullptr; }
-  DBuf(const DBuf&) = delete;
-  DBuf& operator=(const DBuf&) = delete;
-  DBuf(DBuf&& o) noexcept { *this = std::move(o); }
-  DBuf& operator=(DBuf&& o) noexcept {
-    release();
-    ctx = o.ctx;
-    p = o.p;
-    bytes = o.bytes;
-    o.p = nullptr;
-    return *this;
-  }
-  ~DBuf() { release(); }
-  void release() {
-    if (p && ctx) ctx->dfree(p, bytes);
-    p = nullptr;
-  }
-  template <class T>
-  T* as() const {
-    return static_cast<T*>(p);
-  }
-};
-
-struct Layout {
-  int64_t n = 0;
-  int P = 1;
-  int nc = 0;    // real chunks
-  int cpr = 0;   // chunks per shard
-  int ncg = 0;   // P * cpr
-  int64_t row0(int s) const { return std::min<int64_t>(n, (int64_t)s * cpr * kChunk); }
-  int64_t rows(int s) const {
-    return std::min<int64_t>(n, (int64_t)(s + 1) * cpr * kChunk) - row0(s);
-  }
-  int chunks(int s) const { return (int)((rows(s) + kChunk - 1) / kChunk); }
-};
-
-Layout make_layout(int64_t n, int P) {
-  Layout L;
-  L.n = n;
-  L.P = P;
-  L.nc = (int)((n + kChunk - 1) / kChunk);
-  L.cpr = (L.nc + P - 1) / P;
-  L.ncg = L.cpr * P;
-  return L;
-}
-
-struct Shard {
-  int gidx = 0;  // global shard index
-  int64_t row0 = 0, n_loc = 0;
-  int chunk0 = 0, nchunks = 0;
-  DBuf X, sqn, F, u, tile_g2;
-};
-
-}  // namespace
-
-struct rpc_result {
-  rpc_ctx* ctx = nullptr;
-  int64_t n = 0, d = 0, kcur = 0, ldf = 0, b = 0;
-  std::vector<Shard> shards;
-  std::vector<int64_t> pivots;
-  std::vector<std::vector<int64_t>> proposed, accepted;
-  bool exhausted = false;
-  bool lowmem = false;       // accelerated_rpcholesky_lowmem: no factor is kept
-  int64_t surplus = 0;
-  double captured_sq = 0.0;
-  double fro2 = 0.0;
-  DBuf chol_dev;             // kcur x kcur column-major lower triangle (device)
-  rpc_timing timing{};
-};
-
-namespace {
-
-int fail(rpc_ctx* ctx, int code, const std::string& msg) {
-  g_last_error = msg;
-  if (ctx) ctx->err = msg;
-  return code;
-}
-
-template <class F>
-int guarded(rpc_ctx* ctx, F&& f) {
-  try {
-    f();
-    return RPC_OK;
-  } catch (const RpcError& e) {
-    return fail(ctx, e.code, e.msg);
-  } catch (const std::bad_alloc&) {
-    return fail(ctx, RPC_ENOMEM, "out of host memory");
-  } catch (const std::exception& e) {
-    return fail(ctx, RPC_ENUMERIC, e.what());
-  }
-}
-
-// Allgather of `count` doubles per global shard, in place in buf[P][count].
-void allgather(rpc_ctx* ctx, double* buf, size_t count) {
-  if (ctx->world == 1) return;  // virtual shards already write into buf directly
-  NK(ncclAllGather(buf + (size_t)ctx->rank * ctx->nvirt * count, buf, count * ctx->nvirt,
-                   ncclDouble, ctx->comm, ctx->stream));
-}
-
-void validate(int64_t n, int64_t d, const rpc_kernel_spec& k, rpc_run_config& cfg, int& kind) {
-  if (n < 1 || d < 1) raise(RPC_EINVAL, "DataMatrix: need at least one point and one dimension");
-  if (!(k.sigma > 0.0) || !std::isfinite(k.sigma))
-    raise(RPC_EINVAL, "KernelSpec: bandwidth must be positive");
-  int mode = k.distance_mode;
-  if (k.kind == RPC_KERNEL_GAUSSIAN) {
-    if (mode == RPC_DIST_DEFAULT) mode = RPC_DIST_GRAM;
-    if (mode != RPC_DIST_GRAM && mode != RPC_DIST_DIRECT) raise(RPC_EINVAL, "unknown distance mode");
-    kind = mode == RPC_DIST_GRAM ? kGaussGram : kGaussDirect;
-  } else if (k.kind == RPC_KERNEL_L1LAPLACE) {
-    if (mode == RPC_DIST_DEFAULT) mode = RPC_DIST_DIRECT;
-    if (mode == RPC_DIST_GRAM)
-      raise(RPC_EINVAL, "KernelOracle: GramTrick requires an l2 translation-invariant kernel");
-    kind = kL1;
-  } else {
-    raise(RPC_EINVAL, "unknown kernel kind");
-  }
-  if (cfg.block_size < 1) raise(RPC_EINVAL, "accelerated_rpcholesky: block size must be >= 1");
-  if (cfg.block_size > 256)
-    raise(RPC_EINVAL, "accelerated_rpcholesky: this build supports block size <= 256");
-  if (cfg.mode == RPC_FIXED_ROUNDS) {
-    if (cfg.rounds < 1) raise(RPC_EINVAL, "RunConfig: t, b must be >= 1");
-  } else if (cfg.mode == RPC_UNTIL_RANK) {
-    if (cfg.target_rank < 1) raise(RPC_EINVAL, "RunConfig: k, b must be >= 1");
-  } else {
-    raise(RPC_EINVAL, "RunConfig: unknown mode");
-  }
-}
-
-struct Ev {
-  cudaEvent_t e = nullptr;
-  Ev() { CK(cudaEventCreate(&e)); }
-  Ev(const Ev&) = delete;
-  Ev& operator=(const Ev&) = delete;
-  Ev(Ev&& o) noexcept : e(o.e) { o.e = nullptr; }
-  ~Ev() {
-    if (e) cudaEventDestroy(e);
-  }
-};
+namespace rpcb_rt {
 
 __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, int64_t row0,
                                    int64_t n_loc, const int64_t* __restrict__ piv, int64_t k,
@@ -298,7 +35,7 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 // kernel (lowmem_impl.cuh).  State: X, u, pivot records, L and L^{-1} (k x k).
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
-                       rpc_run_config cfg, rpc_result* res, bool lowmem = false) {
+                       rpc_run_config cfg, rpc_result* res, bool lowmem) {
   int kind = 0;
   validate(n, d, kspec, cfg, kind);
   if (lowmem && round_up(d, 16) > 128)
@@ -611,6 +348,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           lp.kind = kind;
           lp.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
           lp.tile_g2 = s.tile_g2.as<double>();
+          lp.pin = 1;
           upd_ev.emplace_back();
           upd_ev.emplace_back();
           CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
@@ -782,7 +520,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
 
 rpc_result* new_result() { return new rpc_result(); }
 
-}  // namespace
+}  // namespace rpcb_rt
+
+using namespace rpcb_rt;
 
 // ============================================================================
 // C ABI
@@ -859,6 +599,7 @@ void rpc_destroy(rpc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  for (auto fn : ctx->on_destroy) fn(ctx);
   ctx->trim();
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
   if (ctx->comm) ncclCommDestroy(ctx->comm);

@@ -142,6 +142,13 @@ struct LowmemParams {
   int m, kold, knew;
   int kind; double escale;
   double* tile_g2;                                    // [n_tiles] per-tile ||G||^2
+  // product mode (kernel_matvec / predict, krr.hpp:143-162, 227-250): instead of the
+  // diagonal update, out[row * ld_out + j] = (A(R, S) W^T)[row][j] + add_coef * add_vec[row]
+  // + add_const for j < m.  pin = 0 disables the same-index distance pin (cross blocks
+  // between different point sets, oracle.hpp:149-166).
+  int out_mode; double* out; int64_t ld_out;
+  const double* add_vec; double add_coef; double add_const;
+  int pin;
 };
 // Returns the tile height (64), or < 0 on failure (-1 unsupported m/d, -2 attr, -3 map).
 int launch_lowmem(const LowmemParams& p, cudaStream_t st);

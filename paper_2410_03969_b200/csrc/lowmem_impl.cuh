@@ -141,7 +141,7 @@ __global__ void __launch_bounds__(256, 1)
     for (int fr = 0; fr < 2; ++fr) {
       const int64_t grow = tile_row0 + arow[fr];
       sqr[fr] = grow < p.n_loc ? p.sqn[grow] : 0.0;
-      gid[fr] = (double)(p.row0 + grow);
+      gid[fr] = p.pin ? (double)(p.row0 + grow) : -2.0;  // ids are >= 0, padding -1
     }
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr)
@@ -257,6 +257,24 @@ __global__ void __launch_bounds__(256, 1)
       if (warp == 0) pump(cons);
     }
 
+    if (p.out_mode) {  // product mode: out = A(R, S) W^T (+ add terms)
+#pragma unroll
+      for (int fr = 0; fr < 2; ++fr) {
+        const int64_t grow = tile_row0 + arow[fr];
+        if (grow >= p.n_loc) continue;
+        const double add = (p.add_vec ? p.add_coef * p.add_vec[grow] : 0.0) + p.add_const;
+#pragma unroll
+        for (int q = 0; q < NFW; ++q)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            // C column 2t+v of fragment q came from W row 8 (wc NFW + q) + perm8(2t+v)
+            const int col = 8 * (wc * NFW + q) + perm8(2 * t + v);
+            if (col < p.m) p.out[grow * p.ld_out + col] = acc[fr][q][v] + add;
+          }
+      }
+      gsync();  // the next tile's X load overwrites xt
+      continue;
+    }
     // ---- epilogue: u(R) = max(u - rowwise ||g||^2, 0); per-tile ||g||_F^2 ----------
     // (W rows >= m are zero-filled by TMA, so padded columns contribute exactly 0)
     double rs[2] = {0.0, 0.0};

@@ -3,7 +3,8 @@
 // Built by `make -C oracle dropin` (needs the reference headers, compiled against the
 // Eigen-API shim) into oracle/_ref/dropin_test; run on a B200 by tests/test_dropin.py.
 // A reference user swaps rpchol::accelerated_rpcholesky for
-// rpchol::b200::accelerated_rpcholesky with the same KernelOracle and RunConfig.
+// rpchol::b200::accelerated_rpcholesky with the same KernelOracle and RunConfig (and
+// accelerated_rpcholesky_lowmem for rpchol::b200::accelerated_rpcholesky_lowmem).
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -52,6 +53,25 @@ static void compare(const char* name, const PsdOracle& oracle, const RunConfig& 
               name, (long)gpu.approx.rank(), gpu.trace.rounds.size(), ef, ec, eu, tr);
 }
 
+static void compare_lowmem(const char* name, const PsdOracle& oracle, const RunConfig& cfg) {
+  const LowMemResult ref = rpchol::accelerated_rpcholesky_lowmem(oracle, cfg);
+  const LowMemResult gpu = rpchol::b200::accelerated_rpcholesky_lowmem(oracle, cfg);
+  EXPECT(ref.pivots == gpu.pivots);
+  EXPECT(ref.trace.rounds.size() == gpu.trace.rounds.size());
+  for (size_t r = 0; r < std::min(ref.trace.rounds.size(), gpu.trace.rounds.size()); ++r) {
+    EXPECT(ref.trace.rounds[r].proposed == gpu.trace.rounds[r].proposed);
+    EXPECT(ref.trace.rounds[r].accepted == gpu.trace.rounds[r].accepted);
+  }
+  EXPECT(ref.trace.rank_exhausted == gpu.trace.rank_exhausted);
+  EXPECT(ref.trace.surplus == gpu.trace.surplus);
+  const double ec = rel(gpu.chol_factor, ref.chol_factor);
+  const double eu = (gpu.residual_diag - ref.residual_diag).cwiseAbs().maxCoeff();
+  EXPECT(ec <= 1e-10);
+  EXPECT(eu <= 1e-8);
+  std::printf("%s (lowmem): rank %zu rounds %zu  |dL|/|L| %.2e  max|du| %.2e\n", name,
+              gpu.pivots.size(), gpu.trace.rounds.size(), ec, eu);
+}
+
 int main() {
   SplitMix64 rng(0);
   const Eigen::Index n = 6000, d = 10;
@@ -65,6 +85,8 @@ int main() {
   compare("l1 until_rank(150, 60)", l1, RunConfig::until_rank(150, 60, 1));
   KernelOracle direct(DataMatrix(x), KernelSpec(KernelKind::Gaussian, 2.0), DistanceMode::Direct);
   compare("gaussian-direct until_rank(100, 25)", direct, RunConfig::until_rank(100, 25, 2));
+  compare_lowmem("gaussian-gram until_rank(200, 40)", gauss, RunConfig::until_rank(200, 40, 0));
+  compare_lowmem("l1 fixed_rounds(4, 60)", l1, RunConfig::fixed_rounds(4, 60, 1));
 
   // error behaviour mirrors the reference
   try {

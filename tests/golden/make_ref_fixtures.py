@@ -8,7 +8,9 @@ relative_trace_error, for BASELINE config C1 (full size) and scaled-down
 C2/C3-shaped inputs.  `lowmem` fixtures (ref_lowmem_*.npz) carry the reference's
 accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485) answers: pivots, trace,
 chol_factor and residual diagonal.
-Run:  python tests/golden/make_ref_fixtures.py [standard|lowmem|all]
+`krr` fixtures (ref_krr_*.npz) carry fit_krr + predict (krr.hpp:177-250): coefficients,
+PCG report, preconditioner pivots and predictions on a held-out query set.
+Run:  python tests/golden/make_ref_fixtures.py [standard|lowmem|krr|all]
 """
 import math
 import os
@@ -52,6 +54,36 @@ def make_lowmem():
         print("lowmem", name, "rank", len(r.pivots), "rounds", len(r.proposed))
 
 
+# fit_krr (krr.hpp:177-224) + predict: (generator, n, d, kernel, sigma, mu, rank, b, seed, tol,
+# materialize_threshold).  "lazy" exercises the reference's on-the-fly matvec path (n > 0).
+KRR_CASES = {
+    "gauss": ("C1", 3000, 10, "gaussian", math.sqrt(10.0), 1e-3, 200, 40, 0, 1e-8, 8192),
+    "l1": ("C3", 2500, 8, "l1laplace", 2.0, 1e-2, 150, 30, 1, 1e-8, 8192),
+    "lazy": ("C2", 2000, 6, "gaussian", 1.5, 1e-2, 100, 25, 2, 1e-8, 0),
+}
+
+
+def krr_targets(x):
+    return np.sin(x[:, 0]) + 0.3 * x[:, 1] - 0.1 * x[:, -1] ** 2
+
+
+def make_krr():
+    for name, (gen, n, d, kern, sigma, mu, rank, b, seed, tol, thr) in KRR_CASES.items():
+        x = wl.GENERATORS[gen](n, d, 0)
+        q = wl.GENERATORS[gen](257, d, 9)
+        r = pyref.fit_krr(x, krr_targets(x), kern, sigma, mu, rank, b, seed, tol, 500, thr, query=q)
+        np.savez_compressed(
+            os.path.join(HERE, f"ref_krr_{name}.npz"),
+            config=np.array([gen, str(n), str(d), kern, repr(sigma), repr(mu), str(rank), str(b),
+                             str(seed), repr(tol), str(thr)]),
+            coefficients=r["coefficients"], target_mean=np.array(r["target_mean"]),
+            iterations=np.array(r["iterations"]), converged=np.array(r["converged"]),
+            relative_residuals=r["relative_residuals"],
+            relative_residuals_unreg=r["relative_residuals_unreg"], pivots=r["pivots"],
+            predictions=r["predictions"])
+        print("krr", name, "iters", r["iterations"], "converged", r["converged"])
+
+
 def make_standard():
     for name, (gen, n, d, kern, sigma, k, b, seed) in CASES.items():
         x = wl.GENERATORS[gen](n, d, 0)
@@ -76,3 +108,5 @@ if __name__ == "__main__":
         make_standard()
     if what in ("lowmem", "all"):
         make_lowmem()
+    if what in ("krr", "all"):
+        make_krr()
