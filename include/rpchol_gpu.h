@@ -125,6 +125,24 @@ int rpc_accelerated_rpcholesky_lowmem_device(rpc_ctx* ctx, const double* x_dev, 
                                              rpc_result** out);
 int rpc_result_is_lowmem(const rpc_result* r);
 
+/* ---- block and simple RPCholesky (the paper's baselines) ------------------ */
+/* block_rpcholesky (rpcholesky.hpp:268-333): per round b proposals (draws [b r, b r + b)),
+ * every distinct one kept (sorted), the kept block Cholesky-factored (one retry with a
+ * 64 eps tr(A)/N diagonal shift, then RPC_ENUMERIC) and eliminated.  Same result handle. */
+int rpc_block_rpcholesky(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                         int layout, rpc_kernel_spec kernel, rpc_run_config cfg, rpc_result** out);
+int rpc_block_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, int64_t d,
+                                int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                rpc_run_config cfg, rpc_result** out);
+/* simple_rpcholesky (rpcholesky.hpp:206-246): k sequential pivots, one draw each; a
+ * non-positive residual pivot sets rank_exhausted.  flags: RPC_FLAG_REPLAY_SCAN. */
+int rpc_simple_rpcholesky(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                          int layout, rpc_kernel_spec kernel, int64_t k, uint64_t seed,
+                          uint32_t flags, rpc_result** out);
+int rpc_simple_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, int64_t d,
+                                 int64_t ldx, int layout, rpc_kernel_spec kernel, int64_t k,
+                                 uint64_t seed, uint32_t flags, rpc_result** out);
+
 /* ---- result (CholeskyResult, rpcholesky.hpp:106-110) --------------------- */
 int64_t rpc_result_n(const rpc_result* r);
 int64_t rpc_result_rank(const rpc_result* r); /* factor columns = |pivots| */

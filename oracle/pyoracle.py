@@ -97,6 +97,9 @@ def lib() -> C.CDLL:
                                                          C.c_int64, C.POINTER(_Res)]
         L.rpo_accelerated_rpcholesky_lowmem.argtypes = [C.POINTER(_Oracle), C.POINTER(_Cfg),
                                                         C.POINTER(_Res)]
+        L.rpo_block_rpcholesky.argtypes = [C.POINTER(_Oracle), C.POINTER(_Cfg), C.POINTER(_Res)]
+        L.rpo_simple_rpcholesky.argtypes = [C.POINTER(_Oracle), C.c_int64, C.c_uint64,
+                                            C.POINTER(_Res)]
         L.rpo_result_free.argtypes = [C.POINTER(_Res)]
         L.rpo_relative_trace_error.restype = C.c_double
         L.rpo_relative_trace_error.argtypes = [C.POINTER(_Oracle), C.c_void_p, C.c_int64,
@@ -245,6 +248,23 @@ def accelerated_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "unti
     res = _Res()
     _check(lib().rpo_accelerated_rpcholesky_bounded(C.byref(oracle._o), C.byref(cfg),
                                                     max_rounds, C.byref(res)))
+    return _unpack(res)
+
+
+def block_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "until_rank",
+                     rounds: int = 0, target_rank: int = 0, seed: int = 0,
+                     stop_tol: float = 0.0) -> Result:
+    """rpcholesky.hpp:268-333; Result.accepted holds the kept (sorted, distinct) proposals."""
+    cfg = _Cfg(block_size, MODES[mode], rounds, target_rank, seed, stop_tol)
+    res = _Res()
+    _check(lib().rpo_block_rpcholesky(C.byref(oracle._o), C.byref(cfg), C.byref(res)))
+    return _unpack(res)
+
+
+def simple_rpcholesky(oracle: Oracle, k: int, seed: int) -> Result:
+    """rpcholesky.hpp:206-246."""
+    res = _Res()
+    _check(lib().rpo_simple_rpcholesky(C.byref(oracle._o), k, seed, C.byref(res)))
     return _unpack(res)
 
 

@@ -33,6 +33,9 @@ def lib():
         L.ref_accelerated_kernel.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, i64, C.c_int, i64,
                                              i64, C.c_uint64, d, C.POINTER(po._Res)]
         L.ref_lowmem_kernel.argtypes = L.ref_accelerated_kernel.argtypes
+        L.ref_block_kernel.argtypes = L.ref_accelerated_kernel.argtypes
+        L.ref_simple_kernel.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, i64, C.c_uint64,
+                                        C.POINTER(po._Res)]
         L.ref_accelerated_dense.argtypes = [vp, i64, i64, C.c_int, i64, i64, C.c_uint64, d,
                                             C.POINTER(po._Res)]
         L.ref_relative_trace_error_kernel.restype = d
@@ -98,6 +101,30 @@ def accelerated_rpcholesky_lowmem_kernel(x, kernel, sigma, *, block_size, mode="
     _check(lib().ref_lowmem_kernel(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm,
                                    block_size, po.MODES[mode], rounds, target_rank, seed,
                                    stop_tol, C.byref(res)))
+    return _unpack(res)
+
+
+def block_rpcholesky_kernel(x, kernel, sigma, *, block_size, mode="until_rank", rounds=0,
+                            target_rank=0, seed=0, stop_tol=0.0, dist=None) -> po.Result:
+    """block_rpcholesky (rpcholesky.hpp:268-333)."""
+    xf = np.asfortranarray(x, dtype=np.float64)
+    kind = po.KERNELS[kernel]
+    dm = po.DIST[dist or ("direct" if kind == 1 else "gram")]
+    res = po._Res()
+    _check(lib().ref_block_kernel(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm,
+                                  block_size, po.MODES[mode], rounds, target_rank, seed, stop_tol,
+                                  C.byref(res)))
+    return _unpack(res)
+
+
+def simple_rpcholesky_kernel(x, kernel, sigma, k, seed=0, dist=None) -> po.Result:
+    """simple_rpcholesky (rpcholesky.hpp:206-246)."""
+    xf = np.asfortranarray(x, dtype=np.float64)
+    kind = po.KERNELS[kernel]
+    dm = po.DIST[dist or ("direct" if kind == 1 else "gram")]
+    res = po._Res()
+    _check(lib().ref_simple_kernel(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm, k,
+                                   seed, C.byref(res)))
     return _unpack(res)
 
 

@@ -125,6 +125,35 @@ int ref_accelerated_dense(const double* a, int64_t n, int64_t b, int mode, int64
   }
 }
 
+// block_rpcholesky (rpcholesky.hpp:268-333)
+int ref_block_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                     int64_t b, int mode, int64_t rounds, int64_t k, uint64_t seed,
+                     double stop_tol, Res* out) {
+  try {
+    auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+    auto res = rpchol::block_rpcholesky(oracle, make_cfg(b, mode, rounds, k, seed, stop_tol));
+    fill(res, out, b);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// simple_rpcholesky (rpcholesky.hpp:206-246)
+int ref_simple_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                      int64_t k, uint64_t seed, Res* out) {
+  try {
+    auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+    auto res = rpchol::simple_rpcholesky(oracle, k, seed);
+    fill(res, out, 1);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
 // accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485): factor = NULL, rank = |pivots|.
 int ref_lowmem_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
                       int64_t b, int mode, int64_t rounds, int64_t k, uint64_t seed,

@@ -527,6 +527,225 @@ int rpo_accelerated_rpcholesky(const rpo_oracle* o, const rpo_run_config* cfg, r
   return rpo_accelerated_rpcholesky_bounded(o, cfg, -1, res);
 }
 
+/* ---- block_rpcholesky rpcholesky.hpp:268-333 / simple_rpcholesky 206-246 ---- */
+/* Cholesky of an m x m column-major block (the LLT the reference delegates to Eigen;
+ * restated as the left-looking dot-product form, which is what oracle/eigen_shim's LLT
+ * computes, so the restatement and the reference-through-shim agree bitwise).
+ * Returns 0 on success, -1 on a non-positive pivot. */
+static int llt_lower(const double* a, int64_t m, double* l) {
+  memset(l, 0, sizeof(double) * (size_t)(m * m));
+  for (int64_t j = 0; j < m; ++j) {
+    double s = a[j * m + j];
+    for (int64_t k = 0; k < j; ++k) s -= l[k * m + j] * l[k * m + j];
+    if (!(s > 0.0)) return -1;
+    const double dj = sqrt(s);
+    l[j * m + j] = dj;
+    for (int64_t i = j + 1; i < m; ++i) {
+      double t = a[j * m + i];
+      for (int64_t k = 0; k < j; ++k) t -= l[k * m + i] * l[k * m + j];
+      l[j * m + i] = t / dj;
+    }
+  }
+  return 0;
+}
+
+static int cmp_i64(const void* a, const void* b) {
+  const int64_t x = *(const int64_t*)a, y = *(const int64_t*)b;
+  return x < y ? -1 : x > y;
+}
+
+/* algo 1: block (cfg as given); algo 2: simple (cfg = UntilRank(k, 1, seed)). */
+static int rpo_block_or_simple(const rpo_oracle* o, const rpo_run_config* cfg, int algo,
+                               rpo_result* res) {
+  memset(res, 0, sizeof *res);
+  const int64_t n = o->n;
+  const int64_t b = cfg->block_size;
+  const int nt = o->n_threads;
+  const char* who = algo == 2 ? "simple_rpcholesky" : "block_rpcholesky";
+  if (algo == 2 && (cfg->target_rank < 1 || cfg->target_rank > n))
+    return fail(RPO_EINVAL, "simple_rpcholesky: need 1 <= k <= N");
+  if (b < 1) return fail(RPO_EINVAL, "%s: block size must be >= 1", who);
+  if (cfg->mode == RPO_MODE_FIXED_ROUNDS && cfg->rounds < 1)
+    return fail(RPO_EINVAL, "RunConfig: t, b must be >= 1");
+  if (cfg->mode == RPO_MODE_UNTIL_RANK && cfg->target_rank < 1)
+    return fail(RPO_EINVAL, "RunConfig: k, b must be >= 1");
+  double* dg = (double*)malloc(sizeof(double) * (size_t)n);
+  double* cumsum = (double*)malloc(sizeof(double) * (size_t)n);
+  if (!dg || !cumsum) {
+    free(dg);
+    free(cumsum);
+    return fail(RPO_ENOMEM, "out of memory");
+  }
+  diag_of(o, dg);
+  double trace_a = 0.0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (dg[i] < 0.0) dg[i] = 0.0;
+    trace_a += dg[i];
+  }
+  if (!(trace_a > 0.0)) {
+    free(dg);
+    free(cumsum);
+    return fail(RPO_EINVAL, "%s: trace must be > 0", who);
+  }
+  int64_t cap = algo == 2 ? cfg->target_rank
+                          : (cfg->mode == RPO_MODE_FIXED_ROUNDS ? cfg->rounds * b : cfg->target_rank + b);
+  if (cap > n) cap = n;
+  double* f = (double*)malloc(sizeof(double) * (size_t)n * (size_t)cap);
+  int64_t* pivots = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int64_t* proposed = (int64_t*)malloc(sizeof(int64_t) * (size_t)b);
+  int64_t* kept = (int64_t*)malloc(sizeof(int64_t) * (size_t)b);
+  double* fr = (double*)malloc(sizeof(double) * (size_t)(b * cap));
+  double* blk = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  double* lsel = (double*)malloc(sizeof(double) * (size_t)(b * b));
+  int64_t rounds_cap = 16;
+  int64_t* all_prop = (int64_t*)malloc(sizeof(int64_t) * (size_t)(rounds_cap * b));
+  int64_t* all_cnt = (int64_t*)malloc(sizeof(int64_t) * (size_t)rounds_cap);
+  int64_t* all_kept = (int64_t*)malloc(sizeof(int64_t) * (size_t)cap);
+  int rc = RPO_OK;
+  if (!f || !pivots || !proposed || !kept || !fr || !blk || !lsel || !all_prop || !all_cnt ||
+      !all_kept) {
+    rc = fail(RPO_ENOMEM, "out of memory");
+    goto done;
+  }
+  int64_t kcur = 0;
+  double captured_sq = 0.0;
+  uint64_t draw = 0;
+  int64_t round;
+  for (round = 0; !run_finished(cfg, round, kcur); ++round) {
+    double usum = 0.0;
+    for (int64_t i = 0; i < n; ++i) usum += dg[i];
+    if (!(usum > 0.0)) {
+      res->rank_exhausted = 1;
+      break;
+    }
+    if (algo == 1 && cfg->stop_tol > 0.0 && (trace_a - captured_sq) <= cfg->stop_tol * trace_a) break;
+    rpo_cumulative_sums(dg, n, cumsum);
+    for (int64_t j = 0; j < b; ++j) {
+      rc = rpo_sample_discrete(cumsum, n, rpo_u01(rpo_splitmix64_draw(cfg->seed, draw++)),
+                               &proposed[j]);
+      if (rc) goto done;
+    }
+    /* kept = unique_sorted(proposed) */
+    memcpy(kept, proposed, sizeof(int64_t) * (size_t)b);
+    qsort(kept, (size_t)b, sizeof(int64_t), cmp_i64);
+    int64_t m = 0;
+    for (int64_t j = 0; j < b; ++j)
+      if (j == 0 || kept[j] != kept[m - 1]) kept[m++] = kept[j];
+    if (kcur + m > cap) {
+      rc = fail(RPO_ENUMERIC, "%s: factor capacity exceeded", who);
+      goto done;
+    }
+    double* g = f + kcur * n;
+    oracle_columns(o, kept, m, g);
+    if (kcur > 0) {
+      for (int64_t k = 0; k < kcur; ++k)
+        for (int64_t i = 0; i < m; ++i) fr[k * m + i] = f[k * n + kept[i]];
+      residual_gemm(f, n, kcur, fr, m, g, nt);
+    }
+    if (algo == 2) {
+      /* simple: g / sqrt(g[s]); !(g[s] > 0) -> rank exhausted (229-236) */
+      const double gs = g[kept[0]];
+      if (!(gs > 0.0)) {
+        res->rank_exhausted = 1;
+        break;
+      }
+      const double root = sqrt(gs);
+      for (int64_t i = 0; i < n; ++i) g[i] = g[i] / root;
+    } else {
+      for (int64_t j = 0; j < m; ++j)
+        for (int64_t i = 0; i < m; ++i) blk[j * m + i] = g[j * n + kept[i]];
+      if (llt_lower(blk, m, lsel) != 0) {
+        const double shift = 64.0 * 2.220446049250313e-16 * trace_a / (double)n;
+        for (int64_t i = 0; i < m; ++i) blk[i * m + i] += shift;
+        if (llt_lower(blk, m, lsel) != 0) {
+          rc = fail(RPO_ENUMERIC, "block_rpcholesky: Cholesky failed after diagonal shift");
+          goto done;
+        }
+      }
+      right_solve_lt(lsel, m, g, n, nt);
+    }
+    for (int64_t i = 0; i < n; ++i) {
+      double s2 = 0.0;
+      for (int64_t j = 0; j < m; ++j) s2 += g[j * n + i] * g[j * n + i];
+      dg[i] -= s2;
+    }
+    for (int64_t i = 0; i < n; ++i)
+      if (dg[i] < 0.0) dg[i] = 0.0;
+    double gs2 = 0.0;
+    for (int64_t j = 0; j < m; ++j)
+      for (int64_t i = 0; i < n; ++i) gs2 += g[j * n + i] * g[j * n + i];
+    captured_sq += gs2;
+    for (int64_t j = 0; j < m; ++j) pivots[kcur + j] = kept[j];
+    kcur += m;
+    if (round >= rounds_cap) {
+      rounds_cap *= 2;
+      int64_t* np = (int64_t*)realloc(all_prop, sizeof(int64_t) * (size_t)(rounds_cap * b));
+      int64_t* nc = (int64_t*)realloc(all_cnt, sizeof(int64_t) * (size_t)rounds_cap);
+      if (!np || !nc) {
+        rc = fail(RPO_ENOMEM, "out of memory");
+        goto done;
+      }
+      all_prop = np;
+      all_cnt = nc;
+    }
+    memcpy(all_prop + round * b, proposed, sizeof(int64_t) * (size_t)b);
+    all_cnt[round] = m;
+  }
+  res->n = n;
+  res->rank = kcur;
+  res->block_size = b;
+  res->n_rounds = round;
+  res->factor = f;
+  f = NULL;
+  res->pivots = pivots;
+  pivots = NULL;
+  res->chol = (double*)calloc((size_t)(kcur * kcur > 0 ? kcur * kcur : 1), sizeof(double));
+  if (!res->chol) {
+    rc = fail(RPO_ENOMEM, "out of memory");
+    goto done;
+  }
+  for (int64_t j = 0; j < kcur; ++j)
+    for (int64_t i = j; i < kcur; ++i) res->chol[j * kcur + i] = res->factor[j * n + res->pivots[i]];
+  res->residual_diag = dg;
+  dg = NULL;
+  res->proposed = all_prop;
+  all_prop = NULL;
+  res->accepted_count = all_cnt;
+  all_cnt = NULL;
+  if (algo == 1 && cfg->mode == RPO_MODE_UNTIL_RANK && kcur > cfg->target_rank)
+    res->surplus = kcur - cfg->target_rank;
+  res->captured_sq = captured_sq;
+done:
+  free(dg);
+  free(cumsum);
+  free(f);
+  free(pivots);
+  free(proposed);
+  free(kept);
+  free(fr);
+  free(blk);
+  free(lsel);
+  free(all_prop);
+  free(all_cnt);
+  free(all_kept);
+  if (rc) rpo_result_free(res);
+  return rc;
+}
+
+int rpo_block_rpcholesky(const rpo_oracle* o, const rpo_run_config* cfg, rpo_result* res) {
+  return rpo_block_or_simple(o, cfg, 1, res);
+}
+
+int rpo_simple_rpcholesky(const rpo_oracle* o, int64_t k, uint64_t seed, rpo_result* res) {
+  rpo_run_config c;
+  memset(&c, 0, sizeof c);
+  c.block_size = 1;
+  c.mode = RPO_MODE_UNTIL_RANK;
+  c.target_rank = k;
+  c.seed = seed;
+  return rpo_block_or_simple(o, &c, 2, res);
+}
+
 /* ---- rpcholesky.hpp:408-485  accelerated_rpcholesky_lowmem ---------- */
 /* Forward substitution L y = w in place for nc columns (L: k x k column-major lower,
  * w: k x nc column-major with leading dimension ldw) — triangularView<Lower>::solveInPlace. */

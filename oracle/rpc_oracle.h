@@ -112,6 +112,10 @@ int rpo_accelerated_rpcholesky_bounded(const rpo_oracle* o, const rpo_run_config
  * is the k x k L of the pivot block, res->rank = |pivots|. */
 int rpo_accelerated_rpcholesky_lowmem(const rpo_oracle* o, const rpo_run_config* cfg,
                                       rpo_result* res);
+/* block_rpcholesky (rpcholesky.hpp:268-333) and simple_rpcholesky (206-246); the PivotTrace
+ * "accepted" lists are the kept (sorted, distinct) proposals. */
+int rpo_block_rpcholesky(const rpo_oracle* o, const rpo_run_config* cfg, rpo_result* res);
+int rpo_simple_rpcholesky(const rpo_oracle* o, int64_t k, uint64_t seed, rpo_result* res);
 void rpo_result_free(rpo_result* res);
 double rpo_relative_trace_error(const rpo_oracle* o, const double* factor, int64_t n,
                                 int64_t k);

@@ -33,6 +33,8 @@ EXPORTS = [
     "rpc_result_is_lowmem", "rpc_kernel_matvec", "rpc_krr_fit", "rpc_krr_iterations",
     "rpc_krr_converged", "rpc_krr_residuals", "rpc_krr_coefficients", "rpc_krr_target_mean",
     "rpc_krr_precond_rank", "rpc_krr_precond_pivots", "rpc_krr_predict", "rpc_krr_free",
+    "rpc_block_rpcholesky", "rpc_block_rpcholesky_device", "rpc_simple_rpcholesky",
+    "rpc_simple_rpcholesky_device",
 ]
 
 
@@ -100,6 +102,14 @@ def load() -> C.CDLL:
                                                                KernelSpecC, RunConfigC,
                                                                C.POINTER(vp)]),
         "rpc_result_is_lowmem": (C.c_int, [vp]),
+        "rpc_block_rpcholesky": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
+                                           RunConfigC, C.POINTER(vp)]),
+        "rpc_block_rpcholesky_device": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
+                                                  RunConfigC, C.POINTER(vp)]),
+        "rpc_simple_rpcholesky": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, i64,
+                                            C.c_uint64, C.c_uint32, C.POINTER(vp)]),
+        "rpc_simple_rpcholesky_device": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
+                                                   i64, C.c_uint64, C.c_uint32, C.POINTER(vp)]),
         "rpc_kernel_matvec": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, vp, i64, vp]),
         "rpc_krr_fit": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, vp, C.c_double, i64,
                                   RunConfigC, C.c_double, i64, C.POINTER(vp)]),

@@ -283,6 +283,56 @@ def accelerated_rpcholesky_device(x_dev_ptr: int, n: int, d: int, ld: int, layou
     return _wrap_result(h, ctx)
 
 
+def block_rpcholesky(oracle: KernelOracle, cfg: RunConfig,
+                     ctx: Context | None = None) -> CholeskyResult:
+    """rpchol::block_rpcholesky (rpcholesky.hpp:268-333) on the GPU; `accepted` per round is
+    the kept (sorted, distinct) proposal list."""
+    if not isinstance(oracle, KernelOracle):
+        raise ValueError("block_rpcholesky (B200): only KernelOracle inputs are supported")
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    h = C.c_void_p()
+    L.check(L.load().rpc_block_rpcholesky(ctx.handle, x.ctypes.data, x.shape[0], x.shape[1], ld,
+                                          lay, oracle._c_spec(), cfg.to_c(), C.byref(h)),
+            ctx.handle)
+    return _wrap_result(h, ctx)
+
+
+def simple_rpcholesky(oracle: KernelOracle, k: int, seed: int, ctx: Context | None = None,
+                      replay_scan: bool = False) -> CholeskyResult:
+    """rpchol::simple_rpcholesky (rpcholesky.hpp:206-246) on the GPU."""
+    if not isinstance(oracle, KernelOracle):
+        raise ValueError("simple_rpcholesky (B200): only KernelOracle inputs are supported")
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    h = C.c_void_p()
+    L.check(L.load().rpc_simple_rpcholesky(ctx.handle, x.ctypes.data, x.shape[0], x.shape[1], ld,
+                                           lay, oracle._c_spec(), k, seed,
+                                           L.RPC_FLAG_REPLAY_SCAN if replay_scan else 0,
+                                           C.byref(h)), ctx.handle)
+    return _wrap_result(h, ctx)
+
+
+def block_rpcholesky_device(x_dev_ptr: int, n: int, d: int, ld: int, layout: int,
+                            spec: KernelSpec, cfg: RunConfig, ctx: Context) -> CholeskyResult:
+    o = KernelOracle(np.zeros((1, 1)), spec)
+    h = C.c_void_p()
+    L.check(L.load().rpc_block_rpcholesky_device(ctx.handle, C.c_void_p(x_dev_ptr), n, d, ld,
+                                                 layout, o._c_spec(), cfg.to_c(), C.byref(h)),
+            ctx.handle)
+    return _wrap_result(h, ctx)
+
+
+def simple_rpcholesky_device(x_dev_ptr: int, n: int, d: int, ld: int, layout: int,
+                             spec: KernelSpec, k: int, seed: int, ctx: Context) -> CholeskyResult:
+    o = KernelOracle(np.zeros((1, 1)), spec)
+    h = C.c_void_p()
+    L.check(L.load().rpc_simple_rpcholesky_device(ctx.handle, C.c_void_p(x_dev_ptr), n, d, ld,
+                                                  layout, o._c_spec(), k, seed, 0, C.byref(h)),
+            ctx.handle)
+    return _wrap_result(h, ctx)
+
+
 def accelerated_rpcholesky_lowmem(oracle: KernelOracle, cfg: RunConfig,
                                   ctx: Context | None = None) -> CholeskyResult:
     """rpchol::accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485) on the GPU.

@@ -35,9 +35,10 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 // kernel (lowmem_impl.cuh).  State: X, u, pivot records, L and L^{-1} (k x k).
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
-                       rpc_run_config cfg, rpc_result* res, bool lowmem) {
+                       rpc_run_config cfg, rpc_result* res, bool lowmem, int algo) {
   int kind = 0;
   validate(n, d, kspec, cfg, kind);
+  if (algo != kAlgoAccelerated && lowmem) raise(RPC_EINVAL, "low-memory mode is accelerated-only");
   if (lowmem && round_up(d, 16) > 128)
     raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: this build supports d <= 128");
   if (layout != RPC_COL_MAJOR && layout != RPC_ROW_MAJOR) raise(RPC_EINVAL, "unknown layout");
@@ -151,6 +152,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   DBuf xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * ldf),
       sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
   DBuf shard_c0(ctx, sizeof(int) * (P + 1));
+  DBuf kept_idx, propk;  // block / simple: kept proposals (first draw of each distinct id)
+  if (algo != kAlgoAccelerated) {
+    kept_idx = DBuf(ctx, sizeof(int) * b);
+    propk = DBuf(ctx, sizeof(double) * b * lay.rec);
+  }
   DBuf cumsum;
   if (replay) cumsum = DBuf(ctx, sizeof(double) * n);
   // low-memory state (replicated): pivot records, L and L^{-1} row-major [cap][ldf],
@@ -204,7 +210,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   CK(cudaEventRecord(ev_t0.e, st));
   for (int64_t round = 0;; ++round) {
     if (cfg.mode == RPC_FIXED_ROUNDS ? round >= cfg.rounds : kcur >= cfg.target_rank) break;
-    const uint64_t draw0 = 2ull * (uint64_t)b * (uint64_t)round;
+    // SplitMix64 draw counters: accelerated uses b proposal + b accept draws per round
+    // (rpcholesky.hpp:362-364, 179), block b proposals (293-296), simple one (226)
+    const uint64_t draw0 = (algo == kAlgoAccelerated ? 2ull : 1ull) * (uint64_t)b * (uint64_t)round;
     // -- K2: scan of the residual diagonal (+ previous round's ||G||^2 partials)
     for (Shard& s : res->shards) {
       launch_chunk_totals(s.u.as<double>(), s.n_loc, s.nchunks, totals_all.as<double>() + s.chunk0, st);
@@ -265,6 +273,70 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       launches += 2;
       dbg(st, "lowmem fprop");
     }
+    if (algo != kAlgoAccelerated) {
+      // ---- block_rpcholesky (rpcholesky.hpp:268-333) / simple_rpcholesky (206-246):
+      // every distinct proposal is kept (sorted), its block factored by an all-accepting
+      // sweep (= LLT: fails on a pivot <= 0); block retries once with a diagonal shift.
+      CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus), cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),
+                           sizeof(double), b, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      CK(cudaGetLastError());
+      if (pending_g2) {
+        captured_sq += h_scan->g2_prev;
+        pending_g2 = false;
+      }
+      if (h_scan->exhausted) {
+        res->exhausted = true;
+        break;
+      }
+      if (algo == kAlgoBlock && cfg.stop_tol > 0.0 &&
+          (trace_a - captured_sq) <= cfg.stop_tol * trace_a)
+        break;
+      // kept = unique_sorted(proposed) (rpcholesky.hpp:297); record of its first draw
+      std::vector<std::pair<int64_t, int>> ids(b);
+      for (int j = 0; j < b; ++j) ids[j] = {(int64_t)h_prop_ids[j], j};
+      std::sort(ids.begin(), ids.end());
+      std::vector<int> kidx;
+      for (int j = 0; j < b; ++j)
+        if (j == 0 || ids[j].first != ids[j - 1].first) kidx.push_back(ids[j].second);
+      const int mk = (int)kidx.size();
+      CK(cudaMemcpyAsync(kept_idx.p, kidx.data(), sizeof(int) * mk, cudaMemcpyHostToDevice, st));
+      launch_gather_records(prop.as<double>(), lay.rec, 2 + dpad + kcur, kept_idx.as<int>(), mk,
+                            propk.as<double>(), st);
+      launch_hblock(propk.as<double>(), lay, mk, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
+                    Hbuf.as<double>(), st);
+      launches += 2;
+      for (int attempt = 0;; ++attempt) {
+        launch_sweep(Hbuf.as<double>(), mk, cfg.seed, 0, propk.as<double>(), lay, pos.as<int>(),
+                     acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(), d_sweep,
+                     hp.as<double>(), st, 1);
+        ++launches;
+        CK(cudaMemcpyAsync(h_sweep, d_sweep, sizeof(SweepOut), cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        if (h_sweep->m == mk) break;
+        if (algo == kAlgoSimple) break;  // !(g[s] > 0): rank exhausted (rpcholesky.hpp:229-232)
+        if (attempt == 1)
+          raise(RPC_ENUMERIC, "block_rpcholesky: Cholesky failed after diagonal shift");
+        // shift = 64 eps tr(A) / N (rpcholesky.hpp:313-315); tr(A) = N for kernel oracles
+        launch_add_diag(Hbuf.as<double>(), mk, 64.0 * 2.220446049250313e-16 * trace_a / (double)n, st);
+        ++launches;
+      }
+      if (algo == kAlgoSimple && h_sweep->m != mk) {
+        res->exhausted = true;
+        break;
+      }
+      CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+      launch_linv(lacc.as<double>(), mk, (int)nbl, ldl, (int)(kcur & 1), linv.as<double>(), st);
+      launch_gather_accepted(propk.as<double>(), lay, pos.as<int>(), mk, 256, 0, (int)dpad,
+                             xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
+                             idS.as<double>(), st);
+      launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), propk.as<double>(), lay,
+                    pos.as<int>(), &d_sweep->m, mk, (int)kcur, fs.as<double>(), ldf, st);
+      launches += 3;
+      CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * mk, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+    } else {
     // -- K3: H block; K4: rejection sweep (replicated on every shard)
     launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
                   Hbuf.as<double>(), st);
@@ -294,6 +366,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                          sizeof(double), b, cudaMemcpyDeviceToHost, st));
     CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    }  // accelerated
     CK(cudaGetLastError());
     if (pending_g2) {
       captured_sq += h_scan->g2_prev;  // captured_sq += ||G||_F^2 (rpcholesky.hpp:388)
@@ -311,6 +384,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     if (m > 0) {
       if (kcur + m > cap)
         raise(RPC_ENUMERIC, "accelerated_rpcholesky: factor capacity exceeded (duplicate pivot)");
+      // (block / simple: kept blocks have m <= b, so cap = min(N, k + b) always suffices)
       CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
       if (lowmem) {
         // L_new = [[L, 0], [F_S, L_sel]]; L_new^{-1} rows [kcur, kcur+m) =
@@ -706,6 +780,67 @@ int rpc_accelerated_rpcholesky_lowmem_device(rpc_ctx* ctx, const double* x_dev, 
   }
   *out = r;
   return RPC_OK;
+}
+
+static int run_algo(rpc_ctx* ctx, const double* x, bool on_device, int64_t n, int64_t d,
+                    int64_t ldx, int layout, rpc_kernel_spec kernel, rpc_run_config cfg, int algo,
+                    rpc_result** out) {
+  if (!ctx || !out) return fail(ctx, RPC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *out = nullptr;
+  rpc_result* r = new_result();
+  int rc = guarded(ctx, [&] {
+    if (!x && n > 0) raise(RPC_EINVAL, "null point matrix");
+    if (!on_device && ldx < (layout == RPC_ROW_MAJOR ? d : n))
+      raise(RPC_EINVAL, "leading dimension too small");
+    run_factorization(ctx, x, on_device, n, d, ldx, layout, kernel, cfg, r, false, algo);
+  });
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return RPC_OK;
+}
+
+int rpc_block_rpcholesky(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                         int layout, rpc_kernel_spec kernel, rpc_run_config cfg, rpc_result** out) {
+  if (cfg.block_size < 1) return fail(ctx, RPC_EINVAL, "block_rpcholesky: block size must be >= 1");
+  return run_algo(ctx, x, false, n, d, ldx, layout, kernel, cfg, kAlgoBlock, out);
+}
+
+int rpc_block_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, int64_t d,
+                                int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                rpc_run_config cfg, rpc_result** out) {
+  if (cfg.block_size < 1) return fail(ctx, RPC_EINVAL, "block_rpcholesky: block size must be >= 1");
+  return run_algo(ctx, x_dev, true, n, d, ldx, layout, kernel, cfg, kAlgoBlock, out);
+}
+
+static rpc_run_config simple_cfg(int64_t k, uint64_t seed, uint32_t flags) {
+  rpc_run_config c{};
+  c.block_size = 1;
+  c.mode = RPC_UNTIL_RANK;
+  c.target_rank = k;
+  c.seed = seed;
+  c.stop_tol = 0.0;
+  c.flags = flags;
+  return c;
+}
+
+int rpc_simple_rpcholesky(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                          int layout, rpc_kernel_spec kernel, int64_t k, uint64_t seed,
+                          uint32_t flags, rpc_result** out) {
+  if (k < 1 || k > n) return fail(ctx, RPC_EINVAL, "simple_rpcholesky: need 1 <= k <= N");
+  return run_algo(ctx, x, false, n, d, ldx, layout, kernel, simple_cfg(k, seed, flags),
+                  kAlgoSimple, out);
+}
+
+int rpc_simple_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, int64_t d,
+                                 int64_t ldx, int layout, rpc_kernel_spec kernel, int64_t k,
+                                 uint64_t seed, uint32_t flags, rpc_result** out) {
+  if (k < 1 || k > n) return fail(ctx, RPC_EINVAL, "simple_rpcholesky: need 1 <= k <= N");
+  return run_algo(ctx, x_dev, true, n, d, ldx, layout, kernel, simple_cfg(k, seed, flags),
+                  kAlgoSimple, out);
 }
 
 int rpc_result_is_lowmem(const rpc_result* r) { return r ? (int)r->lowmem : 0; }

@@ -72,7 +72,12 @@ struct SweepOut {
 // column-major), status.
 void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
                   RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
-                  SweepOut* out, double* scratch_hp, cudaStream_t st);
+                  SweepOut* out, double* scratch_hp, cudaStream_t st, int accept_all = 0);
+// H[i][i] += shift (block_rpcholesky's LLT retry, rpcholesky.hpp:311-319)
+void launch_add_diag(double* H, int b, double shift, cudaStream_t st);
+// out[j] = first `words` of record prop[idx[j]] (stride rec), j < m
+void launch_gather_records(const double* prop, int64_t rec, int64_t words, const int* idx, int m,
+                           double* out, cudaStream_t st);
 // linv_rm[perm_row(a)][c + koff] = (L^{-1})[a][c], [nb][ldl], zero elsewhere (koff = kcur & 1,
 // matching the update kernel's 16-byte-aligned phase-2 tiles).
 void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,

@@ -275,8 +275,10 @@ struct Ev {
 
 // The factorization proper (api.cu).  `src` points to this process's shard rows
 // (device memory when src_on_device, else host memory of the full X).
+enum { kAlgoAccelerated = 0, kAlgoBlock = 1, kAlgoSimple = 2 };
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
-                       rpc_run_config cfg, rpc_result* res, bool lowmem = false);
+                       rpc_run_config cfg, rpc_result* res, bool lowmem = false,
+                       int algo = kAlgoAccelerated);
 
 }  // namespace rpcb_rt

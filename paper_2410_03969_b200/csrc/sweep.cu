@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     const double* __restrict__ H, int b, uint64_t seed, uint64_t draw0,
     const double* __restrict__ prop, RecordLayout lay, int* __restrict__ pos,
     int64_t* __restrict__ acc_ids, double* __restrict__ lcol, double* __restrict__ lacc_cm,
-    SweepOut* out, double* hp_global) {
+    SweepOut* out, double* hp_global, int accept_all) {
   extern __shared__ double sm[];
   __shared__ int s_m, s_nacc, s_acc[kSweepBlock];
   __shared__ double s_root[kSweepBlock];
@@ -89,7 +89,9 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   for (int p = warp; p < b; p += nwarps)
     for (int q = lane; q <= p; q += 32) hp[tri(p) + q] = H[(int64_t)p * b + q];
   for (int i = tid; i < b; i += kSweepThreads) {
-    rdraw[i] = u01(splitmix64_draw(seed, draw0 + (uint64_t)i));
+    // accept_all (block / simple RPCholesky): r = 0, so a row is kept iff h_ii > 0 — the
+    // LLT success condition (Eigen fails on the first pivot <= 0)
+    rdraw[i] = accept_all ? 0.0 : u01(splitmix64_draw(seed, draw0 + (uint64_t)i));
     udiag[i] = H[(int64_t)i * b + i];
   }
   if (tid == 0) s_m = 0;
@@ -177,7 +179,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
 
 void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
                   RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
-                  SweepOut* out, double* scratch_hp, cudaStream_t st) {
+                  SweepOut* out, double* scratch_hp, cudaStream_t st, int accept_all) {
   const size_t packed = (size_t)b * (b + 1) / 2;
   size_t smem = sizeof(double) * (2 * (size_t)b + kSweepBlock * kSweepBlock + kSweepBlock * (size_t)b);
   double* hpg = nullptr;
@@ -192,7 +194,7 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
     attr = true;
   }
   sweep_kernel<<<1, kSweepThreads, smem, st>>>(H, b, seed, draw0, prop, lay, pos, acc_ids, lcol,
-                                                lacc_cm, out, hpg);
+                                                lacc_cm, out, hpg, accept_all);
 }
 
 // L^{-1} by forward substitution L x = e_c, one warp per column c (8 columns per
@@ -273,6 +275,31 @@ void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb,
   const int in_smem = bytes <= 200 * 1024;
   linv_kernel<<<(m_max + kLinvWarps - 1) / kLinvWarps, 32 * kLinvWarps, in_smem ? bytes : 0,
                 st>>>(lacc_cm, 0, m_dev, nb, ldl, koff, in_smem, linv_rm);
+}
+
+}  // namespace rpcb
+
+namespace rpcb {
+
+__global__ void add_diag_shift_kernel(double* H, int b, double shift) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < b) H[(int64_t)i * b + i] += shift;
+}
+
+void launch_add_diag(double* H, int b, double shift, cudaStream_t st) {
+  add_diag_shift_kernel<<<(b + 127) / 128, 128, 0, st>>>(H, b, shift);
+}
+
+__global__ void gather_records_kernel(const double* __restrict__ prop, int64_t rec, int64_t words,
+                                      const int* __restrict__ idx, double* __restrict__ out) {
+  const double* src = prop + (int64_t)idx[blockIdx.x] * rec;
+  double* dst = out + (int64_t)blockIdx.x * rec;
+  for (int64_t w = threadIdx.x; w < words; w += blockDim.x) dst[w] = src[w];
+}
+
+void launch_gather_records(const double* prop, int64_t rec, int64_t words, const int* idx, int m,
+                           double* out, cudaStream_t st) {
+  if (m > 0) gather_records_kernel<<<m, 256, 0, st>>>(prop, rec, words, idx, out);
 }
 
 }  // namespace rpcb

@@ -10,7 +10,9 @@ accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485) answers: pivots, trace,
 chol_factor and residual diagonal.
 `krr` fixtures (ref_krr_*.npz) carry fit_krr + predict (krr.hpp:177-250): coefficients,
 PCG report, preconditioner pivots and predictions on a held-out query set.
-Run:  python tests/golden/make_ref_fixtures.py [standard|lowmem|krr|all]
+`baselines` fixtures (ref_block_*.npz, ref_simple_*.npz) carry block_rpcholesky and
+simple_rpcholesky (rpcholesky.hpp:206-333).
+Run:  python tests/golden/make_ref_fixtures.py [standard|lowmem|krr|baselines|all]
 """
 import math
 import os
@@ -84,6 +86,33 @@ def make_krr():
         print("krr", name, "iters", r["iterations"], "converged", r["converged"])
 
 
+# block_rpcholesky / simple_rpcholesky (rpcholesky.hpp:206-333): (algo, generator, n, d,
+# kernel, sigma, k, b, seed)
+BASELINE_CASES = {
+    "block_c1": ("block", "C1", 20000, 10, "gaussian", math.sqrt(10.0), 200, 40, 0),
+    "block_c3s": ("block", "C3", 6000, 50, "l1laplace", 5.0, 300, 120, 0),
+    "simple_c1s": ("simple", "C1", 6000, 10, "gaussian", math.sqrt(10.0), 150, 1, 0),
+}
+
+
+def make_baselines():
+    for name, (algo, gen, n, d, kern, sigma, k, b, seed) in BASELINE_CASES.items():
+        x = wl.GENERATORS[gen](n, d, 0)
+        if algo == "block":
+            r = pyref.block_rpcholesky_kernel(x, kern, sigma, block_size=b, target_rank=k, seed=seed)
+        else:
+            r = pyref.simple_rpcholesky_kernel(x, kern, sigma, k, seed)
+        acc_counts = np.array([len(a) for a in r.accepted], np.int64)
+        np.savez_compressed(
+            os.path.join(HERE, f"ref_{name}.npz"),
+            config=np.array([algo, gen, str(n), str(d), kern, repr(sigma), str(k), str(b), str(seed)]),
+            pivots=r.pivots, proposed=np.array(r.proposed), accepted_counts=acc_counts,
+            rank_exhausted=np.array(r.rank_exhausted), surplus=np.array(r.surplus),
+            chol=r.chol, col_sums=r.factor.sum(axis=0), col_sqnorms=(r.factor ** 2).sum(axis=0),
+            residual_diag=r.residual_diag, factor_rows_probe=r.factor[:: max(1, n // 64)])
+        print(name, "rank", r.factor.shape[1], "rounds", len(r.proposed))
+
+
 def make_standard():
     for name, (gen, n, d, kern, sigma, k, b, seed) in CASES.items():
         x = wl.GENERATORS[gen](n, d, 0)
@@ -110,3 +139,5 @@ if __name__ == "__main__":
         make_lowmem()
     if what in ("krr", "all"):
         make_krr()
+    if what in ("baselines", "all"):
+        make_baselines()
