@@ -169,6 +169,13 @@ double rpc_result_relative_trace_error(const rpc_result* r);
 const double* rpc_result_factor_device(const rpc_result* r, int64_t* ldf, int64_t* row0,
                                        int64_t* nrows);
 
+/* write_rpcf (io.hpp:218-256) from the device-resident result: byte-identical to the
+ * reference's file for the same factor, pivots and chol_factor.  Under NCCL every rank
+ * calls it with the same path on a shared filesystem; each writes its own rows. */
+int rpc_result_write_rpcf(const rpc_result* r, const char* path);
+/* write_pivot_trace_csv (io.hpp:336-350). */
+int rpc_result_write_trace_csv(const rpc_result* r, const char* path);
+
 typedef struct {
   double factorize_ms;     /* device time, first kernel to factor complete (CUDA events) */
   double upload_ms;        /* X host->device + packing */

@@ -282,3 +282,62 @@ def relative_trace_error(oracle: Oracle, factor: np.ndarray) -> float:
     f = np.asfortranarray(factor, dtype=np.float64)
     return float(lib().rpo_relative_trace_error(C.byref(oracle._o), _p(f), f.shape[0],
                                                 f.shape[1]))
+
+
+# ---- io.hpp:218-293, 336-350: RPCF factor file and pivot-trace CSV (restatement) ----------
+def write_rpcf(path: str, factor: np.ndarray, pivots, chol: np.ndarray | None) -> None:
+    """write_rpcf (io.hpp:218-256): "RPCF", u32 1, u64 N, u64 k, factor column-major f64 LE,
+    k u64 pivots, u64 packed count, chol lower triangle row by row."""
+    import struct
+    f = np.asarray(factor, dtype="<f8")
+    n, k = f.shape
+    piv = np.asarray(pivots, dtype="<u8")
+    if piv.size != k:
+        raise ValueError("write_rpcf: pivot count must match factor columns")
+    has_chol = chol is not None and chol.shape == (k, k) and k > 0
+    with open(path, "wb") as fh:
+        fh.write(b"RPCF" + struct.pack("<IQQ", 1, n, k))
+        fh.write(np.asfortranarray(f).tobytes(order="F"))
+        fh.write(piv.tobytes())
+        fh.write(struct.pack("<Q", k * (k + 1) // 2 if has_chol else 0))
+        if has_chol:
+            fh.write(np.concatenate([np.asarray(chol, "<f8")[i, : i + 1] for i in range(k)]).tobytes())
+
+
+def read_rpcf(path: str):
+    """read_rpcf (io.hpp:258-293): (factor N x k, pivots int64, chol k x k or None)."""
+    import struct
+    with open(path, "rb") as fh:
+        data = fh.read()
+    if data[:4] != b"RPCF":
+        raise RuntimeError(f"read_rpcf: bad magic in {path}")
+    ver, n, k = struct.unpack_from("<IQQ", data, 4)
+    if ver != 1:
+        raise RuntimeError("read_rpcf: unsupported version")
+    off = 24
+    factor = np.frombuffer(data, "<f8", n * k, off).reshape((n, k), order="F").copy()
+    off += 8 * n * k
+    piv = np.frombuffer(data, "<u8", k, off).astype(np.int64)
+    off += 8 * k
+    (cnt,) = struct.unpack_from("<Q", data, off)
+    off += 8
+    chol = None
+    if cnt:
+        if cnt != k * (k + 1) // 2:
+            raise RuntimeError("read_rpcf: unexpected Cholesky payload size")
+        vals = np.frombuffer(data, "<f8", cnt, off)
+        chol = np.zeros((k, k))
+        p = 0
+        for i in range(k):
+            chol[i, : i + 1] = vals[p: p + i + 1]
+            p += i + 1
+    return factor, piv, chol
+
+
+def write_pivot_trace_csv(path: str, proposed, accepted) -> None:
+    """write_pivot_trace_csv (io.hpp:336-350)."""
+    with open(path, "w") as fh:
+        fh.write("round,proposed,accepted,acceptance_rate\n")
+        for r, (p, a) in enumerate(zip(proposed, accepted)):
+            rate = len(a) / len(p) if len(p) else 0.0
+            fh.write(f"{r},{len(p)},{len(a)},{'%.17g' % rate}\n")

@@ -33,6 +33,9 @@ def lib():
         L.ref_accelerated_kernel.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, i64, C.c_int, i64,
                                              i64, C.c_uint64, d, C.POINTER(po._Res)]
         L.ref_lowmem_kernel.argtypes = L.ref_accelerated_kernel.argtypes
+        L.ref_read_rpcf.argtypes = [C.c_char_p, C.POINTER(po._Res)]
+        L.ref_write_rpcf_kernel.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, i64, i64,
+                                            C.c_uint64, C.c_char_p, C.c_char_p]
         L.ref_block_kernel.argtypes = L.ref_accelerated_kernel.argtypes
         L.ref_simple_kernel.argtypes = [vp, i64, i64, C.c_int, d, C.c_int, i64, C.c_uint64,
                                         C.POINTER(po._Res)]
@@ -213,3 +216,21 @@ def fit_krr(x, targets, kernel, sigma, mu, precond_rank, block_size, seed, tol, 
     return dict(coefficients=coef, target_mean=mean.value, iterations=it, converged=bool(conv.value),
                 relative_residuals=rel[:it].copy(), relative_residuals_unreg=unreg[:it].copy(),
                 pivots=piv[:k.value].copy(), predictions=pred if qf is not None else None)
+
+
+def read_rpcf(path):
+    """read_rpcf (io.hpp:258-293): (factor N x k, pivots, chol k x k)."""
+    res = po._Res()
+    _check(lib().ref_read_rpcf(path.encode(), C.byref(res)))
+    r = _unpack(res)
+    return r.factor, r.pivots, r.chol
+
+
+def write_rpcf_kernel(x, kernel, sigma, block_size, target_rank, seed, path, trace_csv=None, dist=None):
+    """The reference's accelerated run written by its own write_rpcf / write_pivot_trace_csv."""
+    xf = np.asfortranarray(x, dtype=np.float64)
+    kind = po.KERNELS[kernel]
+    dm = po.DIST[dist or ("direct" if kind == 1 else "gram")]
+    _check(lib().ref_write_rpcf_kernel(xf.ctypes.data, xf.shape[0], xf.shape[1], kind, sigma, dm,
+                                       block_size, target_rank, seed, path.encode(),
+                                       trace_csv.encode() if trace_csv else None))

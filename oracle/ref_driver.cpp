@@ -13,6 +13,7 @@
 #include <string>
 #include <vector>
 
+#include "rpchol/io.hpp"
 #include "rpchol/krr.hpp"
 #include "rpchol/rpcholesky.hpp"
 
@@ -309,6 +310,46 @@ int ref_fit_krr(const double* x, int64_t n, int64_t d, int kind, double sigma,
       Eigen::VectorXd p = rpchol::predict(fit.model, rpchol::DataMatrix(std::move(q)));
       std::memcpy(pred, p.data(), sizeof(double) * (size_t)nq);
     }
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// read_rpcf (io.hpp:258-293) -> Res (factor, pivots, chol; chol empty -> rank x rank zeros)
+int ref_read_rpcf(const char* path, Res* out) {
+  try {
+    rpchol::LowRankApprox a = rpchol::read_rpcf(path);
+    std::memset(out, 0, sizeof *out);
+    out->n = a.factor.rows();
+    out->rank = a.factor.cols();
+    out->factor = dup(a.factor.data(), (size_t)(a.factor.rows() * a.factor.cols()));
+    std::vector<int64_t> piv(a.pivots.begin(), a.pivots.end());
+    out->pivots = dup(piv.data(), piv.size());
+    Eigen::MatrixXd c = a.chol_factor.rows() ? a.chol_factor
+                                             : Eigen::MatrixXd::Zero(a.factor.cols(), a.factor.cols());
+    out->chol = dup(c.data(), (size_t)(c.rows() * c.cols()));
+    Eigen::VectorXd z = Eigen::VectorXd::Zero(out->n);
+    out->residual_diag = dup(z.data(), (size_t)out->n);
+    out->proposed = dup<int64_t>(nullptr, 0);
+    out->accepted_count = dup<int64_t>(nullptr, 0);
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return code_of(e);
+  }
+}
+
+// write_rpcf (io.hpp:218-256) of a reference accelerated run -> the reference's own bytes
+int ref_write_rpcf_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma, int dist,
+                          int64_t b, int64_t k, uint64_t seed, const char* path,
+                          const char* trace_csv) {
+  try {
+    auto oracle = make_kernel(x, n, d, kind, sigma, dist);
+    auto res = rpchol::accelerated_rpcholesky(oracle, rpchol::RunConfig::until_rank(k, b, seed));
+    rpchol::write_rpcf(path, res.approx);
+    if (trace_csv) rpchol::write_pivot_trace_csv(trace_csv, res.trace);
     return 0;
   } catch (const std::exception& e) {
     g_err = e.what();

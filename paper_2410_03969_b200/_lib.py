@@ -34,7 +34,7 @@ EXPORTS = [
     "rpc_krr_converged", "rpc_krr_residuals", "rpc_krr_coefficients", "rpc_krr_target_mean",
     "rpc_krr_precond_rank", "rpc_krr_precond_pivots", "rpc_krr_predict", "rpc_krr_free",
     "rpc_block_rpcholesky", "rpc_block_rpcholesky_device", "rpc_simple_rpcholesky",
-    "rpc_simple_rpcholesky_device",
+    "rpc_simple_rpcholesky_device", "rpc_result_write_rpcf", "rpc_result_write_trace_csv",
 ]
 
 
@@ -102,6 +102,8 @@ def load() -> C.CDLL:
                                                                KernelSpecC, RunConfigC,
                                                                C.POINTER(vp)]),
         "rpc_result_is_lowmem": (C.c_int, [vp]),
+        "rpc_result_write_rpcf": (C.c_int, [vp, C.c_char_p]),
+        "rpc_result_write_trace_csv": (C.c_int, [vp, C.c_char_p]),
         "rpc_block_rpcholesky": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
                                            RunConfigC, C.POINTER(vp)]),
         "rpc_block_rpcholesky_device": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,

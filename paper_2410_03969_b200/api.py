@@ -220,6 +220,14 @@ class CholeskyResult:
                 self._ctx.handle)
         return out
 
+    def write_rpcf(self, path: str) -> None:
+        """write_rpcf (io.hpp:218-256), streamed from the device-resident factor."""
+        L.check(L.load().rpc_result_write_rpcf(self._handle, path.encode()), self._ctx.handle)
+
+    def write_trace_csv(self, path: str) -> None:
+        """write_pivot_trace_csv (io.hpp:336-350)."""
+        L.check(L.load().rpc_result_write_trace_csv(self._handle, path.encode()), self._ctx.handle)
+
     def free(self):
         if self._handle:
             L.load().rpc_result_free(self._handle)

@@ -676,6 +676,7 @@ void rpc_destroy(rpc_ctx* ctx) {
   for (auto fn : ctx->on_destroy) fn(ctx);
   ctx->trim();
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
+  if (ctx->io_pinned) cudaFreeHost(ctx->io_pinned);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;

@@ -81,6 +81,8 @@ struct rpc_ctx {
   std::multimap<size_t, void*> pool;  // cached device blocks (size -> ptr)
   void* host_pinned = nullptr;
   size_t host_pinned_bytes = 0;
+  void* io_pinned = nullptr;  // RPCF writer staging (2 halves), grown on demand
+  size_t io_pinned_bytes = 0;
   void* blas = nullptr;    // cublasHandle_t (KRR preconditioner, created on first use)
   void* solver = nullptr;  // cusolverDnHandle_t
   std::vector<void (*)(rpc_ctx*)> on_destroy;
