@@ -198,6 +198,23 @@ void rpc_result_free(rpc_result* r);
 int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
                        int layout, rpc_kernel_spec kernel, const int64_t* cols, int64_t m,
                        double* out, int64_t ld_out, double* device_ms);
+/* bench_column_throughput (experiment.hpp:344-387): ~1000 columns drawn as
+ * SplitMix64(seed).next_u64() % N, generated on the device in blocks of each requested
+ * size (one standalone K5 launch per block of <= 256 columns, output kept in HBM), for the
+ * Direct and (Gaussian only) GramTrick modes.  rows needs 2 * n_sizes entries; wall_ms
+ * is device time (CUDA events) after one warm-up pass; output_gbs = 8 N columns / time. */
+typedef struct {
+  int64_t block_size;
+  int distance_mode; /* rpc_distance_mode */
+  int64_t columns;
+  double wall_ms;
+  double columns_per_sec;
+  double output_gbs; /* kernel-col GB/s (BASELINE metric) */
+} rpc_throughput_row;
+int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                                int layout, rpc_kernel_spec kernel, const int64_t* block_sizes,
+                                int n_sizes, uint64_t seed, rpc_throughput_row* rows,
+                                int* n_rows);
 /* b draws of sample_discrete (rng.hpp:80-96) against cumulative_sums(u), using
  * SplitMix64(seed) draws [draw0, draw0+b).  replay != 0: sequential scan. */
 int rpc_sample_discrete(rpc_ctx* ctx, const double* u, int64_t n, int64_t b, uint64_t seed,

@@ -35,6 +35,7 @@ EXPORTS = [
     "rpc_krr_precond_rank", "rpc_krr_precond_pivots", "rpc_krr_predict", "rpc_krr_free",
     "rpc_block_rpcholesky", "rpc_block_rpcholesky_device", "rpc_simple_rpcholesky",
     "rpc_simple_rpcholesky_device", "rpc_result_write_rpcf", "rpc_result_write_trace_csv",
+    "rpc_bench_column_throughput",
 ]
 
 
@@ -52,6 +53,12 @@ class RunConfigC(C.Structure):
         ("stop_tol", C.c_double),
         ("flags", C.c_uint32),
     ]
+
+
+class ThroughputRowC(C.Structure):
+    _fields_ = [("block_size", C.c_int64), ("distance_mode", C.c_int), ("columns", C.c_int64),
+                ("wall_ms", C.c_double), ("columns_per_sec", C.c_double),
+                ("output_gbs", C.c_double)]
 
 
 class TimingC(C.Structure):
@@ -103,6 +110,8 @@ def load() -> C.CDLL:
                                                                C.POINTER(vp)]),
         "rpc_result_is_lowmem": (C.c_int, [vp]),
         "rpc_result_write_rpcf": (C.c_int, [vp, C.c_char_p]),
+        "rpc_bench_column_throughput": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, vp,
+                                                  C.c_int, C.c_uint64, vp, C.POINTER(C.c_int)]),
         "rpc_result_write_trace_csv": (C.c_int, [vp, C.c_char_p]),
         "rpc_block_rpcholesky": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
                                            RunConfigC, C.POINTER(vp)]),

@@ -371,6 +371,24 @@ def accelerated_rpcholesky_lowmem_device(x_dev_ptr: int, n: int, d: int, ld: int
     return _wrap_result(h, ctx)
 
 
+def bench_column_throughput(oracle: KernelOracle, block_sizes, seed: int = 0,
+                            ctx: Context | None = None) -> list:
+    """bench_column_throughput (experiment.hpp:344-387) on the device: one dict per
+    (block size, distance mode) with columns, wall_ms (device), columns_per_sec, output_gbs."""
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    bs = np.ascontiguousarray(block_sizes, dtype=np.int64)
+    rows = (L.ThroughputRowC * (2 * bs.size))()
+    nr = C.c_int()
+    L.check(L.load().rpc_bench_column_throughput(ctx.handle, x.ctypes.data, x.shape[0], x.shape[1],
+                                                 ld, lay, oracle._c_spec(), bs.ctypes.data, bs.size,
+                                                 seed, rows, C.byref(nr)), ctx.handle)
+    names = {L.RPC_DIST_DIRECT: "direct", L.RPC_DIST_GRAM: "gram"}
+    return [dict(block_size=r.block_size, mode=names[r.distance_mode], columns=r.columns,
+                 wall_ms=r.wall_ms, columns_per_sec=r.columns_per_sec, output_gbs=r.output_gbs)
+            for r in rows[: nr.value]]
+
+
 def relative_trace_error(oracle: KernelOracle, result: CholeskyResult) -> float:
     """rpcholesky.hpp:577-583, evaluated from the device-resident factor."""
     return result.relative_trace_error

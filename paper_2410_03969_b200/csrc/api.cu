@@ -965,7 +965,131 @@ void rpc_result_free(rpc_result* r) {
   delete r;
 }
 
+// ---- bench_column_throughput (experiment.hpp:344-387) ------------------------------
+namespace rpcb_rt {
+// prop[j] = record of column point cols[j] = SplitMix64(seed) draw (draw0 + j) mod n
+__global__ void draw_column_records_kernel(const double* __restrict__ X, const double* __restrict__ sqn,
+                                           int64_t n, int64_t dpad, uint64_t seed, uint64_t draw0,
+                                           RecordLayout lay, double* __restrict__ prop) {
+  const int j = blockIdx.x;
+  const int64_t c = (int64_t)(splitmix64_draw(seed, draw0 + (uint64_t)j) % (uint64_t)n);
+  double* rec = prop + (int64_t)j * lay.rec;
+  if (threadIdx.x == 0) {
+    rec[0] = (double)c;
+    rec[1] = sqn[c];
+  }
+  for (int64_t i = threadIdx.x; i < dpad; i += blockDim.x) rec[lay.xoff + i] = X[c * dpad + i];
+}
+}  // namespace rpcb_rt
+
 // ---- component entry points --------------------------------------------------
+int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
+                                int layout, rpc_kernel_spec kspec, const int64_t* block_sizes,
+                                int n_sizes, uint64_t seed, rpc_throughput_row* rows,
+                                int* n_rows) {
+  if (!ctx) return fail(nullptr, RPC_EINVAL, "null context");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  return guarded(ctx, [&] {
+    int kind0 = 0;
+    rpc_run_config cfg{1, RPC_UNTIL_RANK, 0, 1, 0, 0.0, 0};
+    validate(n, d, kspec, cfg, kind0);
+    CK(cudaSetDevice(ctx->device));
+    cudaStream_t st = ctx->stream;
+    const int64_t dpad = round_up(d, 16);
+    DBuf X(ctx, sizeof(double) * n * dpad), sqn(ctx, sizeof(double) * n),
+        raw(ctx, sizeof(double) * n * d);
+    if (layout == RPC_ROW_MAJOR)
+      CK(cudaMemcpy2DAsync(raw.p, d * 8, x, ldx * 8, d * 8, n, cudaMemcpyHostToDevice, st));
+    else
+      CK(cudaMemcpy2DAsync(raw.p, n * 8, x, ldx * 8, n * 8, d, cudaMemcpyHostToDevice, st));
+    launch_pack_points(raw.as<double>(), n, (int)d, layout == RPC_ROW_MAJOR ? d : n,
+                       layout == RPC_ROW_MAJOR, dpad, X.as<double>(), sqn.as<double>(), nullptr, st);
+    RecordLayout lay{2 + dpad, 2, 2 + dpad};
+    // Gaussian: Direct and GramTrick (is_l2_translation_invariant); l1: Direct only
+    std::vector<int> modes{RPC_DIST_DIRECT};
+    if (kspec.kind == RPC_KERNEL_GAUSSIAN) modes.push_back(RPC_DIST_GRAM);
+    int64_t maxb = 1;
+    for (int i = 0; i < n_sizes; ++i) {
+      if (block_sizes[i] < 1) raise(RPC_EINVAL, "bench_column_throughput: block size must be >= 1");
+      maxb = std::max(maxb, block_sizes[i]);
+    }
+    const int64_t mb = std::min<int64_t>(maxb, 256);
+    DBuf prop(ctx, sizeof(double) * 256 * lay.rec), pos(ctx, sizeof(int) * 256),
+        outd(ctx, sizeof(double) * n * mb), tile(ctx, sizeof(double) * (n / 64 + 2)),
+        xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * 16),
+        sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
+    std::vector<int> hpos(256);
+    for (int i = 0; i < 256; ++i) hpos[i] = i;
+    CK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * 256, cudaMemcpyHostToDevice, st));
+    int nr = 0;
+    for (int i = 0; i < n_sizes; ++i) {
+      const int64_t b = block_sizes[i];
+      for (int mode : modes) {
+        rpc_kernel_spec ks = kspec;
+        ks.distance_mode = mode;
+        int kind = 0;
+        validate(n, d, ks, cfg, kind);
+        const int64_t n_blocks = (1000 + b - 1) / b;
+        auto run = [&]() {
+          for (int64_t blk = 0; blk < n_blocks; ++blk) {
+            // one oracle.columns(cols) call: b columns, in launches of <= 256
+            for (int64_t c0 = 0; c0 < b; c0 += 256) {
+              const int nc = (int)std::min<int64_t>(256, b - c0);
+              draw_column_records_kernel<<<nc, 64, 0, st>>>(X.as<double>(), sqn.as<double>(), n,
+                                                             dpad, seed, (uint64_t)(blk * b + c0),
+                                                             lay, prop.as<double>());
+              launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), nc, 256, 0, (int)dpad,
+                                     xs.as<double>(), fs.as<double>(), 16, sqnS.as<double>(),
+                                     idS.as<double>(), st);
+              UpdateParams up{};
+              up.X = X.as<double>();
+              up.dpad = dpad;
+              up.dchunks = (int)(dpad / 16);
+              up.sqn = sqn.as<double>();
+              up.F = X.as<double>();
+              up.ldf = dpad;
+              up.n_loc = n;
+              up.xs = xs.as<double>();
+              up.fs = fs.as<double>();
+              up.ldfs = 16;
+              up.sqnS = sqnS.as<double>();
+              up.idS = idS.as<double>();
+              up.m = nc;
+              up.linv = xs.as<double>();
+              up.ldl = 16;
+              up.sigma = ks.sigma;
+              up.kind = kind;
+              up.escale = kind == kL1 ? -1.0 / ks.sigma : -0.5 / (ks.sigma * ks.sigma);
+              up.tile_g2 = tile.as<double>();
+              up.columns_only = 1;
+              up.cols_out = outd.as<double>() + (c0 % mb) * n;
+              up.ld_out = n;
+              if (launch_update(up, st) < 0) raise(RPC_ECUDA, "kernel-column launch failed");
+            }
+          }
+        };
+        run();  // warm-up (module load, TMA descriptors)
+        Ev e0, e1;
+        CK(cudaEventRecord(e0.e, st));
+        run();
+        CK(cudaEventRecord(e1.e, st));
+        CK(cudaEventSynchronize(e1.e));
+        CK(cudaGetLastError());
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0.e, e1.e));
+        rpc_throughput_row& r = rows[nr++];
+        r.block_size = b;
+        r.distance_mode = mode;
+        r.columns = n_blocks * b;
+        r.wall_ms = ms;
+        r.columns_per_sec = ms > 0 ? 1000.0 * (double)r.columns / ms : 0.0;
+        r.output_gbs = ms > 0 ? 8.0 * (double)n * (double)r.columns / (ms * 1e-3) / 1e9 : 0.0;
+      }
+    }
+    *n_rows = nr;
+  });
+}
+
 int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
                        int layout, rpc_kernel_spec kspec, const int64_t* cols, int64_t m,
                        double* out, int64_t ld_out, double* device_ms) {
