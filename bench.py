@@ -284,7 +284,8 @@ def main():
     e2e = None
     if not args.no_e2e:
         xh = torch.from_numpy(np.ascontiguousarray(x)).pin_memory().numpy()
-        fout = torch.empty((nr * max(k_final, 1) + k_final * k_final + nr + 16,),
+        cap = api.factor_capacity(w.n, cfg)
+        fout = torch.empty((nr * cap + cap * cap + nr + 16,),
                            dtype=torch.float64).pin_memory().numpy()
         ko = api.KernelOracle(xh, spec)
         e2e_times = []
@@ -301,12 +302,18 @@ def main():
                 L.check(lib.rpc_result_residual_diag_copy(
                     res._handle, C.c_void_p(fout.ctypes.data + 8 * (kk * kk - r0))), ctx.handle)
             else:
-                res = api.accelerated_rpcholesky(ko, cfg, ctx)
+                # the factor streams into this rank's pinned rows (ld = nr, global row
+                # indexing) while the rounds run; then chol_factor; pivots come with the handle
+                xx, lay, ldx = ko._host_layout()
+                h = C.c_void_p()
+                L.check(lib.rpc_accelerated_rpcholesky_into(
+                    ctx.handle, xx.ctypes.data, w.n, w.d, ldx, lay, ko._c_spec(), cfg.to_c(),
+                    C.c_void_p(fout.ctypes.data - r0 * 8), nr, cap, C.byref(h)), ctx.handle)
+                res = api._wrap_result(h, ctx)
                 kk = res.rank
-                # rows owned by this rank, column-major with ld = nr
-                buf = np.ndarray((nr, kk), dtype=np.float64, buffer=fout, order="F")
-                L.check(lib.rpc_result_factor_copy(res._handle, C.c_void_p(buf.ctypes.data - r0 * 8),
-                                                   nr, L.RPC_COL_MAJOR), ctx.handle)
+                L.check(lib.rpc_result_chol_copy(res._handle,
+                                                 C.c_void_p(fout.ctypes.data + 8 * nr * cap)),
+                        ctx.handle)
             barrier()
             dt = time.perf_counter() - t0
             res.free()

@@ -16,6 +16,8 @@
 #ifndef RPCHOL_B200_HPP
 #define RPCHOL_B200_HPP
 
+#include <algorithm>
+#include <functional>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -64,11 +66,11 @@ inline Device& default_device() {
 namespace detail {
 
 using ResultPtr = std::unique_ptr<rpc_result, void (*)(rpc_result*)>;
-using Entry = int (*)(rpc_ctx*, const double*, int64_t, int64_t, int64_t, int, rpc_kernel_spec,
-                      rpc_run_config, rpc_result**);
+using Entry = std::function<int(rpc_ctx*, const double*, int64_t, int64_t, int64_t, int,
+                                rpc_kernel_spec, rpc_run_config, rpc_result**)>;
 
 // Runs `entry` (standard or low-memory) on a KernelOracle; throws like the reference.
-inline ResultPtr run(const PsdOracle& oracle, const RunConfig& cfg, Device& dev, Entry entry,
+inline ResultPtr run(const PsdOracle& oracle, const RunConfig& cfg, Device& dev, const Entry& entry,
                      const char* who) {
   const auto* ko = dynamic_cast<const KernelOracle*>(&oracle);
   if (!ko) throw std::invalid_argument(std::string(who) + " (B200): only KernelOracle inputs are supported");
@@ -140,15 +142,25 @@ inline PivotTrace trace_of(rpc_result* r) {
 /// accelerated_rpcholesky (rpcholesky.hpp:338-401) for kernel oracles, on B200.
 inline CholeskyResult accelerated_rpcholesky(const PsdOracle& oracle, const RunConfig& cfg,
                                              Device& dev = default_device()) {
-  auto r = detail::run(oracle, cfg, dev, rpc_accelerated_rpcholesky, "accelerated_rpcholesky");
-  const Eigen::Index n = rpc_result_n(r.get());
-  const Eigen::Index k = rpc_result_rank(r.get());
+  // the factor streams into res.approx.factor while the rounds run
+  // (rpc_accelerated_rpcholesky_into), sized like the reference's (rpcholesky.hpp:348-351)
+  const Eigen::Index n = oracle.dimension();
+  const Eigen::Index cap = std::min<Eigen::Index>(
+      n, cfg.mode == RunConfig::Mode::FixedRounds ? cfg.rounds * cfg.block_size
+                                                  : cfg.target_rank + cfg.block_size);
   CholeskyResult res;
-  res.approx.factor.resize(n, k);
-  if (k > 0) {
-    if (int st = rpc_result_factor_copy(r.get(), res.approx.factor.data(), n, RPC_COL_MAJOR))
-      throw_status(st, rpc_last_error(dev.get()));
-  }
+  res.approx.factor.resize(n, std::max<Eigen::Index>(cap, 1));
+  double* fbuf = res.approx.factor.data();
+  const Eigen::Index fcols = res.approx.factor.cols();
+  auto r = detail::run(
+      oracle, cfg, dev,
+      [fbuf, n, fcols](rpc_ctx* c, const double* x, int64_t nn, int64_t d, int64_t ldx, int lay,
+                       rpc_kernel_spec ks, rpc_run_config rc, rpc_result** out) {
+        return rpc_accelerated_rpcholesky_into(c, x, nn, d, ldx, lay, ks, rc, fbuf, n, fcols, out);
+      },
+      "accelerated_rpcholesky");
+  const Eigen::Index k = rpc_result_rank(r.get());
+  res.approx.factor.conservativeResize(n, k);
   res.approx.pivots = detail::pivots_of(r.get());
   res.approx.chol_factor = detail::chol_of(r.get());
   res.residual_diag = detail::residual_of(r.get());

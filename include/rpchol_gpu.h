@@ -109,6 +109,18 @@ int rpc_accelerated_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t
                                       int64_t ldx, int layout, rpc_kernel_spec kernel,
                                       rpc_run_config cfg, rpc_result** out);
 
+/* Same, with the factor delivered to host memory while the rounds run: factor_out is
+ * column-major, element (i, j) at factor_out[j * ld_out + i] for the global rows i this
+ * process owns (ld_out >= its row count; pass base - row0 for a rank-local buffer), with
+ * cols_out >= min(N, k + b) (FixedRounds:
+ * min(N, t b)) columns; on return its first rpc_result_rank() columns hold this process's
+ * rows of F.  Each round's finished columns are transposed and copied on a second stream,
+ * overlapping the next rounds (the buffer is page-locked for the call unless it already is). */
+int rpc_accelerated_rpcholesky_into(rpc_ctx* ctx, const double* x, int64_t n, int64_t d,
+                                    int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                    rpc_run_config cfg, double* factor_out, int64_t ld_out,
+                                    int64_t cols_out, rpc_result** out);
+
 /* ---- low-memory variant ------------------------------------------------- */
 /* accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485; LowMemResult 114-119):
  * same pivots, trace and stopping rules as the standard call; keeps O(N + k^2)

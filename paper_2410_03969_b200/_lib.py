@@ -35,7 +35,7 @@ EXPORTS = [
     "rpc_krr_precond_rank", "rpc_krr_precond_pivots", "rpc_krr_predict", "rpc_krr_free",
     "rpc_block_rpcholesky", "rpc_block_rpcholesky_device", "rpc_simple_rpcholesky",
     "rpc_simple_rpcholesky_device", "rpc_result_write_rpcf", "rpc_result_write_trace_csv",
-    "rpc_bench_column_throughput",
+    "rpc_bench_column_throughput", "rpc_accelerated_rpcholesky_into",
 ]
 
 
@@ -110,6 +110,8 @@ def load() -> C.CDLL:
                                                                C.POINTER(vp)]),
         "rpc_result_is_lowmem": (C.c_int, [vp]),
         "rpc_result_write_rpcf": (C.c_int, [vp, C.c_char_p]),
+        "rpc_accelerated_rpcholesky_into": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC,
+                                                      RunConfigC, vp, i64, i64, C.POINTER(vp)]),
         "rpc_bench_column_throughput": (C.c_int, [vp, vp, i64, i64, i64, C.c_int, KernelSpecC, vp,
                                                   C.c_int, C.c_uint64, vp, C.POINTER(C.c_int)]),
         "rpc_result_write_trace_csv": (C.c_int, [vp, C.c_char_p]),

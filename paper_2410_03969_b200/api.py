@@ -279,6 +279,37 @@ def accelerated_rpcholesky(oracle: KernelOracle, cfg: RunConfig,
     return _wrap_result(h, ctx)
 
 
+def factor_capacity(n: int, cfg: RunConfig) -> int:
+    """Columns the factor can reach: min(N, t b) (FixedRounds) or min(N, k + b)."""
+    cap = cfg.rounds * cfg.block_size if cfg.mode == "fixed_rounds" else cfg.target_rank + cfg.block_size
+    return min(n, cap)
+
+
+def accelerated_rpcholesky_into(oracle: KernelOracle, cfg: RunConfig, out: np.ndarray | None = None,
+                                ctx: Context | None = None) -> CholeskyResult:
+    """accelerated_rpcholesky with the factor streamed to host memory while the rounds run
+    (rpc_accelerated_rpcholesky_into).  `out`: Fortran-ordered N x >= factor_capacity; the
+    result's `factor` is a view of its first rank columns."""
+    if not isinstance(oracle, KernelOracle):
+        raise ValueError("accelerated_rpcholesky (B200): only KernelOracle inputs are supported")
+    ctx = ctx or default_context()
+    x, lay, ld = oracle._host_layout()
+    n = x.shape[0]
+    cap = factor_capacity(n, cfg)
+    if out is None:
+        out = np.empty((n, cap), order="F")
+    if not out.flags.f_contiguous or out.shape[0] != n or out.shape[1] < cap:
+        raise ValueError("accelerated_rpcholesky_into: out must be Fortran-ordered N x capacity")
+    h = C.c_void_p()
+    L.check(L.load().rpc_accelerated_rpcholesky_into(ctx.handle, x.ctypes.data, n, x.shape[1], ld,
+                                                     lay, oracle._c_spec(), cfg.to_c(),
+                                                     out.ctypes.data, n, out.shape[1], C.byref(h)),
+            ctx.handle)
+    r = _wrap_result(h, ctx)
+    r._factor = out[:, : r.rank]
+    return r
+
+
 def accelerated_rpcholesky_device(x_dev_ptr: int, n: int, d: int, ld: int, layout: int,
                                   spec: KernelSpec, cfg: RunConfig, ctx: Context,
                                   distance_mode: str | None = None) -> CholeskyResult:

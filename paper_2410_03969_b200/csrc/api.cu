@@ -35,10 +35,12 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 // kernel (lowmem_impl.cuh).  State: X, u, pivot records, L and L^{-1} (k x k).
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
-                       rpc_run_config cfg, rpc_result* res, bool lowmem, int algo) {
+                       rpc_run_config cfg, rpc_result* res, bool lowmem, int algo,
+                       HostSink sink) {
   int kind = 0;
   validate(n, d, kspec, cfg, kind);
   if (algo != kAlgoAccelerated && lowmem) raise(RPC_EINVAL, "low-memory mode is accelerated-only");
+  if (sink.p && lowmem) raise(RPC_EINVAL, "low-memory result has no factor to stream");
   if (lowmem && round_up(d, 16) > 128)
     raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: this build supports d <= 128");
   if (layout != RPC_COL_MAJOR && layout != RPC_ROW_MAJOR) raise(RPC_EINVAL, "unknown layout");
@@ -205,6 +207,21 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   double update_ms = 0.0, flops = 0.0, bytes = 0.0;
   int64_t upd_launches = 0;
 
+  // Factor streaming (HostSink): round r's finished columns F(:, kcur:kcur+m) are final, so
+  // a second stream transposes them to column-major and copies them to the host while the
+  // next rounds compute (double-buffered staging, one half per round in flight).
+  cudaStream_t cst = ctx->copy_stream;
+  int64_t rows_here = 0;
+  for (const Shard& s : res->shards) rows_here += s.n_loc;
+  DBuf sink_tmp[2];
+  std::vector<Ev> sink_ev(sink.p ? 2 : 0);
+  int sink_slot = 0;
+  if (sink.p) {
+    if (sink.cols < cap || sink.ld < rows_here)
+      raise(RPC_EINVAL, "factor buffer too small (needs this process's rows x min(N, k + b))");
+    sink_tmp[0] = DBuf(ctx, sizeof(double) * std::max<int64_t>(rows_here, 1) * b);
+    sink_tmp[1] = DBuf(ctx, sizeof(double) * std::max<int64_t>(rows_here, 1) * b);
+  }
   const double setup_ms = ms_since(h0);
   const auto h1 = clk::now();
   CK(cudaEventRecord(ev_t0.e, st));
@@ -511,6 +528,22 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         bytes += 8.0 * (N * kcur + N * m + N * d + 2.0 * N);
       }
       pending_g2 = true;
+      if (sink.p) {
+        CK(cudaEventRecord(sink_ev[sink_slot].e, st));
+        CK(cudaStreamWaitEvent(cst, sink_ev[sink_slot].e, 0));
+        int64_t off = 0;
+        for (Shard& s : res->shards) {
+          if (s.n_loc == 0) continue;
+          double* tmp = sink_tmp[sink_slot].as<double>() + off;
+          launch_f_to_colmajor(s.F.as<double>(), ldf, s.n_loc, (int)kcur, m, tmp, s.n_loc, cst);
+          CK(cudaMemcpy2DAsync(sink.p + kcur * sink.ld + s.row0, sink.ld * sizeof(double), tmp,
+                               s.n_loc * sizeof(double), s.n_loc * sizeof(double), m,
+                               cudaMemcpyDeviceToHost, cst));
+          off += s.n_loc * m;
+          ++launches;
+        }
+        sink_slot ^= 1;
+      }
       res->pivots.insert(res->pivots.end(), ac.begin(), ac.end());
       kcur += m;
     }
@@ -518,6 +551,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     res->accepted.push_back(std::move(ac));
   }
   CK(cudaEventRecord(ev_t1.e, st));
+  if (sink.p) CK(cudaStreamSynchronize(cst));  // every column is on the host
   const double loop_ms = ms_since(h1);
   const auto h2 = clk::now();
   // ---- finalize ----------------------------------------------------------------
@@ -623,6 +657,7 @@ static int make_ctx(int device, int nvirt, rpc_ctx** out) {
     ctx->nvirt = nvirt;
     CK(cudaSetDevice(device));
     CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
   });
   if (rc) {
     g_last_error = ctx->err;
@@ -679,6 +714,7 @@ void rpc_destroy(rpc_ctx* ctx) {
   if (ctx->io_pinned) cudaFreeHost(ctx->io_pinned);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
   delete ctx;
 }
 
@@ -842,6 +878,52 @@ int rpc_simple_rpcholesky_device(rpc_ctx* ctx, const double* x_dev, int64_t n, i
   if (k < 1 || k > n) return fail(ctx, RPC_EINVAL, "simple_rpcholesky: need 1 <= k <= N");
   return run_algo(ctx, x_dev, true, n, d, ldx, layout, kernel, simple_cfg(k, seed, flags),
                   kAlgoSimple, out);
+}
+
+int rpc_accelerated_rpcholesky_into(rpc_ctx* ctx, const double* x, int64_t n, int64_t d,
+                                    int64_t ldx, int layout, rpc_kernel_spec kernel,
+                                    rpc_run_config cfg, double* factor_out, int64_t ld_out,
+                                    int64_t cols_out, rpc_result** out) {
+  if (!ctx || !out || !factor_out) return fail(ctx, RPC_EINVAL, "null argument");
+  std::lock_guard<std::mutex> lk(ctx->mu);
+  *out = nullptr;
+  rpc_result* r = new_result();
+  double* reg_ptr = nullptr;
+  int rc = guarded(ctx, [&] {
+    if (!x && n > 0) raise(RPC_EINVAL, "null point matrix");
+    if (ldx < (layout == RPC_ROW_MAJOR ? d : n)) raise(RPC_EINVAL, "leading dimension too small");
+    CK(cudaSetDevice(ctx->device));
+    // page-lock the caller's buffer for the duration (asynchronous D2H), unless it is already
+    // rows [r0, r1) of every column belong to this process (global row indexing)
+    const Layout Lz = make_layout(std::max<int64_t>(n, 1), ctx->nshards());
+    const int64_t r0 = Lz.row0(ctx->first_shard());
+    const int64_t r1 = std::min<int64_t>(n, Lz.row0(ctx->first_shard()) +
+                                                (int64_t)ctx->nvirt * Lz.cpr * kChunk);
+    if (cols_out < 1 || ld_out < r1 - r0) raise(RPC_EINVAL, "factor buffer too small");
+    double* lo = factor_out + r0;
+    const size_t span = sizeof(double) * (size_t)((cols_out - 1) * ld_out + (r1 - r0));
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, lo) == cudaSuccess &&
+                        pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    if (!pinned && span > 0) {
+      CK(cudaHostRegister(lo, span, cudaHostRegisterPortable));
+      reg_ptr = lo;
+    }
+    HostSink sink;
+    sink.p = factor_out;
+    sink.ld = ld_out;
+    sink.cols = cols_out;
+    run_factorization(ctx, x, false, n, d, ldx, layout, kernel, cfg, r, false, kAlgoAccelerated,
+                      sink);
+  });
+  if (reg_ptr) cudaHostUnregister(reg_ptr);
+  if (rc) {
+    delete r;
+    return rc;
+  }
+  *out = r;
+  return RPC_OK;
 }
 
 int rpc_result_is_lowmem(const rpc_result* r) { return r ? (int)r->lowmem : 0; }

@@ -73,6 +73,7 @@ using namespace rpcb_rt;
 struct rpc_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy_stream = nullptr;  // factor streaming to the host (overlaps the rounds)
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   int nvirt = 1;
@@ -278,9 +279,15 @@ struct Ev {
 // The factorization proper (api.cu).  `src` points to this process's shard rows
 // (device memory when src_on_device, else host memory of the full X).
 enum { kAlgoAccelerated = 0, kAlgoBlock = 1, kAlgoSimple = 2 };
+// Host destination for the factor, filled while the rounds run: column-major, leading
+// dimension ld >= N, at least `cols` columns (this process's rows only).
+struct HostSink {
+  double* p = nullptr;
+  int64_t ld = 0, cols = 0;
+};
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
                        rpc_run_config cfg, rpc_result* res, bool lowmem = false,
-                       int algo = kAlgoAccelerated);
+                       int algo = kAlgoAccelerated, HostSink sink = HostSink());
 
 }  // namespace rpcb_rt

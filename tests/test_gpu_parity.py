@@ -284,3 +284,31 @@ def test_virtual_shards_p_invariance(p):  # p = 7: shards 5 and 6 own no rows
     assert g1.relative_trace_error == gp.relative_trace_error
     assert g1.captured_sq == gp.captured_sq
     assert np.array_equal(g1.chol_factor, gp.chol_factor)
+
+
+# ------------------------------------------------------ streamed factor output
+def test_factor_streamed_into_host_buffer(ctx):
+    """rpc_accelerated_rpcholesky_into: the factor arrives in host memory during the rounds
+    and is bitwise the device factor (rpc_result_factor_copy)."""
+    w = wl.CONFIGS["C1"]
+    ko = api.KernelOracle(w.points(), api.KernelSpec(w.kernel, w.sigma))
+    cfg = api.RunConfig.until_rank(w.k, w.b, w.seed)
+    g = api.accelerated_rpcholesky_into(ko, cfg, None, ctx)          # pageable: registered
+    ref = api.accelerated_rpcholesky(ko, cfg, ctx)
+    assert np.array_equal(g.pivots, ref.pivots)
+    assert np.array_equal(g.factor, ref.factor_into(np.zeros((w.n, ref.rank), order="F")))
+    buf = np.zeros((w.n, api.factor_capacity(w.n, cfg) + 5), order="F")
+    g2 = api.accelerated_rpcholesky_into(ko, cfg, buf, ctx)
+    assert np.array_equal(g2.factor, g.factor)
+    with pytest.raises(ValueError):
+        api.accelerated_rpcholesky_into(ko, cfg, np.zeros((w.n, 3), order="F"), ctx)
+
+
+@pytest.mark.parametrize("p", [3])
+def test_factor_streamed_virtual_shards(p):
+    x = wl.gen_c1(20000, 10, 0)
+    ko = api.KernelOracle(x, api.KernelSpec("gaussian", math.sqrt(10.0)))
+    cfg = api.RunConfig.until_rank(200, 40, 0)
+    a = api.accelerated_rpcholesky_into(ko, cfg, None, api.Context(0))
+    b = api.accelerated_rpcholesky_into(ko, cfg, None, api.Context(0, virtual_shards=p))
+    assert np.array_equal(a.factor, b.factor)
