@@ -26,6 +26,26 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
   for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[j * k + i] = F[lr * ldf + j];
 }
 
+// Round status -> mapped pinned host memory: ScanStatus | SweepOut | proposal ids (double,
+// from the records) [b] | accepted ids [b].
+__global__ void publish_status_kernel(const ScanStatus* __restrict__ scan,
+                                      const SweepOut* __restrict__ sw, const double* __restrict__ prop,
+                                      int64_t rec, int b, const int64_t* __restrict__ acc,
+                                      char* host) {
+  ScanStatus* hs = reinterpret_cast<ScanStatus*>(host);
+  SweepOut* hw = reinterpret_cast<SweepOut*>(hs + 1);
+  double* hp = reinterpret_cast<double*>(hw + 1);
+  int64_t* ha = reinterpret_cast<int64_t*>(hp + b);
+  if (threadIdx.x == 0) {
+    *hs = *scan;
+    *hw = *sw;
+  }
+  for (int j = threadIdx.x; j < b; j += blockDim.x) {
+    hp[j] = prop[(int64_t)j * rec];
+    ha[j] = acc[j];
+  }
+}
+
 // The factorization proper.  `src` points to this process's shard rows (device
 // memory when src_on_device, else host memory of the full X).
 //
@@ -109,8 +129,12 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     } else {
       if (layout == RPC_ROW_MAJOR) {
         tmp = DBuf(ctx, sizeof(double) * s.n_loc * d);
-        CK(cudaMemcpy2DAsync(tmp.p, d * sizeof(double), src + s.row0 * ldx, ldx * sizeof(double),
-                             d * sizeof(double), s.n_loc, cudaMemcpyHostToDevice, st));
+        if (ldx == d)  // contiguous rows: one linear copy (a pitched copy of 8d-byte rows is slow)
+          CK(cudaMemcpyAsync(tmp.p, src + s.row0 * ldx, sizeof(double) * s.n_loc * d,
+                             cudaMemcpyHostToDevice, st));
+        else
+          CK(cudaMemcpy2DAsync(tmp.p, d * sizeof(double), src + s.row0 * ldx, ldx * sizeof(double),
+                               d * sizeof(double), s.n_loc, cudaMemcpyHostToDevice, st));
         ld_src = d;
       } else {
         tmp = DBuf(ctx, sizeof(double) * s.n_loc * d);
@@ -193,6 +217,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   SweepOut* h_sweep = reinterpret_cast<SweepOut*>(h_scan + 1);
   double* h_prop_ids = reinterpret_cast<double*>(h_sweep + 1);
   int64_t* h_acc_ids = reinterpret_cast<int64_t*>(h_prop_ids + b);
+  char* hbuf_dev = nullptr;  // device alias of the pinned status buffer (UVA mapping)
+  if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&hbuf_dev), hbuf, 0) != cudaSuccess) {
+    cudaGetLastError();
+    hbuf_dev = nullptr;
+  }
 
   const double trace_a = (double)n;  // sum of diag(A) = N exactly
   int64_t kcur = 0;
@@ -377,11 +406,19 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                     &d_sweep->m, b, (int)kcur, fs.as<double>(), ldf, st);
       launches += 2;
     }
-    CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
-                       cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),
-                         sizeof(double), b, cudaMemcpyDeviceToHost, st));
-    CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
+    if (hbuf_dev) {
+      // status words straight into mapped host memory: no copy-engine transfer, so the
+      // read never queues behind a factor block streaming out on the copy stream
+      publish_status_kernel<<<1, 256, 0, st>>>(d_scan, d_sweep, prop.as<double>(), lay.rec, b,
+                                               acc_ids.as<int64_t>(), hbuf_dev);
+      ++launches;
+    } else {
+      CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpy2DAsync(h_prop_ids, sizeof(double), prop.p, lay.rec * sizeof(double),
+                           sizeof(double), b, cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
     }  // accelerated
     CK(cudaGetLastError());
@@ -529,6 +566,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       }
       pending_g2 = true;
       if (sink.p) {
+        const auto hs0 = clk::now();
         CK(cudaEventRecord(sink_ev[sink_slot].e, st));
         CK(cudaStreamWaitEvent(cst, sink_ev[sink_slot].e, 0));
         int64_t off = 0;
@@ -542,6 +580,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           off += s.n_loc * m;
           ++launches;
         }
+        if (std::getenv("RPC_DEBUG_TIMING"))
+          std::fprintf(stderr, "[rpc] sink round %lld: host enqueue %.3f ms\n", (long long)round,
+                       ms_since(hs0));
         sink_slot ^= 1;
       }
       res->pivots.insert(res->pivots.end(), ac.begin(), ac.end());
@@ -1080,10 +1121,7 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
     const int64_t dpad = round_up(d, 16);
     DBuf X(ctx, sizeof(double) * n * dpad), sqn(ctx, sizeof(double) * n),
         raw(ctx, sizeof(double) * n * d);
-    if (layout == RPC_ROW_MAJOR)
-      CK(cudaMemcpy2DAsync(raw.p, d * 8, x, ldx * 8, d * 8, n, cudaMemcpyHostToDevice, st));
-    else
-      CK(cudaMemcpy2DAsync(raw.p, n * 8, x, ldx * 8, n * 8, d, cudaMemcpyHostToDevice, st));
+    h2d_points(raw.p, x, n, d, ldx, layout, st);
     launch_pack_points(raw.as<double>(), n, (int)d, layout == RPC_ROW_MAJOR ? d : n,
                        layout == RPC_ROW_MAJOR, dpad, X.as<double>(), sqn.as<double>(), nullptr, st);
     RecordLayout lay{2 + dpad, 2, 2 + dpad};
@@ -1189,10 +1227,7 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
     const int64_t dpad = round_up(d, 16);
     DBuf X(ctx, sizeof(double) * n * dpad), sqn(ctx, sizeof(double) * n),
         raw(ctx, sizeof(double) * n * d);
-    if (layout == RPC_ROW_MAJOR)
-      CK(cudaMemcpy2DAsync(raw.p, d * 8, x, ldx * 8, d * 8, n, cudaMemcpyHostToDevice, st));
-    else
-      CK(cudaMemcpy2DAsync(raw.p, n * 8, x, ldx * 8, n * 8, d, cudaMemcpyHostToDevice, st));
+    h2d_points(raw.p, x, n, d, ldx, layout, st);
     launch_pack_points(raw.as<double>(), n, (int)d, layout == RPC_ROW_MAJOR ? d : n,
                        layout == RPC_ROW_MAJOR, dpad, X.as<double>(), sqn.as<double>(), nullptr,
                        st);

@@ -234,10 +234,7 @@ void upload_points(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t 
   sqn = DBuf(ctx, sizeof(double) * n);
   DBuf raw(ctx, sizeof(double) * n * d), bad(ctx, sizeof(int));
   CK(cudaMemsetAsync(bad.p, 0, sizeof(int), st));
-  if (layout == RPC_ROW_MAJOR)
-    CK(cudaMemcpy2DAsync(raw.p, d * 8, x, ldx * 8, d * 8, n, cudaMemcpyHostToDevice, st));
-  else
-    CK(cudaMemcpy2DAsync(raw.p, n * 8, x, ldx * 8, n * 8, d, cudaMemcpyHostToDevice, st));
+  h2d_points(raw.p, x, n, d, ldx, layout, st);
   launch_pack_points(raw.as<double>(), n, (int)d, layout == RPC_ROW_MAJOR ? d : n,
                      layout == RPC_ROW_MAJOR, dpad, X.as<double>(), sqn.as<double>(),
                      bad.as<int>(), st);

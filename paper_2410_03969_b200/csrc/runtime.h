@@ -276,6 +276,18 @@ struct Ev {
   }
 };
 
+// Host points (n x d, either layout, leading dimension ldx) -> dense device copy (row-major
+// [n][d] or column-major [d][n] as given).  Contiguous inputs go as one linear copy: a pitched
+// copy of 8d-byte rows runs at a few GB/s.
+inline void h2d_points(void* dst, const double* x, int64_t n, int64_t d, int64_t ldx, int layout,
+                       cudaStream_t st) {
+  const int64_t inner = layout == RPC_ROW_MAJOR ? d : n, outer = layout == RPC_ROW_MAJOR ? n : d;
+  if (ldx == inner)
+    CK(cudaMemcpyAsync(dst, x, sizeof(double) * inner * outer, cudaMemcpyHostToDevice, st));
+  else
+    CK(cudaMemcpy2DAsync(dst, inner * 8, x, ldx * 8, inner * 8, outer, cudaMemcpyHostToDevice, st));
+}
+
 // The factorization proper (api.cu).  `src` points to this process's shard rows
 // (device memory when src_on_device, else host memory of the full X).
 enum { kAlgoAccelerated = 0, kAlgoBlock = 1, kAlgoSimple = 2 };
