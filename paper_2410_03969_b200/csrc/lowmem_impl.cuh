@@ -332,7 +332,15 @@ int launch_lowmem_t(const LowmemParams& p, cudaStream_t st) {
             make_map(&mW, p.W, p.knew, p.m, p.ldw, C::NB);
   if (!ok) return -3;
   const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
-  const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)num_sms());
+  // persistent grid: as many CTAs per SM as registers and shared memory allow (small m, as in
+  // the KRR product mode, fits two, which hides the latency of the short per-chunk chains)
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowmem_kernel<WC, NFW, GRAM, G>, C::NT,
+                                                    C::smem_bytes(S, nD)) != cudaSuccess || occ < 1) {
+    cudaGetLastError();
+    occ = 1;
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
   if (grid)
     lowmem_kernel<WC, NFW, GRAM, G><<<grid, C::NT, C::smem_bytes(S, nD), st>>>(p, S, mX, mXS, mW);
   return C::BM;
