@@ -534,7 +534,17 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
   if (!ok) return -3;
   // persistent: one CTA per SM, tiles strided by the grid (p.tile_g2 is per tile)
   const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
-  const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)MINB * num_sms());
+  // persistent grid sized by occupancy: small m (early rounds, kernel-column bench) fits two
+  // CTAs per SM, which hides the latency of the short per-tile chains
+  static int occ = 0;
+  if (!occ) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<WC, NFW, GRAM, MINB, G>,
+                                                      C::NT, C::SMEM) != cudaSuccess || occ < 1) {
+      cudaGetLastError();
+      occ = MINB;
+    }
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
   if (grid)
     update_kernel<WC, NFW, GRAM, MINB, G><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
   return C::BM;
