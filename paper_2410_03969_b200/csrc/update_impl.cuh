@@ -323,9 +323,9 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       mark(6);
     }
     // ---- acc (Gram dot / distance) -> -A(R, S) ------------------------------------
-    // Rolled over the warp's column fragments: each pass transforms fragment 0 and
-    // rotates the accumulator array by one fragment, so the code stays small
-    // (one fragment's epilogue) while acc never leaves registers.
+    // Rolled over the warp's column fragments: each pass transforms fragments 0 and 1 and
+    // rotates the accumulator array by two fragments, so the code stays small while acc
+    // never leaves registers.
     {
       // exponent = D * (-0.5 / sigma^2) (Gaussian) or D * (-1 / sigma) (l1): one multiply
       // instead of the reference's division, <= 1 ulp apart (kernel values agree to 1e-15).
@@ -340,22 +340,51 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
         gid[fr] = (double)(p.row0 + grow);
       }
       mark(7);
+      // two fragments per pass (8 independent exp chains in flight), rotating by two
+      auto xform = [&](double& a, int col, int fr, double sqc, double idc) {
+        double dd = a;
+        if (GRAM) {
+          dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr[fr]), sqc);
+          dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
+        }
+        const double val = exp_tab(dd * escale, s_exp2);
+        a = (col < m && rin[fr]) ? -val : 0.0;
+      };
 #pragma unroll 1
-      for (int it = 0; it < NFW; ++it) {
+      for (int it = 0; it + 1 < NFW; it += 2) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int col = 8 * (wc * NFW + it + h) + 2 * t + v;
+            const double sqc = s_sqnS[col], idc = s_idS[col];
+#pragma unroll
+            for (int fr = 0; fr < 2; ++fr) xform(acc[fr][h][v], col, fr, sqc, idc);
+          }
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr) {
+          const double t0 = acc[fr][0][0], t1 = acc[fr][0][1];
+          const double t2 = acc[fr][NFW > 1 ? 1 : 0][0], t3 = acc[fr][NFW > 1 ? 1 : 0][1];
+#pragma unroll
+          for (int q = 0; q + 2 < NFW; ++q) {
+            acc[fr][q][0] = acc[fr][q + 2][0];
+            acc[fr][q][1] = acc[fr][q + 2][1];
+          }
+          if (NFW > 1) {
+            acc[fr][NFW - 2][0] = t0;
+            acc[fr][NFW - 2][1] = t1;
+            acc[fr][NFW - 1][0] = t2;
+            acc[fr][NFW - 1][1] = t3;
+          }
+        }
+      }
+      if (NFW & 1) {  // last fragment (now at position 0), then rotate by one
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int col = 8 * (wc * NFW + it) + 2 * t + v;
+          const int col = 8 * (wc * NFW + NFW - 1) + 2 * t + v;
           const double sqc = s_sqnS[col], idc = s_idS[col];
 #pragma unroll
-          for (int fr = 0; fr < 2; ++fr) {
-            double dd = acc[fr][0][v];
-            if (GRAM) {
-              dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr[fr]), sqc);
-              dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
-            }
-            const double val = exp_tab(dd * escale, s_exp2);
-            acc[fr][0][v] = (col < m && rin[fr]) ? -val : 0.0;
-          }
+          for (int fr = 0; fr < 2; ++fr) xform(acc[fr][0][v], col, fr, sqc, idc);
         }
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) {
