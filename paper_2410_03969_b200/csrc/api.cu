@@ -217,6 +217,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   SweepOut* h_sweep = reinterpret_cast<SweepOut*>(h_scan + 1);
   double* h_prop_ids = reinterpret_cast<double*>(h_sweep + 1);
   int64_t* h_acc_ids = reinterpret_cast<int64_t*>(h_prop_ids + b);
+  Ev ev_pub;                  // status published (mapped-memory path)
   char* hbuf_dev = nullptr;  // device alias of the pinned status buffer (UVA mapping)
   if (cudaHostGetDevicePointer(reinterpret_cast<void**>(&hbuf_dev), hbuf, 0) != cudaSuccess) {
     cudaGetLastError();
@@ -392,6 +393,16 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                  hp.as<double>(), st);
     dbg(st, "sweep");
     launches += 3;
+    if (hbuf_dev) {
+      // status words straight into mapped host memory: no copy-engine transfer, so the read
+      // never queues behind a factor block streaming out on the copy stream.  Published
+      // before L^{-1} / B' so the host's bookkeeping overlaps them and the update kernel is
+      // already queued when they finish.
+      publish_status_kernel<<<1, 256, 0, st>>>(d_scan, d_sweep, prop.as<double>(), lay.rec, b,
+                                               acc_ids.as<int64_t>(), hbuf_dev);
+      CK(cudaEventRecord(ev_pub.e, st));
+      ++launches;
+    }
     // L^{-1} and the accepted-pivot operands only need the sweep's device-side outputs:
     // queue them before the status read so they run while the host waits.
     CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
@@ -407,11 +418,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       launches += 2;
     }
     if (hbuf_dev) {
-      // status words straight into mapped host memory: no copy-engine transfer, so the
-      // read never queues behind a factor block streaming out on the copy stream
-      publish_status_kernel<<<1, 256, 0, st>>>(d_scan, d_sweep, prop.as<double>(), lay.rec, b,
-                                               acc_ids.as<int64_t>(), hbuf_dev);
-      ++launches;
+      // (published right after the sweep, above)
     } else {
       CK(cudaMemcpyAsync(hbuf, status.p, sizeof(ScanStatus) + sizeof(SweepOut),
                          cudaMemcpyDeviceToHost, st));
@@ -419,7 +426,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                            sizeof(double), b, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
     }
-    CK(cudaStreamSynchronize(st));
+    if (hbuf_dev) CK(cudaEventSynchronize(ev_pub.e));
+    else CK(cudaStreamSynchronize(st));
     }  // accelerated
     CK(cudaGetLastError());
     if (pending_g2) {
