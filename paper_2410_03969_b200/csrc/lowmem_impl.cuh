@@ -46,8 +46,8 @@ struct LCfg {
   }
 };
 
-template <int WC, int NFW, bool GRAM, int G>
-__global__ void __launch_bounds__(256, 1)
+template <int WC, int NFW, bool GRAM, int G, int MINB>
+__global__ void __launch_bounds__(256, MINB)
     lowmem_kernel(LowmemParams p, int S, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmW) {
   using C = LCfg<WC, NFW, G>;
@@ -115,9 +115,12 @@ __global__ void __launch_bounds__(256, 1)
   int arow[2];
 #pragma unroll
   for (int fr = 0; fr < 2; ++fr) arow[fr] = wr * 16 + 8 * fr + pg;
-  uint32_t foff[4];
+  uint32_t foff[4], foffw[4];
 #pragma unroll
-  for (int s = 0; s < 4; ++s) foff[s] = swz_off(pg, 4 * s + t);
+  for (int s = 0; s < 4; ++s) {
+    foff[s] = swz_off(pg, 4 * s + t);
+    foffw[s] = swz_off(pg, 8 * (s >> 1) + perm8(2 * t + (s & 1)));  // register-A k order
+  }
   const uint32_t a_base = (uint32_t)(wr * 16) * 128u;
   const uint32_t b_base = (uint32_t)(wc * NFW) * 1024u;
   const double escale = p.escale;
@@ -157,6 +160,107 @@ __global__ void __launch_bounds__(256, 1)
       unsigned char* As = stages + s * STAGE;
       const unsigned char* Bs = As + C::A_BYTES;
       const unsigned char* XSs = Bs + C::B_BYTES;
+      const int z = 16 * c - kold;  // W rows n have zeros beyond column kold + n
+      const int q_lo = z > 0 ? max(0, z / 8 - wc * NFW) : 0;
+      const unsigned char* Bw = Bs + b_base;
+      if constexpr (WC == 1) {
+        // ---- one warp column: the warp's 16 x 16 kernel tile stays in registers ------
+        // Lane (g, t) generates rows arow[fr] x chunk columns kc(j, v) = 8j + perm8(2t + v),
+        // exactly the C-fragment positions of a Gram DMMA against the TMA-staged pivot rows;
+        // read as A operand with k-step s = 2j + v (the k order inside the chunk is free,
+        // the W operand is fetched with the same permutation, foffw).
+        double gv[2][2][2];
+        if constexpr (GRAM) {
+#pragma unroll
+          for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) gv[fr][j][0] = gv[fr][j][1] = 0.0;
+#pragma unroll 1
+          for (int dc = 0; dc < nD; ++dc) {
+            const unsigned char* Xw = xt + dc * C::A_BYTES + a_base;
+            const unsigned char* Sw = XSs + dc * 2048;
+#pragma unroll
+            for (int s4 = 0; s4 < 4; ++s4) {
+              double a[2];
+#pragma unroll
+              for (int fr = 0; fr < 2; ++fr) a[fr] = *reinterpret_cast<const double*>(Xw + fr * 1024 + foff[s4]);
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const double bv = *reinterpret_cast<const double*>(Sw + j * 1024 + foff[s4]);
+#pragma unroll
+                for (int fr = 0; fr < 2; ++fr) dmma884(gv[fr][j][0], gv[fr][j][1], a[fr], bv);
+              }
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int col = 16 * c + 8 * j + perm8(2 * t + v);
+              const bool cin = col < knew;
+              const double sqc = cin ? p.piv[(int64_t)col * p.prec + 1] : 0.0;
+              const double idc = cin ? p.piv[(int64_t)col * p.prec] : -1.0;
+#pragma unroll
+              for (int fr = 0; fr < 2; ++fr) {
+                double dd = __dadd_rn(__dadd_rn(-2.0 * gv[fr][j][v], sqr[fr]), sqc);
+                dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
+                gv[fr][j][v] = exp_tab(dd * escale, s_exp2);
+              }
+            }
+        } else {
+          // direct / l1 distances in the same fragment positions, ascending coordinates
+          double dsum[2][2][2];
+#pragma unroll
+          for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+            for (int j = 0; j < 2; ++j) dsum[fr][j][0] = dsum[fr][j][1] = 0.0;
+#pragma unroll 1
+          for (int dc = 0; dc < nD; ++dc) {
+            const unsigned char* Xw = xt + dc * C::A_BYTES;
+            const unsigned char* Sw = XSs + dc * 2048;
+            const int jn = min(16, p.d - 16 * dc);
+#pragma unroll 2
+            for (int jj = 0; jj < jn; ++jj) {
+              double xr[2], xs[2][2];
+#pragma unroll
+              for (int fr = 0; fr < 2; ++fr) xr[fr] = *reinterpret_cast<const double*>(Xw + swz_off(arow[fr], jj));
+#pragma unroll
+              for (int j = 0; j < 2; ++j)
+#pragma unroll
+                for (int v = 0; v < 2; ++v)
+                  xs[j][v] = *reinterpret_cast<const double*>(Sw + swz_off(8 * j + perm8(2 * t + v), jj));
+#pragma unroll
+              for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+#pragma unroll
+                  for (int v = 0; v < 2; ++v) {
+                    const double df = __dsub_rn(xr[fr], xs[j][v]);
+                    dsum[fr][j][v] = l1 ? __dadd_rn(dsum[fr][j][v], fabs(df))
+                                        : __dadd_rn(dsum[fr][j][v], __dmul_rn(df, df));
+                  }
+            }
+          }
+#pragma unroll
+          for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+            for (int j = 0; j < 2; ++j)
+#pragma unroll
+              for (int v = 0; v < 2; ++v) gv[fr][j][v] = exp_tab(dsum[fr][j][v] * escale, s_exp2);
+        }
+        // ---- acc += A(R, S_c) W(:, S_c)^T from registers --------------------------------
+#pragma unroll
+        for (int s4 = 0; s4 < 4; ++s4) {
+#pragma unroll
+          for (int q = 0; q < NFW; ++q) {
+            if (q < q_lo) continue;
+            const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foffw[s4]);
+#pragma unroll
+            for (int fr = 0; fr < 2; ++fr)
+              dmma884(acc[fr][q][0], acc[fr][q][1], gv[fr][s4 >> 1][s4 & 1], bv);
+          }
+        }
+      } else {
       // ---- regenerate the kernel tile A(R, S_c) (64 x 16) into As -----------------
       if constexpr (GRAM) {
         double ga[2][NG][2];
@@ -229,14 +333,10 @@ __global__ void __launch_bounds__(256, 1)
         for (int e = 0; e < EPT; ++e)
           *reinterpret_cast<double*>(As + swz_off(r, c0 + e)) = exp_tab(da[e] * escale, s_exp2);
       }
-      if (WC == 1) __syncwarp();  // each warp consumes only the rows it generated
-      else gsync();
+      gsync();
       // ---- acc += A(R, S_c) W(:, S_c)^T; W rows n have zeros beyond column kold + n ----
       {
-        const int z = 16 * c - kold;
-        const int q_lo = z > 0 ? max(0, z / 8 - wc * NFW) : 0;
         const unsigned char* Aw = As + a_base;
-        const unsigned char* Bw = Bs + b_base;
 #pragma unroll
         for (int s4 = 0; s4 < 4; ++s4) {
           double a[2];
@@ -251,6 +351,7 @@ __global__ void __launch_bounds__(256, 1)
           }
         }
       }
+      }  // WC == 2
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       ++cons;
@@ -311,7 +412,7 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
-template <int WC, int NFW, bool GRAM, int G>
+template <int WC, int NFW, bool GRAM, int G, int MINB = 1>
 int launch_lowmem_t(const LowmemParams& p, cudaStream_t st) {
   using C = LCfg<WC, NFW, G>;
   constexpr int kMaxSmem = 227 * 1024;
@@ -321,7 +422,7 @@ int launch_lowmem_t(const LowmemParams& p, cudaStream_t st) {
   if (S < 2) return -1;  // dimension too large for a resident tile
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(lowmem_kernel<WC, NFW, GRAM, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(lowmem_kernel<WC, NFW, GRAM, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kMaxSmem) != cudaSuccess)
       return -2;
     attr = true;
@@ -335,14 +436,14 @@ int launch_lowmem_t(const LowmemParams& p, cudaStream_t st) {
   // persistent grid: as many CTAs per SM as registers and shared memory allow (small m, as in
   // the KRR product mode, fits two, which hides the latency of the short per-chunk chains)
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowmem_kernel<WC, NFW, GRAM, G>, C::NT,
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowmem_kernel<WC, NFW, GRAM, G, MINB>, C::NT,
                                                     C::smem_bytes(S, nD)) != cudaSuccess || occ < 1) {
     cudaGetLastError();
     occ = 1;
   }
   const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
   if (grid)
-    lowmem_kernel<WC, NFW, GRAM, G><<<grid, C::NT, C::smem_bytes(S, nD), st>>>(p, S, mX, mXS, mW);
+    lowmem_kernel<WC, NFW, GRAM, G, MINB><<<grid, C::NT, C::smem_bytes(S, nD), st>>>(p, S, mX, mXS, mW);
   return C::BM;
 }
 
