@@ -171,6 +171,18 @@ __global__ void __launch_bounds__(256, MINB)
         // the W operand is fetched with the same permutation, foffw).
         double gv[2][2][2];
         if constexpr (GRAM) {
+          // pivot norms / ids of this lane's four columns: issued before the Gram products so
+          // their L2 latency hides behind the DMMA chain
+          double sqc4[2][2], idc4[2][2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+#pragma unroll
+            for (int v = 0; v < 2; ++v) {
+              const int col = 16 * c + 8 * j + perm8(2 * t + v);
+              const bool cin = col < knew;
+              sqc4[j][v] = cin ? __ldg(p.piv + (int64_t)col * p.prec + 1) : 0.0;
+              idc4[j][v] = cin ? __ldg(p.piv + (int64_t)col * p.prec) : -1.0;
+            }
 #pragma unroll
           for (int fr = 0; fr < 2; ++fr)
 #pragma unroll
@@ -196,10 +208,7 @@ __global__ void __launch_bounds__(256, MINB)
           for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-              const int col = 16 * c + 8 * j + perm8(2 * t + v);
-              const bool cin = col < knew;
-              const double sqc = cin ? p.piv[(int64_t)col * p.prec + 1] : 0.0;
-              const double idc = cin ? p.piv[(int64_t)col * p.prec] : -1.0;
+              const double sqc = sqc4[j][v], idc = idc4[j][v];
 #pragma unroll
               for (int fr = 0; fr < 2; ++fr) {
                 double dd = __dadd_rn(__dadd_rn(-2.0 * gv[fr][j][v], sqr[fr]), sqc);
