@@ -86,8 +86,10 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   double* hp = hp_global ? hp_global : lpan + kSweepBlock * b;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr int nwarps = kSweepThreads / 32;
-  for (int p = warp; p < b; p += nwarps)
-    for (int q = lane; q <= p; q += 32) hp[tri(p) + q] = H[(int64_t)p * b + q];
+  for (int p = warp; p < b; p += nwarps) {
+#pragma unroll 4
+    for (int q = lane; q <= p; q += 32) hp[tri(p) + q] = __ldg(H + (int64_t)p * b + q);
+  }
   for (int i = tid; i < b; i += kSweepThreads) {
     // accept_all (block / simple RPCholesky): r = 0, so a row is kept iff h_ii > 0 — the
     // LLT success condition (Eigen fails on the first pivot <= 0)
@@ -213,7 +215,13 @@ __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __r
   if ((int)blockIdx.x * kLinvWarps >= m) return;  // whole CTA beyond m (device-side m)
   const double* sL = lacc_cm;
   if (in_smem) {
-    for (int i = tid; i < m * m; i += blockDim.x) smem_l[i] = lacc_cm[i];
+    // independent 16-byte loads, eight in flight per thread (the copy is latency bound)
+    const int n2 = (m * m) >> 1;
+    const double2* src2 = reinterpret_cast<const double2*>(lacc_cm);
+    double2* dst2 = reinterpret_cast<double2*>(smem_l);
+#pragma unroll 8
+    for (int i = tid; i < n2; i += blockDim.x) dst2[i] = __ldg(src2 + i);
+    if (tid == 0 && ((m * m) & 1)) smem_l[m * m - 1] = lacc_cm[m * m - 1];
     __syncthreads();
     sL = smem_l;
   }
