@@ -312,3 +312,24 @@ def test_factor_streamed_virtual_shards(p):
     a = api.accelerated_rpcholesky_into(ko, cfg, None, api.Context(0))
     b = api.accelerated_rpcholesky_into(ko, cfg, None, api.Context(0, virtual_shards=p))
     assert np.array_equal(a.factor, b.factor)
+
+
+def test_bench_column_throughput_rows(ctx):
+    """bench_column_throughput (experiment.hpp:344-387): one row per (block size, mode),
+    ~1000 columns each, Direct + GramTrick for the Gaussian, Direct only for l1."""
+    x = wl.gen_c2(30000, 12, 1)
+    rows = api.bench_column_throughput(api.KernelOracle(x, api.KernelSpec("gaussian", 3.0)),
+                                       [1, 7, 120, 300], 0, ctx)
+    assert [(r["block_size"], r["mode"]) for r in rows] == [
+        (1, "direct"), (1, "gram"), (7, "direct"), (7, "gram"), (120, "direct"), (120, "gram"),
+        (300, "direct"), (300, "gram")]
+    for r in rows:
+        b = r["block_size"]
+        assert r["columns"] == -(-1000 // b) * b
+        assert r["wall_ms"] > 0 and r["columns_per_sec"] > 0
+        assert abs(r["output_gbs"] - 8 * 30000 * r["columns"] / (r["wall_ms"] * 1e-3) / 1e9) < 1e-6 * r["output_gbs"]
+    l1 = api.bench_column_throughput(api.KernelOracle(x, api.KernelSpec("l1laplace", 3.0)), [40],
+                                     0, ctx)
+    assert [r["mode"] for r in l1] == ["direct"]
+    with pytest.raises(ValueError, match="block size"):
+        api.bench_column_throughput(api.KernelOracle(x, api.KernelSpec("l1laplace", 3.0)), [0], 0, ctx)
