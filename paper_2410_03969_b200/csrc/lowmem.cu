@@ -20,8 +20,12 @@ int launch_lowmem_wc2(const LowmemParams& p, int nfw, cudaStream_t st);
 
 int launch_lowmem(const LowmemParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
-  if (nf <= 16) return launch_lowmem_wc1(p, nf, st);
-  if (nf <= 32) return launch_lowmem_wc2(p, std::max(9, (nf + 1) / 2), st);
+  if (nf <= 16) {
+    const int r = launch_lowmem_wc1(p, nf, st);
+    if (r != -1) return r;
+    // -1: two groups' resident X tiles exceed shared memory (large d): one group of 8 warps
+  }
+  if (nf <= 32) return launch_lowmem_wc2(p, (nf + 1) / 2, st);
   return -1;
 }
 

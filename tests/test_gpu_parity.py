@@ -333,3 +333,13 @@ def test_bench_column_throughput_rows(ctx):
     assert [r["mode"] for r in l1] == ["direct"]
     with pytest.raises(ValueError, match="block size"):
         api.bench_column_throughput(api.KernelOracle(x, api.KernelSpec("l1laplace", 3.0)), [0], 0, ctx)
+
+
+@pytest.mark.parametrize("b,d,kernel", [(256, 8, "gaussian"), (256, 40, "l1laplace")])
+def test_max_block_size(ctx, b, d, kernel):  # b = 256: the largest tile configuration
+    x = wl.gen_c2(9000, d, 4)
+    g, r, o = run_both(x, kernel, math.sqrt(d), k=600, b=b, ctx=ctx)
+    assert_parity(g, r, o)
+    with pytest.raises(ValueError, match="block size <= 256"):
+        api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec(kernel, 1.0)),
+                                   api.RunConfig.until_rank(10, 257, 0), ctx)

@@ -227,3 +227,14 @@ def test_gpu_lowmem_invalid_arguments(ctx):
     wide = api.KernelOracle(wl.gen_c1(100, 200, 0), api.KernelSpec("gaussian", 1.0))
     with pytest.raises(ValueError, match="d <= 128"):
         api.accelerated_rpcholesky_lowmem(wide, api.RunConfig.until_rank(3, 2, 0), ctx)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("b,d,kernel", [(256, 8, "gaussian"), (120, 120, "l1laplace"),
+                                        (200, 128, "gaussian")])
+def test_gpu_lowmem_extreme_shapes(ctx, b, d, kernel):
+    """largest block (two warp columns), largest supported dimension (resident X tile of
+    128 coordinates, fewer pipeline stages)."""
+    x = wl.gen_c2(5000, d, 6)
+    g, r = run_both(ctx, x, kernel, math.sqrt(d), k=400, b=b)
+    assert_parity(g, r)
