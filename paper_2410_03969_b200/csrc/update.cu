@@ -9,6 +9,7 @@ namespace rpcb {
 
 int launch_update_wc1(const UpdateParams& p, int nf, cudaStream_t st);
 int launch_update_wc2(const UpdateParams& p, int nfw, cudaStream_t st);
+int launch_update_cols(const UpdateParams& p, int nf, cudaStream_t st);
 
 // Fragment count nf = ceil(m / 8).  nf <= 16: two ping-pong warp groups per CTA, each
 // with 64-row tiles and a single warp column (no padded columns).  16 < nf <= 32: one
@@ -21,6 +22,7 @@ int update_tile_rows(int m) {
 
 int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
+  if (p.columns_only && nf <= 16) return launch_update_cols(p, nf, st);
   if (nf <= 16) return launch_update_wc1(p, nf, st);
   if (nf <= 32) return launch_update_wc2(p, (nf + 1) / 2, st);
   return -1;

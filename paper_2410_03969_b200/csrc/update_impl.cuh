@@ -91,7 +91,9 @@ __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ t
   return fma(t, q, t) * s1 * s2;
 }
 
-template <int WC, int NFW, bool GRAM, int MINB, int G>
+// COLS: compiled for the standalone K5 only (p.columns_only): phases 1-2, the park and the
+// epilogue are compiled out, so registers go to more resident CTAs instead.
+template <int WC, int NFW, bool GRAM, int MINB, int G, bool COLS = false>
 __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     update_kernel(UpdateParams p, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ CUtensorMap tmXS, const __grid_constant__ CUtensorMap tmF,
@@ -121,12 +123,12 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 
   const int m = p.m, kcur = p.kcur;
   const int nX = p.dchunks;
-  const int nFk = (kcur + 15) >> 4;
+  const int nFk = COLS ? 0 : (kcur + 15) >> 4;
   // Phase-2 A tiles start at F column kcur - koff: TMA box starts must be 16-byte
   // aligned in the inner dimension, so for odd kcur one extra leading column is
   // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
   const int koff = kcur & 1;
-  const int nL = p.columns_only ? 0 : (m + koff + 15) >> 4;
+  const int nL = (COLS || p.columns_only) ? 0 : (m + koff + 15) >> 4;
   const int T = nX + nFk + nL;               // chunks per tile
   const int ntiles = (int)((p.n_loc + BM - 1) / BM);
   const int vb = (int)blockIdx.x * G + grp, vgrid = (int)gridDim.x * G;  // virtual block per group
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     }
     if (G > 1 && grp == 0 && k == 0 && gtid == 0) s_go = 1;
     mark(1);
-    if (p.columns_only) {  // standalone K5: A(R, S) -> column-major output
+    if (COLS || p.columns_only) {  // standalone K5: A(R, S) -> column-major output
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) {
         const int64_t grow = tile_row0 + arow[fr];
@@ -543,12 +545,12 @@ inline int num_sms() {
   return n;
 }
 
-template <int WC, int NFW, bool GRAM, int MINB, int G>
+template <int WC, int NFW, bool GRAM, int MINB, int G, bool COLS = false>
 int launch_t(const UpdateParams& p, cudaStream_t st) {
   using C = UCfg<WC, NFW, G>;
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(update_kernel<WC, NFW, GRAM, MINB, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    if (cudaFuncSetAttribute(update_kernel<WC, NFW, GRAM, MINB, G, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              C::SMEM) != cudaSuccess)
       return -2;
     attr = true;
@@ -567,7 +569,7 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
   // CTAs per SM, which hides the latency of the short per-tile chains
   static int occ = 0;
   if (!occ) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<WC, NFW, GRAM, MINB, G>,
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<WC, NFW, GRAM, MINB, G, COLS>,
                                                       C::NT, C::SMEM) != cudaSuccess || occ < 1) {
       cudaGetLastError();
       occ = MINB;
@@ -575,7 +577,7 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
   }
   const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
   if (grid)
-    update_kernel<WC, NFW, GRAM, MINB, G><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
+    update_kernel<WC, NFW, GRAM, MINB, G, COLS><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
   return C::BM;
 }
 
