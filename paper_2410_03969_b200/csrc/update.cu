@@ -23,6 +23,9 @@ int update_tile_rows(int m) {
 int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
   if (p.columns_only && nf <= 16) return launch_update_cols(p, nf, st);
+  // 64 < m <= 96: two warp columns of half the accumulators, two CTAs per SM (measured
+  // 9% faster than the ping-pong pair at C4 rounds 1-2; slower for m > 96)
+  if (nf > 8 && nf <= 12) return launch_update_wc2(p, (nf + 1) / 2, st);
   if (nf <= 16) return launch_update_wc1(p, nf, st);
   if (nf <= 32) return launch_update_wc2(p, (nf + 1) / 2, st);
   return -1;
