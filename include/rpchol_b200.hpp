@@ -79,6 +79,8 @@ inline ResultPtr run(const PsdOracle& oracle, const RunConfig& cfg, Device& dev,
   switch (ko->kernel().kind) {
     case KernelKind::Gaussian: ks.kind = RPC_KERNEL_GAUSSIAN; break;
     case KernelKind::L1Laplace: ks.kind = RPC_KERNEL_L1LAPLACE; break;
+    case KernelKind::Matern32: ks.kind = RPC_KERNEL_MATERN32; break;
+    case KernelKind::Matern52: ks.kind = RPC_KERNEL_MATERN52; break;
     default:
       throw std::invalid_argument(std::string(who) + " (B200): unsupported kernel kind " +
                                   kernel_kind_name(ko->kernel().kind));

@@ -39,8 +39,13 @@ typedef enum {
   RPC_ENOMEM = 6    /* device or host allocation failed */
 } rpc_status;
 
-/* KernelKind (kernels.hpp:20) — the kinds the kernel oracle path supports. */
-typedef enum { RPC_KERNEL_GAUSSIAN = 0, RPC_KERNEL_L1LAPLACE = 1 } rpc_kernel_kind;
+/* KernelKind (kernels.hpp:20): every kind the reference's KernelOracle supports. */
+typedef enum {
+  RPC_KERNEL_GAUSSIAN = 0,
+  RPC_KERNEL_L1LAPLACE = 1,
+  RPC_KERNEL_MATERN32 = 2,
+  RPC_KERNEL_MATERN52 = 3
+} rpc_kernel_kind;
 /* DistanceMode (oracle.hpp:37); DEFAULT = default_distance_mode (oracle.hpp:39-42). */
 typedef enum { RPC_DIST_DIRECT = 0, RPC_DIST_GRAM = 1, RPC_DIST_DEFAULT = -1 } rpc_distance_mode;
 /* RunConfig::Mode (rpcholesky.hpp:37). */

@@ -20,7 +20,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB = None
 
-KERNELS = {"gaussian": 0, "l1laplace": 1, "laplace": 1}
+KERNELS = {"gaussian": 0, "l1laplace": 1, "laplace": 1, "matern32": 2, "matern52": 3}
 DIST = {"direct": 0, "gram": 1}
 MODES = {"fixed_rounds": 0, "until_rank": 1}
 _ERRS = {1: ValueError, 2: IndexError, 3: RuntimeError, 4: MemoryError}

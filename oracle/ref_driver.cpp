@@ -80,12 +80,20 @@ void fill(const rpchol::CholeskyResult& r, Res* out, int64_t b) {
   out->captured_sq = 0.0;
 }
 
+rpchol::KernelKind kind_of(int kind) {
+  switch (kind) {
+    case 0: return rpchol::KernelKind::Gaussian;
+    case 1: return rpchol::KernelKind::L1Laplace;
+    case 2: return rpchol::KernelKind::Matern32;
+    default: return rpchol::KernelKind::Matern52;
+  }
+}
+
 rpchol::KernelOracle make_kernel(const double* x, int64_t n, int64_t d, int kind, double sigma,
                                  int dist) {
   Eigen::MatrixXd pts(n, d);
   std::memcpy(pts.data(), x, sizeof(double) * (size_t)(n * d));
-  rpchol::KernelSpec spec(kind == 0 ? rpchol::KernelKind::Gaussian : rpchol::KernelKind::L1Laplace,
-                          sigma);
+  rpchol::KernelSpec spec(kind_of(kind), sigma);
   return rpchol::KernelOracle(rpchol::DataMatrix(std::move(pts)), spec,
                               dist == 1 ? rpchol::DistanceMode::GramTrick
                                         : rpchol::DistanceMode::Direct);
@@ -258,8 +266,7 @@ int ref_kernel_matvec(const double* x, int64_t n, int64_t d, int kind, double si
     Eigen::MatrixXd pts(n, d);
     std::memcpy(pts.data(), x, sizeof(double) * (size_t)(n * d));
     rpchol::DataMatrix data(std::move(pts));
-    rpchol::KernelSpec spec(kind == 0 ? rpchol::KernelKind::Gaussian : rpchol::KernelKind::L1Laplace,
-                            sigma);
+    rpchol::KernelSpec spec(kind_of(kind), sigma);
     Eigen::VectorXd vv(n);
     std::memcpy(vv.data(), v, sizeof(double) * (size_t)n);
     Eigen::VectorXd o = rpchol::kernel_matvec(
@@ -284,8 +291,7 @@ int ref_fit_krr(const double* x, int64_t n, int64_t d, int kind, double sigma,
     Eigen::MatrixXd pts(n, d);
     std::memcpy(pts.data(), x, sizeof(double) * (size_t)(n * d));
     rpchol::DataMatrix data(std::move(pts));
-    rpchol::KernelSpec spec(kind == 0 ? rpchol::KernelKind::Gaussian : rpchol::KernelKind::L1Laplace,
-                            sigma);
+    rpchol::KernelSpec spec(kind_of(kind), sigma);
     Eigen::VectorXd t(n);
     std::memcpy(t.data(), targets, sizeof(double) * (size_t)n);
     rpchol::KrrOptions opts;

@@ -93,7 +93,7 @@ int rpo_oracle_kernel(rpo_oracle* o, const double* x, int64_t n, int64_t d, int 
     if (!isfinite(x[i])) return fail(RPO_EINVAL, "DataMatrix: non-finite entry");
   /* kernels.hpp:47-49 */
   if (!(sigma > 0.0) || !isfinite(sigma)) return fail(RPO_EINVAL, "KernelSpec: bandwidth must be positive");
-  if (kind != RPO_KERNEL_GAUSSIAN && kind != RPO_KERNEL_L1LAPLACE)
+  if (kind < RPO_KERNEL_GAUSSIAN || kind > RPO_KERNEL_MATERN52)
     return fail(RPO_EINVAL, "unknown kernel kind");
   /* oracle.hpp:253-257 */
   if (dist_mode == RPO_DIST_GRAM && kind == RPO_KERNEL_L1LAPLACE)
@@ -145,8 +145,18 @@ static int check_indices(const int64_t* idx, int64_t k, int64_t n, const char* w
   return RPO_OK;
 }
 
-/* kernels.hpp:60-64  kernel_from_sq_dist (Gaussian) */
-static inline double gaussian_from_sq(double sq, double sigma) {
+/* kernels.hpp:59-79  kernel_from_sq_dist (l2 kernels) */
+static inline double kernel_from_sq(int kind, double sq, double sigma) {
+  if (kind == RPO_KERNEL_MATERN32) {
+    const double rho = sqrt(sq) / sigma;
+    const double z = sqrt(3.0) * rho;
+    return (1.0 + z) * exp(-z);
+  }
+  if (kind == RPO_KERNEL_MATERN52) {
+    const double rho2 = sq / (sigma * sigma);
+    const double z = sqrt(5.0 * rho2);
+    return (1.0 + z + (5.0 / 3.0) * rho2) * exp(-z);
+  }
   return exp(-0.5 * sq / (sigma * sigma));
 }
 
@@ -195,7 +205,7 @@ static void kernel_column(const rpo_oracle* o, const int64_t* rows, int64_t nr, 
       out[a] = dd;
     }
   }
-  for (int64_t a = 0; a < nr; ++a) out[a] = gaussian_from_sq(out[a], o->sigma);
+  for (int64_t a = 0; a < nr; ++a) out[a] = kernel_from_sq(o->kind, out[a], o->sigma);
 }
 
 int rpo_submatrix(const rpo_oracle* o, const int64_t* rows, int64_t nr, const int64_t* cols,

@@ -34,7 +34,7 @@ enum {
   RPO_ENOMEM = 4
 };
 
-enum { RPO_KERNEL_GAUSSIAN = 0, RPO_KERNEL_L1LAPLACE = 1 };
+enum { RPO_KERNEL_GAUSSIAN = 0, RPO_KERNEL_L1LAPLACE = 1, RPO_KERNEL_MATERN32 = 2, RPO_KERNEL_MATERN52 = 3 };
 enum { RPO_DIST_DIRECT = 0, RPO_DIST_GRAM = 1 };
 enum { RPO_MODE_FIXED_ROUNDS = 0, RPO_MODE_UNTIL_RANK = 1 };
 

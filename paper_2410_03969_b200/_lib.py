@@ -13,7 +13,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "librpchol_b200.so")
 
 RPC_OK, RPC_EINVAL, RPC_ERANGE, RPC_ENUMERIC, RPC_ECUDA, RPC_ENCCL, RPC_ENOMEM = range(7)
-RPC_KERNEL_GAUSSIAN, RPC_KERNEL_L1LAPLACE = 0, 1
+RPC_KERNEL_GAUSSIAN, RPC_KERNEL_L1LAPLACE, RPC_KERNEL_MATERN32, RPC_KERNEL_MATERN52 = 0, 1, 2, 3
 RPC_DIST_DIRECT, RPC_DIST_GRAM, RPC_DIST_DEFAULT = 0, 1, -1
 RPC_FIXED_ROUNDS, RPC_UNTIL_RANK = 0, 1
 RPC_COL_MAJOR, RPC_ROW_MAJOR = 0, 1

@@ -21,7 +21,8 @@ import numpy as np
 from . import _lib as L
 
 KERNEL_KINDS = {"gaussian": L.RPC_KERNEL_GAUSSIAN, "l1laplace": L.RPC_KERNEL_L1LAPLACE,
-                "laplace": L.RPC_KERNEL_L1LAPLACE}
+                "laplace": L.RPC_KERNEL_L1LAPLACE, "matern32": L.RPC_KERNEL_MATERN32,
+                "matern52": L.RPC_KERNEL_MATERN52}  # kernel_kind_from_name (kernels.hpp:31-37)
 DISTANCE_MODES = {None: L.RPC_DIST_DEFAULT, "direct": L.RPC_DIST_DIRECT, "gram": L.RPC_DIST_GRAM}
 
 

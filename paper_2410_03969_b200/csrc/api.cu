@@ -59,6 +59,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                        HostSink sink) {
   int kind = 0;
   validate(n, d, kspec, cfg, kind);
+  double kscale = 0.0;
+  const int kfun = kernel_fun(kspec, &kscale);
   if (algo != kAlgoAccelerated && lowmem) raise(RPC_EINVAL, "low-memory mode is accelerated-only");
   if (sink.p && lowmem) raise(RPC_EINVAL, "low-memory result has no factor to stream");
   if (lowmem && round_up(d, 16) > 128)
@@ -313,7 +315,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                   prop.as<double>(), st);
     if (lowmem && kcur > 0) {
       // F(S', :) = A(S', S) L^{-T}  (= W_prop^T of rpcholesky.hpp:441-444)
-      launch_kprop(prop.as<double>(), lay, b, piv.as<double>(), prec, (int)kcur, (int)d, kind,
+      launch_kprop(prop.as<double>(), lay, b, piv.as<double>(), prec, (int)kcur, (int)d, kind, kfun,
                    kspec.sigma, Kp.as<double>(), ldf, st);
       launch_gemm(b, (int)kcur, (int)kcur, 1.0, Kp.as<double>(), ldf, 0, Linv.as<double>(), ldf, 1,
                   0.0, prop.as<double>() + lay.foff, lay.rec, st);
@@ -351,7 +353,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       CK(cudaMemcpyAsync(kept_idx.p, kidx.data(), sizeof(int) * mk, cudaMemcpyHostToDevice, st));
       launch_gather_records(prop.as<double>(), lay.rec, 2 + dpad + kcur, kept_idx.as<int>(), mk,
                             propk.as<double>(), st);
-      launch_hblock(propk.as<double>(), lay, mk, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
+      launch_hblock(propk.as<double>(), lay, mk, (int)dpad, (int)d, (int)kcur, kind, kfun, kspec.sigma,
                     Hbuf.as<double>(), st);
       launches += 2;
       for (int attempt = 0;; ++attempt) {
@@ -385,7 +387,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       CK(cudaStreamSynchronize(st));
     } else {
     // -- K3: H block; K4: rejection sweep (replicated on every shard)
-    launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kspec.sigma,
+    launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kfun, kspec.sigma,
                   Hbuf.as<double>(), st);
     dbg(st, "hblock");
     launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
@@ -482,7 +484,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           lp.kold = (int)kcur;
           lp.knew = (int)(kcur + m);
           lp.kind = kind;
-          lp.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
+          lp.kfun = kernel_fun(kspec, &lp.escale);
           lp.tile_g2 = s.tile_g2.as<double>();
           lp.pin = 1;
           upd_ev.emplace_back();
@@ -529,7 +531,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.ldl = ldl;
         up.sigma = kspec.sigma;
         up.kind = kind;
-        up.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
+        up.kfun = kernel_fun(kspec, &up.escale);
         up.tile_g2 = s.tile_g2.as<double>();
         if (dbg_phase) {
           CK(cudaMemsetAsync(phase_clk.p, 0, phase_clk.bytes, st));
@@ -1135,7 +1137,7 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
     RecordLayout lay{2 + dpad, 2, 2 + dpad};
     // Gaussian: Direct and GramTrick (is_l2_translation_invariant); l1: Direct only
     std::vector<int> modes{RPC_DIST_DIRECT};
-    if (kspec.kind == RPC_KERNEL_GAUSSIAN) modes.push_back(RPC_DIST_GRAM);
+    if (kspec.kind != RPC_KERNEL_L1LAPLACE) modes.push_back(RPC_DIST_GRAM);
     int64_t maxb = 1;
     for (int i = 0; i < n_sizes; ++i) {
       if (block_sizes[i] < 1) raise(RPC_EINVAL, "bench_column_throughput: block size must be >= 1");
@@ -1187,7 +1189,7 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
               up.ldl = 16;
               up.sigma = ks.sigma;
               up.kind = kind;
-              up.escale = kind == kL1 ? -1.0 / ks.sigma : -0.5 / (ks.sigma * ks.sigma);
+              up.kfun = kernel_fun(ks, &up.escale);
               up.tile_g2 = tile.as<double>();
               up.columns_only = 1;
               up.cols_out = outd.as<double>() + (c0 % mb) * n;
@@ -1287,7 +1289,7 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.ldl = 16;
       up.sigma = kspec.sigma;
       up.kind = kind;
-      up.escale = kind == kL1 ? -1.0 / kspec.sigma : -0.5 / (kspec.sigma * kspec.sigma);
+      up.kfun = kernel_fun(kspec, &up.escale);
       up.tile_g2 = tile.as<double>();
       up.columns_only = 1;
       up.cols_out = outd.as<double>();

@@ -5,7 +5,12 @@
 
 namespace rpcb {
 
+// Distance term: l2 squared distance by the Gram trick or directly, or the l1 distance.
 enum DistKind { kGaussGram = 0, kGaussDirect = 1, kL1 = 2 };
+// Kernel function of the distance term (kernels.hpp:60-79): exp(scale * dd) for Gaussian
+// (scale -0.5/sigma^2) and l1 Laplace (scale -1/sigma); Matern 3/2 (scale 1/sigma) and
+// Matern 5/2 (scale 1/sigma^2) of the squared l2 distance.
+enum KernelFun { kFunExp = 0, kFunMatern32 = 1, kFunMatern52 = 2 };
 
 // Proposal record layout (one per draw, fp64 words):
 //   [0] global id (exact in fp64), [1] ||x||^2, [2, 2+dpad) x, [2+dpad, 2+dpad+ldf) F row
@@ -62,7 +67,7 @@ void launch_select(const double* recv, int64_t slot_stride, const int* owner, in
 
 // ---- K3/K4: H block, rejection sweep, L^{-1} ------------------------------
 void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d, int kcur,
-                   int kind, double sigma, double* H, cudaStream_t st);
+                   int kind, int kfun, double sigma, double* H, cudaStream_t st);
 struct SweepOut {
   int32_t m;
   int32_t pad;
@@ -99,7 +104,8 @@ struct UpdateParams {
   int m;
   const double* linv; int64_t ldl;             // L^{-1} rows perm_row(a), [256][ldl]
   double sigma; int kind;
-  double escale;            // -0.5/sigma^2 (Gaussian) or -1/sigma (l1), host-computed
+  double escale;            // kernel-function scale (KernelFun), host-computed
+  int kfun;                 // KernelFun
   double* tile_g2;                              // [n_tiles] per-CTA ||G||^2 partial (row order)
   // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
   int columns_only; double* cols_out; int64_t ld_out;
@@ -145,7 +151,7 @@ struct LowmemParams {
   const double* piv; int64_t prec;                    // pivot records [knew][prec]
   const double* W; int64_t ldw;                       // W = Linv + kold * ldw, [m][knew]
   int m, kold, knew;
-  int kind; double escale;
+  int kind; double escale; int kfun;                  // DistKind, KernelFun scale, KernelFun
   double* tile_g2;                                    // [n_tiles] per-tile ||G||^2
   // product mode (kernel_matvec / predict, krr.hpp:143-162, 227-250): instead of the
   // diagonal update, out[row * ld_out + j] = (A(R, S) W^T)[row][j] + add_coef * add_vec[row]
@@ -163,7 +169,8 @@ void launch_gemm(int M, int N, int K, double alpha, const double* A, int64_t lda
                  cudaStream_t st);
 // K[j][i] = A(prop_j, piv_i) for j < b, i < k (kentry.cuh).
 void launch_kprop(const double* prop, RecordLayout lay, int b, const double* piv, int64_t prec,
-                  int k, int d, int kind, double sigma, double* K, int64_t ldk, cudaStream_t st);
+                  int k, int d, int kind, int kfun, double sigma, double* K, int64_t ldk,
+                  cudaStream_t st);
 // Appends the m accepted pivots: piv rows, F_S = prop F rows -> fs[m][ldk] and L rows
 // [kold+a] = (F_S[a], L_sel[a]), Linv rows [kold+a][kold..] = L_sel^{-1}[a] (from linv_rm,
 // rows perm_row(a), koff 0).

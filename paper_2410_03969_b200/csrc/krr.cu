@@ -249,7 +249,7 @@ void upload_points(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t 
 // A(R, S) W^T in product mode: rows = packed points (X, sqn), columns = point records.
 void kernel_product(rpc_ctx* ctx, const double* X, const double* sqn, int64_t n_rows, int64_t dpad,
                     int64_t d, const double* rec, int64_t prec, int64_t n_cols, const double* W,
-                    int64_t ldw, int m, int kind, double sigma, int pin, double* out,
+                    int64_t ldw, int m, int kind, int kfun, double kscale, int pin, double* out,
                     int64_t ld_out, const double* add_vec, double add_coef, double add_const) {
   LowmemParams lp{};
   lp.X = X;
@@ -268,7 +268,8 @@ void kernel_product(rpc_ctx* ctx, const double* X, const double* sqn, int64_t n_
   lp.kold = (int)n_cols;  // no triangular structure in W
   lp.knew = (int)n_cols;
   lp.kind = kind;
-  lp.escale = kind == kL1 ? -1.0 / sigma : -0.5 / (sigma * sigma);
+  lp.kfun = kfun;
+  lp.escale = kscale;
   lp.tile_g2 = nullptr;
   lp.out_mode = 1;
   lp.out = out;
@@ -289,8 +290,8 @@ using namespace rpcb_rt;
 struct rpc_krr {
   rpc_ctx* ctx = nullptr;
   int64_t n = 0, d = 0, dpad = 0, prec = 0;
-  int kind = 0;
-  double sigma = 1.0, mu = 0.0, mean = 0.0;
+  int kind = 0, kfun = 0;
+  double sigma = 1.0, kscale = 0.0, mu = 0.0, mean = 0.0;
   DBuf X, sqn, rec, coef;
   int64_t iterations = 0;
   bool converged = false;
@@ -322,6 +323,8 @@ int rpc_kernel_matvec(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64
     int kind = 0;
     rpc_run_config cfg{1, RPC_UNTIL_RANK, 0, 1, 0, 0.0, 0};
     validate(n, d, kspec, cfg, kind);
+    double kscale = 0.0;
+    const int kfun = kernel_fun(kspec, &kscale);
     if (nrhs < 1 || nrhs > 8) raise(RPC_EINVAL, "kernel_matvec: this build supports 1..8 right-hand sides");
     if (round_up(d, 16) > 128) raise(RPC_EINVAL, "kernel_matvec: this build supports d <= 128");
     if (ldx < (layout == RPC_ROW_MAJOR ? d : n)) raise(RPC_EINVAL, "leading dimension too small");
@@ -337,7 +340,7 @@ int rpc_kernel_matvec(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64
     // V (n x nrhs column-major) is W^T row-major with rows padded to ldv
     CK(cudaMemcpy2DAsync(W.p, ldv * 8, v, n * 8, n * 8, nrhs, cudaMemcpyHostToDevice, st));
     kernel_product(ctx, X.as<double>(), sqn.as<double>(), n, dpad, d, rec.as<double>(), prec, n,
-                   W.as<double>(), ldv, (int)nrhs, kind, kspec.sigma, 1, o.as<double>(), nrhs,
+                   W.as<double>(), ldv, (int)nrhs, kind, kfun, kscale, 1, o.as<double>(), nrhs,
                    nullptr, 0.0, 0.0);
     // out: n x nrhs column-major <- o row-major [n][nrhs]
     if (nrhs == 1) {
@@ -377,6 +380,7 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
     m->prec = 2 + m->dpad;
     m->kind = kind;
     m->sigma = kspec.sigma;
+    m->kfun = kernel_fun(kspec, &m->kscale);
     m->mu = mu;
 
     // ---- low-rank preconditioner: accelerated_rpcholesky, UntilRank(min(rank, N)) ----
@@ -495,7 +499,7 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
     for (int64_t it = 0; it < max_iters; ++it) {
       // ap = A p + mu p  (fused kernel regeneration + tensor-core product)
       kernel_product(ctx, m->X.as<double>(), m->sqn.as<double>(), n, m->dpad, d,
-                     m->rec.as<double>(), m->prec, n, p.as<double>(), ldv, 1, kind, kspec.sigma,
+                     m->rec.as<double>(), m->prec, n, p.as<double>(), ldv, 1, kind, m->kfun, m->kscale,
                      1, ap.as<double>(), 1, p.as<double>(), mu, 0.0);
       dot_partial_kernel<<<nb, kRedThreads, 0, st>>>(p.as<double>(), ap.as<double>(), n,
                                                      part.as<double>());
@@ -576,7 +580,7 @@ int rpc_krr_predict(const rpc_krr* m, const double* q, int64_t nq, int64_t d, in
     // f(x) = sum_i beta_i kappa(x_i, x) + mean; query and training are different sets:
     // no same-index pin (oracle.hpp:149-166)
     kernel_product(ctx, Q.as<double>(), qsqn.as<double>(), nq, m->dpad, d, m->rec.as<double>(),
-                   m->prec, m->n, m->coef.as<double>(), round_up(m->n, 16), 1, m->kind, m->sigma,
+                   m->prec, m->n, m->coef.as<double>(), round_up(m->n, 16), 1, m->kind, m->kfun, m->kscale,
                    0, o.as<double>(), 1, nullptr, 0.0, m->mean);
     CK(cudaMemcpyAsync(out, o.p, sizeof(double) * nq, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

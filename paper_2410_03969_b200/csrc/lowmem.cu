@@ -94,23 +94,26 @@ void launch_gemm(int M, int N, int K, double alpha, const double* A, int64_t lda
 
 __global__ void kprop_kernel(const double* __restrict__ prop, RecordLayout lay,
                              const double* __restrict__ piv, RecordLayout play, int k, int d,
-                             int kind, double sigma, double* __restrict__ K, int64_t ldk) {
+                             int kind, int kfun, double sigma, double* __restrict__ K,
+                             int64_t ldk) {
   const int j = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= k) return;
   K[(int64_t)j * ldk + i] =
-      kernel_entry(prop + (int64_t)j * lay.rec, piv + (int64_t)i * play.rec, lay, d, kind, sigma);
+      kernel_entry(prop + (int64_t)j * lay.rec, piv + (int64_t)i * play.rec, lay, d, kind, kfun,
+                   sigma);
 }
 
 void launch_kprop(const double* prop, RecordLayout lay, int b, const double* piv, int64_t prec,
-                  int k, int d, int kind, double sigma, double* K, int64_t ldk, cudaStream_t st) {
+                  int k, int d, int kind, int kfun, double sigma, double* K, int64_t ldk,
+                  cudaStream_t st) {
   if (k <= 0 || b <= 0) return;
   RecordLayout play;
   play.rec = prec;
   play.xoff = 2;
   play.foff = prec;
   kprop_kernel<<<dim3((unsigned)((k + 127) / 128), (unsigned)b), 128, 0, st>>>(
-      prop, lay, piv, play, k, d, kind, sigma, K, ldk);
+      prop, lay, piv, play, k, d, kind, kfun, sigma, K, ldk);
 }
 
 __global__ void lowmem_append_kernel(const double* __restrict__ prop, RecordLayout lay,

@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(256, MINB)
               for (int fr = 0; fr < 2; ++fr) {
                 double dd = __dadd_rn(__dadd_rn(-2.0 * gv[fr][j][v], sqr[fr]), sqc);
                 dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
-                gv[fr][j][v] = exp_tab(dd * escale, s_exp2);
+                gv[fr][j][v] = kfun_eval(dd, p.kfun, escale, s_exp2);
               }
             }
         } else {
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
             for (int j = 0; j < 2; ++j)
 #pragma unroll
-              for (int v = 0; v < 2; ++v) gv[fr][j][v] = exp_tab(dsum[fr][j][v] * escale, s_exp2);
+              for (int v = 0; v < 2; ++v) gv[fr][j][v] = kfun_eval(dsum[fr][j][v], p.kfun, escale, s_exp2);
         }
         // ---- acc += A(R, S_c) W(:, S_c)^T from registers --------------------------------
 #pragma unroll
@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(256, MINB)
             for (int fr = 0; fr < 2; ++fr) {
               double dd = __dadd_rn(__dadd_rn(-2.0 * ga[fr][j][v], sqr[fr]), sqc);
               dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
-              *reinterpret_cast<double*>(As + swz_off(arow[fr], kc)) = exp_tab(dd * escale, s_exp2);
+              *reinterpret_cast<double*>(As + swz_off(arow[fr], kc)) = kfun_eval(dd, p.kfun, escale, s_exp2);
             }
           }
         }
@@ -340,7 +340,7 @@ __global__ void __launch_bounds__(256, MINB)
         }
 #pragma unroll
         for (int e = 0; e < EPT; ++e)
-          *reinterpret_cast<double*>(As + swz_off(r, c0 + e)) = exp_tab(da[e] * escale, s_exp2);
+          *reinterpret_cast<double*>(As + swz_off(r, c0 + e)) = kfun_eval(da[e], p.kfun, escale, s_exp2);
       }
       gsync();
       // ---- acc += A(R, S_c) W(:, S_c)^T; W rows n have zeros beyond column kold + n ----

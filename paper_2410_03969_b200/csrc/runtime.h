@@ -241,7 +241,8 @@ inline void validate(int64_t n, int64_t d, const rpc_kernel_spec& k, rpc_run_con
   if (!(k.sigma > 0.0) || !std::isfinite(k.sigma))
     raise(RPC_EINVAL, "KernelSpec: bandwidth must be positive");
   int mode = k.distance_mode;
-  if (k.kind == RPC_KERNEL_GAUSSIAN) {
+  if (k.kind == RPC_KERNEL_GAUSSIAN || k.kind == RPC_KERNEL_MATERN32 ||
+      k.kind == RPC_KERNEL_MATERN52) {  // l2 translation-invariant (kernels.hpp:55-57)
     if (mode == RPC_DIST_DEFAULT) mode = RPC_DIST_GRAM;
     if (mode != RPC_DIST_GRAM && mode != RPC_DIST_DIRECT) raise(RPC_EINVAL, "unknown distance mode");
     kind = mode == RPC_DIST_GRAM ? kGaussGram : kGaussDirect;
@@ -262,6 +263,17 @@ inline void validate(int64_t n, int64_t d, const rpc_kernel_spec& k, rpc_run_con
     if (cfg.target_rank < 1) raise(RPC_EINVAL, "RunConfig: k, b must be >= 1");
   } else {
     raise(RPC_EINVAL, "RunConfig: unknown mode");
+  }
+}
+
+// KernelFun id and its scale for the device transforms (kernels.hpp:60-79; l1: oracle.hpp:303).
+inline int kernel_fun(const rpc_kernel_spec& k, double* scale) {
+  const double sg = k.sigma;
+  switch (k.kind) {
+    case RPC_KERNEL_MATERN32: *scale = 1.0 / sg; return kFunMatern32;
+    case RPC_KERNEL_MATERN52: *scale = 1.0 / (sg * sg); return kFunMatern52;
+    case RPC_KERNEL_L1LAPLACE: *scale = -1.0 / sg; return kFunExp;
+    default: *scale = -0.5 / (sg * sg); return kFunExp;
   }
 }
 

@@ -20,7 +20,7 @@ namespace rpcb {
 
 __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ prop,
                                                      RecordLayout lay, int b, int d, int kcur,
-                                                     int kind, double sigma,
+                                                     int kind, int kfun, double sigma,
                                                      double* __restrict__ H) {
   __shared__ double sp[16][129];
   __shared__ double sq[16][129];
@@ -43,16 +43,17 @@ __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ 
   }
   if (p < b && q < b) {
     const double a = kernel_entry(prop + (int64_t)p * lay.rec, prop + (int64_t)q * lay.rec, lay,
-                                  d, kind, sigma);
+                                  d, kind, kfun, sigma);
     H[(int64_t)p * b + q] = __dsub_rn(a, acc);
   }
 }
 
 void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d, int kcur,
-                   int kind, double sigma, double* H, cudaStream_t st) {
+                   int kind, int kfun, double sigma, double* H, cudaStream_t st) {
   (void)dpad;
   const int nb = (b + 15) / 16;
-  hblock_kernel<<<dim3(nb, nb), dim3(16, 16), 0, st>>>(prop, lay, b, d, kcur, kind, sigma, H);
+  hblock_kernel<<<dim3(nb, nb), dim3(16, 16), 0, st>>>(prop, lay, b, d, kcur, kind, kfun, sigma,
+                                                        H);
 }
 
 constexpr int kSweepThreads = 512;

@@ -91,6 +91,20 @@ __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ t
   return fma(t, q, t) * s1 * s2;
 }
 
+// Kernel value from the distance term (KernelFun, kernels.hpp:60-79); s = host-computed scale.
+__device__ __forceinline__ double kfun_eval(double dd, int f, double s, const double* tab) {
+  if (f == kFunMatern32) {
+    const double z = 1.7320508075688772 * (sqrt(dd) * s);
+    return (1.0 + z) * exp_tab(-z, tab);
+  }
+  if (f == kFunMatern52) {
+    const double rho2 = dd * s;
+    const double z = sqrt(5.0 * rho2);
+    return (1.0 + z + (5.0 / 3.0) * rho2) * exp_tab(-z, tab);
+  }
+  return exp_tab(dd * s, tab);
+}
+
 // COLS: compiled for the standalone K5 only (p.columns_only): phases 1-2, the park and the
 // epilogue are compiled out, so registers go to more resident CTAs instead.
 template <int WC, int NFW, bool GRAM, int MINB, int G, bool COLS = false>
@@ -349,7 +363,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
           dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr[fr]), sqc);
           dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
         }
-        const double val = exp_tab(dd * escale, s_exp2);
+        const double val = kfun_eval(dd, p.kfun, escale, s_exp2);
         a = (col < m && rin[fr]) ? -val : 0.0;
       };
 #pragma unroll 1

@@ -85,6 +85,10 @@ int main() {
   compare("l1 until_rank(150, 60)", l1, RunConfig::until_rank(150, 60, 1));
   KernelOracle direct(DataMatrix(x), KernelSpec(KernelKind::Gaussian, 2.0), DistanceMode::Direct);
   compare("gaussian-direct until_rank(100, 25)", direct, RunConfig::until_rank(100, 25, 2));
+  KernelOracle m32(DataMatrix(x), KernelSpec(KernelKind::Matern32, 2.0));
+  compare("matern32-gram until_rank(150, 40)", m32, RunConfig::until_rank(150, 40, 4));
+  KernelOracle m52(DataMatrix(x), KernelSpec(KernelKind::Matern52, 2.0), DistanceMode::Direct);
+  compare("matern52-direct fixed_rounds(4, 30)", m52, RunConfig::fixed_rounds(4, 30, 5));
   compare_lowmem("gaussian-gram until_rank(200, 40)", gauss, RunConfig::until_rank(200, 40, 0));
   compare_lowmem("l1 fixed_rounds(4, 60)", l1, RunConfig::fixed_rounds(4, 60, 1));
 

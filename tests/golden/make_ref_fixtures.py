@@ -32,6 +32,9 @@ CASES = {
     "c1": ("C1", 20000, 10, "gaussian", math.sqrt(10.0), 200, 40, 0),
     "c2s": ("C2", 8000, 20, "gaussian", math.sqrt(20.0), 300, 120, 0),
     "c3s": ("C3", 6000, 50, "l1laplace", 5.0, 300, 120, 0),
+    # Matern kernels (kernels.hpp:66-75) through the same KernelOracle path
+    "m32s": ("C2", 6000, 8, "matern32", 2.0, 250, 60, 0),
+    "m52s": ("C4", 8000, 30, "matern52", 3.0, 300, 120, 0),
 }
 
 LOWMEM_CASES = {

@@ -12,7 +12,7 @@ import pyoracle as po
 from paper_2410_03969_b200 import workloads as wl
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
-CASES = ["c1", "c2s", "c3s"]
+CASES = ["c1", "c2s", "c3s", "m32s", "m52s"]
 
 
 def load(name):

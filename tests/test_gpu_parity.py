@@ -135,7 +135,9 @@ def test_rejection_sweep_reference_properties(ctx):  # test_rpcholesky.cpp:98-14
 
 @pytest.mark.parametrize("kernel,dist,d", [("gaussian", "gram", 10), ("gaussian", "gram", 37),
                                            ("gaussian", "direct", 12), ("l1laplace", None, 50),
-                                           ("l1laplace", None, 3)])
+                                           ("l1laplace", None, 3), ("matern32", "gram", 9),
+                                           ("matern32", "direct", 20), ("matern52", "gram", 30),
+                                           ("matern52", "direct", 5)])
 def test_kernel_columns(ctx, kernel, dist, d):
     x = wl.gen_c3(5000, d, 1) * 3.0
     sigma = math.sqrt(d) * 0.7
@@ -343,3 +345,11 @@ def test_max_block_size(ctx, b, d, kernel):  # b = 256: the largest tile configu
     with pytest.raises(ValueError, match="block size <= 256"):
         api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec(kernel, 1.0)),
                                    api.RunConfig.until_rank(10, 257, 0), ctx)
+
+
+@pytest.mark.parametrize("kernel,dist", [("matern32", None), ("matern32", "direct"),
+                                         ("matern52", None), ("matern52", "direct")])
+def test_matern_parity(ctx, kernel, dist):  # KernelKind::Matern32/52, kernels.hpp:66-75
+    x = wl.gen_c2(6000, 8, 3)
+    g, r, o = run_both(x, kernel, 2.5, k=250, b=60, ctx=ctx, dist=dist)
+    assert_parity(g, r, o)

@@ -43,9 +43,16 @@ def rel(a, b):
 
 
 def dense_kernel(x, y, kern, sigma):
+    d2 = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
     if kern == "gaussian":
-        d2 = ((x[:, None, :] - y[None, :, :]) ** 2).sum(-1)
         return np.exp(-0.5 * d2 / sigma ** 2)
+    if kern == "matern32":
+        z = np.sqrt(3.0) * np.sqrt(d2) / sigma
+        return (1.0 + z) * np.exp(-z)
+    if kern == "matern52":
+        r2 = d2 / sigma ** 2
+        z = np.sqrt(5.0 * r2)
+        return (1.0 + z + 5.0 / 3.0 * r2) * np.exp(-z)
     return np.exp(-np.abs(x[:, None, :] - y[None, :, :]).sum(-1) / sigma)
 
 
@@ -87,7 +94,8 @@ def ctx():
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("kern,dist,d", [("gaussian", None, 3), ("gaussian", "direct", 10),
-                                         ("l1laplace", None, 20), ("gaussian", None, 100)])
+                                         ("l1laplace", None, 20), ("gaussian", None, 100),
+                                         ("matern32", None, 6), ("matern52", "direct", 4)])
 def test_gpu_kernel_matvec(ctx, kern, dist, d):
     from paper_2410_03969_b200 import api
     x = wl.gen_c2(1500, d, 2)

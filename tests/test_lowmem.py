@@ -238,3 +238,11 @@ def test_gpu_lowmem_extreme_shapes(ctx, b, d, kernel):
     x = wl.gen_c2(5000, d, 6)
     g, r = run_both(ctx, x, kernel, math.sqrt(d), k=400, b=b)
     assert_parity(g, r)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kernel,dist", [("matern32", None), ("matern52", "direct")])
+def test_gpu_lowmem_matern(ctx, kernel, dist):
+    x = wl.gen_c2(5000, 10, 2)
+    g, r = run_both(ctx, x, kernel, 3.0, k=200, b=50, dist=dist)
+    assert_parity(g, r)
