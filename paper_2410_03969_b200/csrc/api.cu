@@ -26,26 +26,6 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
   for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[j * k + i] = F[lr * ldf + j];
 }
 
-// Round status -> mapped pinned host memory: ScanStatus | SweepOut | proposal ids (double,
-// from the records) [b] | accepted ids [b].
-__global__ void publish_status_kernel(const ScanStatus* __restrict__ scan,
-                                      const SweepOut* __restrict__ sw, const double* __restrict__ prop,
-                                      int64_t rec, int b, const int64_t* __restrict__ acc,
-                                      char* host) {
-  ScanStatus* hs = reinterpret_cast<ScanStatus*>(host);
-  SweepOut* hw = reinterpret_cast<SweepOut*>(hs + 1);
-  double* hp = reinterpret_cast<double*>(hw + 1);
-  int64_t* ha = reinterpret_cast<int64_t*>(hp + b);
-  if (threadIdx.x == 0) {
-    *hs = *scan;
-    *hw = *sw;
-  }
-  for (int j = threadIdx.x; j < b; j += blockDim.x) {
-    hp[j] = prop[(int64_t)j * rec];
-    ha[j] = acc[j];
-  }
-}
-
 // The factorization proper.  `src` points to this process's shard rows (device
 // memory when src_on_device, else host memory of the full X).
 //
@@ -300,7 +280,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.draw0 = draw0;
       sp.b = b;
       sp.lay = lay;
-      sp.records = recv.as<double>() + (size_t)s.gidx * b * lay.rec;
+      // one shard: every draw is owned here, so records go straight to prop (no select)
+      sp.records = P == 1 ? prop.as<double>() : recv.as<double>() + (size_t)s.gidx * b * lay.rec;
       sp.owner = owner.as<int>();
       // every shard runs the sampler, including shards without rows: it also fills the
       // replicated owner[] table that the proposal selection reads
@@ -309,10 +290,13 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       dbg(st, "sample");
       ++launches;
     }
-    allgather(ctx, recv.as<double>(), (size_t)b * lay.rec);
-    const int64_t words = 2 + dpad + (lowmem ? 0 : kcur);
-    launch_select(recv.as<double>(), (int64_t)b * lay.rec, owner.as<int>(), b, lay.rec, words,
-                  prop.as<double>(), st);
+    if (P > 1) {
+      allgather(ctx, recv.as<double>(), (size_t)b * lay.rec);
+      const int64_t words = 2 + dpad + (lowmem ? 0 : kcur);
+      launch_select(recv.as<double>(), (int64_t)b * lay.rec, owner.as<int>(), b, lay.rec, words,
+                    prop.as<double>(), st);
+      ++launches;
+    }
     if (lowmem && kcur > 0) {
       // F(S', :) = A(S', S) L^{-T}  (= W_prop^T of rpcholesky.hpp:441-444)
       launch_kprop(prop.as<double>(), lay, b, piv.as<double>(), prec, (int)kcur, (int)d, kind, kfun,
@@ -390,20 +374,18 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kfun, kspec.sigma,
                   Hbuf.as<double>(), st);
     dbg(st, "hblock");
+    // the sweep's tail also publishes the round status into mapped host memory
     launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
                  pos.as<int>(), acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(), d_sweep,
-                 hp.as<double>(), st);
+                 hp.as<double>(), st, 0, hbuf_dev ? d_scan : nullptr, hbuf_dev);
     dbg(st, "sweep");
-    launches += 3;
+    launches += 2;
     if (hbuf_dev) {
-      // status words straight into mapped host memory: no copy-engine transfer, so the read
-      // never queues behind a factor block streaming out on the copy stream.  Published
-      // before L^{-1} / B' so the host's bookkeeping overlaps them and the update kernel is
-      // already queued when they finish.
-      publish_status_kernel<<<1, 256, 0, st>>>(d_scan, d_sweep, prop.as<double>(), lay.rec, b,
-                                               acc_ids.as<int64_t>(), hbuf_dev);
+      // status words went straight into mapped host memory (sweep tail): no copy-engine
+      // transfer, so the read never queues behind a factor block streaming out on the copy
+      // stream; recorded before L^{-1} / B' so the host's bookkeeping overlaps them and the
+      // update kernel is already queued when they finish.
       CK(cudaEventRecord(ev_pub.e, st));
-      ++launches;
     }
     // L^{-1} and the accepted-pivot operands only need the sweep's device-side outputs:
     // queue them before the status read so they run while the host waits.

@@ -77,7 +77,8 @@ struct SweepOut {
 // column-major), status.
 void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
                   RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
-                  SweepOut* out, double* scratch_hp, cudaStream_t st, int accept_all = 0);
+                  SweepOut* out, double* scratch_hp, cudaStream_t st, int accept_all = 0,
+                  const ScanStatus* pub_scan = nullptr, char* pub_host = nullptr);
 // H[i][i] += shift (block_rpcholesky's LLT retry, rpcholesky.hpp:311-319)
 void launch_add_diag(double* H, int b, double shift, cudaStream_t st);
 // out[j] = first `words` of record prop[idx[j]] (stride rec), j < m

@@ -75,7 +75,8 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     const double* __restrict__ H, int b, uint64_t seed, uint64_t draw0,
     const double* __restrict__ prop, RecordLayout lay, int* __restrict__ pos,
     int64_t* __restrict__ acc_ids, double* __restrict__ lcol, double* __restrict__ lacc_cm,
-    SweepOut* out, double* hp_global, int accept_all) {
+    SweepOut* out, double* hp_global, int accept_all, const ScanStatus* pub_scan,
+    char* pub_host) {
   extern __shared__ double sm[];
   __shared__ int s_m, s_nacc, s_acc[kSweepBlock];
   __shared__ double s_root[kSweepBlock];
@@ -178,11 +179,29 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     lacc_cm[idx] = (a >= c) ? lcol[(int64_t)c * b + s_pos[a]] : 0.0;
   }
   if (tid == 0) out->m = m;
+  if (pub_host) {  // round status -> mapped pinned host memory: ScanStatus | SweepOut | ids
+    ScanStatus* hs = reinterpret_cast<ScanStatus*>(pub_host);
+    SweepOut* hw = reinterpret_cast<SweepOut*>(hs + 1);
+    double* hpid = reinterpret_cast<double*>(hw + 1);
+    int64_t* haid = reinterpret_cast<int64_t*>(hpid + b);
+    if (tid == 0) {
+      *hs = *pub_scan;
+      SweepOut o;
+      o.m = m;
+      o.pad = 0;
+      *hw = o;
+    }
+    for (int j = tid; j < b; j += kSweepThreads) {
+      hpid[j] = prop[(int64_t)j * lay.rec];
+      haid[j] = j < m ? (int64_t)prop[(int64_t)s_pos[j] * lay.rec] : 0;
+    }
+  }
 }
 
 void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
                   RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol, double* lacc_cm,
-                  SweepOut* out, double* scratch_hp, cudaStream_t st, int accept_all) {
+                  SweepOut* out, double* scratch_hp, cudaStream_t st, int accept_all,
+                  const ScanStatus* pub_scan, char* pub_host) {
   const size_t packed = (size_t)b * (b + 1) / 2;
   size_t smem = sizeof(double) * (2 * (size_t)b + kSweepBlock * kSweepBlock + kSweepBlock * (size_t)b);
   double* hpg = nullptr;
@@ -197,7 +216,8 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
     attr = true;
   }
   sweep_kernel<<<1, kSweepThreads, smem, st>>>(H, b, seed, draw0, prop, lay, pos, acc_ids, lcol,
-                                                lacc_cm, out, hpg, accept_all);
+                                                lacc_cm, out, hpg, accept_all, pub_scan,
+                                                pub_host);
 }
 
 // L^{-1} by forward substitution L x = e_c, one warp per column c (8 columns per
