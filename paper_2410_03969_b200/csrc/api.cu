@@ -244,7 +244,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     const uint64_t draw0 = (algo == kAlgoAccelerated ? 2ull : 1ull) * (uint64_t)b * (uint64_t)round;
     // -- K2: scan of the residual diagonal (+ previous round's ||G||^2 partials)
     for (Shard& s : res->shards) {
-      launch_chunk_totals(s.u.as<double>(), s.n_loc, s.nchunks, totals_all.as<double>() + s.chunk0, st);
+      // (+ the previous update's per-tile ||G||^2 partials -> per-chunk, fixed order)
+      launch_chunk_totals(s.u.as<double>(), s.n_loc, s.nchunks, totals_all.as<double>() + s.chunk0, st,
+                          pending_g2 && s.n_loc ? s.tile_g2.as<double>() : nullptr,
+                          (int)((s.n_loc + 63) / 64), g2_all.as<double>() + s.chunk0);
       ++launches;
     }
     allgather(ctx, totals_all.as<double>(), L.cpr);
@@ -477,10 +480,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           dbg(st, "lowmem update");
           if (bm < 0)
             raise(RPC_ECUDA, "low-memory update launch failed (code " + std::to_string(bm) + ")");
-          const int64_t ntiles = (s.n_loc + bm - 1) / bm;
-          launch_tile_to_chunk(s.tile_g2.as<double>(), (int)ntiles, kChunk / bm, s.nchunks,
-                               g2_all.as<double>() + s.chunk0, st);
-          launches += 2;
+          launches += 1;  // per-tile ||G||^2 -> chunks: folded into the next chunk-totals pass
           ++upd_launches;
           const double N = (double)s.n_loc, kn = (double)(kcur + m);
           const double fl = 2.0 * N * m * kn + (kind == kGaussGram ? 2.0 * N * kn * d : 0.0);
@@ -544,10 +544,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                        sum[2] / nb / 1e6, sum[3] / nb / 1e6, sum[4] / nb / 1e6, sum[5] / nb / 1e6);
         }
         if (bm < 0) raise(RPC_ECUDA, "update kernel launch failed (code " + std::to_string(bm) + ")");
-        const int64_t ntiles = (s.n_loc + bm - 1) / bm;
-        launch_tile_to_chunk(s.tile_g2.as<double>(), (int)ntiles, kChunk / bm, s.nchunks,
-                             g2_all.as<double>() + s.chunk0, st);
-        launches += 2;
+        launches += 1;  // per-tile ||G||^2 -> chunks: folded into the next chunk-totals pass
         ++upd_launches;
         const double N = (double)s.n_loc;
         const double fl = 2.0 * N * m * kcur + N * (double)m * m + 2.0 * N * m * d;
@@ -589,6 +586,12 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   const auto h2 = clk::now();
   // ---- finalize ----------------------------------------------------------------
   if (pending_g2) {  // last round's ||G||^2 (no further scan consumed it)
+    for (Shard& s : res->shards) {
+      if (s.n_loc == 0) continue;
+      launch_tile_to_chunk(s.tile_g2.as<double>(), (int)((s.n_loc + 63) / 64), kChunk / 64,
+                           s.nchunks, g2_all.as<double>() + s.chunk0, st);
+      ++launches;
+    }
     allgather(ctx, g2_all.as<double>(), L.cpr);
     launch_chunk_prefix(totals_all.as<double>(), g2_all.as<double>(), L.ncg,
                         chunk_end.as<double>(), d_scan, st);

@@ -22,8 +22,11 @@ struct RecordLayout {
 
 // ---- K2: residual-diagonal scan + inverse-CDF sampling --------------------
 // Per-chunk totals of u over this shard's chunks (deterministic tree).
+// tile_g2 (optional): the previous update's per-64-row-tile ||G||^2 partials, folded into
+// chunk_g2[c] in fixed order (the update kernels' tiles are 64 rows: 64 tiles per chunk).
 void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
-                         cudaStream_t st);
+                         cudaStream_t st, const double* tile_g2 = nullptr, int n_tiles = 0,
+                         double* chunk_g2 = nullptr);
 // Sequential prefix over all global chunk totals -> chunk_end[], status.
 struct ScanStatus {
   double total;       // cumsum[N-1]

@@ -73,9 +73,14 @@ __device__ __forceinline__ double chunk_scan_core(const double* __restrict__ uc,
   return sh[t];
 }
 
+// Also folds the previous update's per-tile ||G||^2 partials into this chunk's partial
+// (tile_g2 != nullptr; same serial order as tile_to_chunk_kernel), saving a launch per round.
 __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double* __restrict__ u,
                                                                     int64_t n_loc,
-                                                                    double* __restrict__ totals) {
+                                                                    double* __restrict__ totals,
+                                                                    const double* __restrict__ tile_g2,
+                                                                    int n_tiles,
+                                                                    double* __restrict__ chunk_g2) {
   __shared__ double sh[kScanThreads + 1];
   const int c = blockIdx.x;
   const int64_t r0 = (int64_t)c * kChunk;
@@ -90,11 +95,21 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
       if (e == (last & 15)) v = s[e];
     totals[c] = __dadd_rn(base, v);
   }
+  if (tile_g2 && threadIdx.x == kScanThreads - 1) {
+    constexpr int kTilesPerChunk = kChunk / 64;
+    double g = 0.0;
+    const int t0 = c * kTilesPerChunk;
+    const int t1 = min(n_tiles, t0 + kTilesPerChunk);
+    for (int t = t0; t < t1; ++t) g = __dadd_rn(g, tile_g2[t]);
+    chunk_g2[c] = g;
+  }
 }
 
 void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
-                         cudaStream_t st) {
-  if (n_chunks > 0) chunk_totals_kernel<<<n_chunks, kScanThreads, 0, st>>>(u, n_loc, totals);
+                         cudaStream_t st, const double* tile_g2, int n_tiles, double* chunk_g2) {
+  if (n_chunks > 0)
+    chunk_totals_kernel<<<n_chunks, kScanThreads, 0, st>>>(u, n_loc, totals, tile_g2, n_tiles,
+                                                           chunk_g2);
 }
 
 // Serial chunk-offset chain (fixed order => p-invariant).  The totals are first staged
