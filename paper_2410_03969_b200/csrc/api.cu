@@ -160,6 +160,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   DBuf xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * ldf),
       sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
   DBuf shard_c0(ctx, sizeof(int) * (P + 1));
+  DBuf prefix_counter(ctx, sizeof(unsigned));
+  CK(cudaMemsetAsync(prefix_counter.p, 0, sizeof(unsigned), st));
   DBuf kept_idx, propk;  // block / simple: kept proposals (first draw of each distinct id)
   if (algo != kAlgoAccelerated) {
     kept_idx = DBuf(ctx, sizeof(int) * b);
@@ -243,19 +245,30 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // (rpcholesky.hpp:362-364, 179), block b proposals (293-296), simple one (226)
     const uint64_t draw0 = (algo == kAlgoAccelerated ? 2ull : 1ull) * (uint64_t)b * (uint64_t)round;
     // -- K2: scan of the residual diagonal (+ previous round's ||G||^2 partials)
+    // one shard: the totals pass also runs the chunk prefix (its last CTA), no extra launch
+    FusedPrefix fp;
+    if (P == 1) {
+      fp.counter = prefix_counter.as<unsigned>();
+      fp.n_chunks = L.ncg;
+      fp.chunk_end = chunk_end.as<double>();
+      fp.status = d_scan;
+      fp.g2_all = pending_g2 ? g2_all.as<double>() : nullptr;
+    }
     for (Shard& s : res->shards) {
       // (+ the previous update's per-tile ||G||^2 partials -> per-chunk, fixed order)
       launch_chunk_totals(s.u.as<double>(), s.n_loc, s.nchunks, totals_all.as<double>() + s.chunk0, st,
                           pending_g2 && s.n_loc ? s.tile_g2.as<double>() : nullptr,
-                          (int)((s.n_loc + 63) / 64), g2_all.as<double>() + s.chunk0);
+                          (int)((s.n_loc + 63) / 64), g2_all.as<double>() + s.chunk0, fp);
       ++launches;
     }
-    allgather(ctx, totals_all.as<double>(), L.cpr);
-    if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
-    launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr, L.ncg,
-                        chunk_end.as<double>(), d_scan, st);
+    if (P > 1) {
+      allgather(ctx, totals_all.as<double>(), L.cpr);
+      if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
+      launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr,
+                          L.ncg, chunk_end.as<double>(), d_scan, st);
+      ++launches;
+    }
     dbg(st, "scan");
-    ++launches;
     if (replay) {
       launch_replay_scan(res->shards[0].u.as<double>(), n, cumsum.as<double>(), d_scan, st);
       ++launches;

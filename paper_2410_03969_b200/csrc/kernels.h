@@ -21,12 +21,6 @@ struct RecordLayout {
 };
 
 // ---- K2: residual-diagonal scan + inverse-CDF sampling --------------------
-// Per-chunk totals of u over this shard's chunks (deterministic tree, DESIGN.md §4.2).
-// tile_g2 (optional): the previous update's per-64-row-tile ||G||^2 partials, folded into
-// chunk_g2[c] in fixed order (the update kernels' tiles are 64 rows: 64 tiles per chunk).
-void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
-                         cudaStream_t st, const double* tile_g2 = nullptr, int n_tiles = 0,
-                         double* chunk_g2 = nullptr);
 // Sequential prefix over all global chunk totals -> chunk_end[], status.
 struct ScanStatus {
   double total;       // cumsum[N-1]
@@ -34,6 +28,21 @@ struct ScanStatus {
   int32_t exhausted;  // !(total > 0)
   int32_t pad;
 };
+// Fused chunk prefix (single shard): counter != nullptr makes the last CTA of the totals
+// pass run launch_chunk_prefix's serial chain over all n_chunks (counter self-resets).
+struct FusedPrefix {
+  unsigned* counter = nullptr;
+  int n_chunks = 0;
+  double* chunk_end = nullptr;
+  ScanStatus* status = nullptr;
+  const double* g2_all = nullptr;
+};
+// Per-chunk totals of u over this shard's chunks (deterministic tree, DESIGN.md §4.2).
+// tile_g2 (optional): the previous update's per-64-row-tile ||G||^2 partials, folded into
+// chunk_g2[c] in fixed order (the update kernels' tiles are 64 rows: 64 tiles per chunk).
+void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
+                         cudaStream_t st, const double* tile_g2 = nullptr, int n_tiles = 0,
+                         double* chunk_g2 = nullptr, FusedPrefix fp = FusedPrefix());
 void launch_chunk_prefix(const double* totals_all, const double* g2_all, int n_chunks,
                          double* chunk_end, ScanStatus* status, cudaStream_t st);
 // One CTA per draw: draw j uses SplitMix64 counter draw0 + j.

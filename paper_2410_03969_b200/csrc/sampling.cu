@@ -80,7 +80,8 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
                                                                     double* __restrict__ totals,
                                                                     const double* __restrict__ tile_g2,
                                                                     int n_tiles,
-                                                                    double* __restrict__ chunk_g2) {
+                                                                    double* __restrict__ chunk_g2,
+                                                                    FusedPrefix fp) {
   __shared__ double sh[kScanThreads + 1];
   const int c = blockIdx.x;
   const int64_t r0 = (int64_t)c * kChunk;
@@ -103,13 +104,37 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
     for (int t = t0; t < t1; ++t) g = __dadd_rn(g, tile_g2[t]);
     chunk_g2[c] = g;
   }
+  if (fp.counter) {
+    // single shard: the last CTA to finish runs the serial chunk-offset chain of
+    // chunk_prefix_kernel (same order, same results) — one launch fewer per round
+    __shared__ int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(fp.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      __threadfence();
+      double off = 0.0, g2 = 0.0;
+#pragma unroll 8
+      for (int k = 0; k < fp.n_chunks; ++k) {
+        off = __dadd_rn(off, __ldcg(totals + k));
+        fp.chunk_end[k] = off;
+        g2 = __dadd_rn(g2, fp.g2_all ? __ldcg(fp.g2_all + k) : 0.0);
+      }
+      fp.status->total = off;
+      fp.status->g2_prev = g2;
+      fp.status->exhausted = !(off > 0.0);
+      *fp.counter = 0u;
+    }
+  }
 }
 
 void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
-                         cudaStream_t st, const double* tile_g2, int n_tiles, double* chunk_g2) {
+                         cudaStream_t st, const double* tile_g2, int n_tiles, double* chunk_g2,
+                         FusedPrefix fp) {
   if (n_chunks > 0)
     chunk_totals_kernel<<<n_chunks, kScanThreads, 0, st>>>(u, n_loc, totals, tile_g2, n_tiles,
-                                                           chunk_g2);
+                                                           chunk_g2, fp);
 }
 
 // Serial chunk-offset chain (fixed order => p-invariant).  The totals are first staged
