@@ -247,7 +247,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // -- K2: scan of the residual diagonal (+ previous round's ||G||^2 partials)
     // one shard: the totals pass also runs the chunk prefix (its last CTA), no extra launch
     FusedPrefix fp;
-    if (P == 1) {
+    const bool fuse_prefix = P == 1 && L.ncg <= kFusedPrefixMax;
+    if (fuse_prefix) {
       fp.counter = prefix_counter.as<unsigned>();
       fp.n_chunks = L.ncg;
       fp.chunk_end = chunk_end.as<double>();
@@ -261,7 +262,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                           (int)((s.n_loc + 63) / 64), g2_all.as<double>() + s.chunk0, fp);
       ++launches;
     }
-    if (P > 1) {
+    if (!fuse_prefix) {
       allgather(ctx, totals_all.as<double>(), L.cpr);
       if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
       launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr,

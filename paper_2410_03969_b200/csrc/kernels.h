@@ -28,8 +28,9 @@ struct ScanStatus {
   int32_t exhausted;  // !(total > 0)
   int32_t pad;
 };
-// Fused chunk prefix (single shard): counter != nullptr makes the last CTA of the totals
-// pass run launch_chunk_prefix's serial chain over all n_chunks (counter self-resets).
+// Fused chunk prefix (single shard, n_chunks <= kFusedPrefixMax): counter != nullptr makes the
+// last CTA of the totals pass run launch_chunk_prefix's serial chain (counter self-resets).
+constexpr int kFusedPrefixMax = 1024;
 struct FusedPrefix {
   unsigned* counter = nullptr;
   int n_chunks = 0;

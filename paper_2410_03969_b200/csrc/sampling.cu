@@ -108,23 +108,33 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
     // single shard: the last CTA to finish runs the serial chunk-offset chain of
     // chunk_prefix_kernel (same order, same results) — one launch fewer per round
     __shared__ int s_last;
+    __shared__ double s_tot[kFusedPrefixMax], s_g2[kFusedPrefixMax];
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = atomicAdd(fp.counter, 1u) == gridDim.x - 1;
     __syncthreads();
-    if (s_last && threadIdx.x == 0) {
+    if (s_last) {
       __threadfence();
-      double off = 0.0, g2 = 0.0;
-#pragma unroll 8
-      for (int k = 0; k < fp.n_chunks; ++k) {
-        off = __dadd_rn(off, __ldcg(totals + k));
-        fp.chunk_end[k] = off;
-        g2 = __dadd_rn(g2, fp.g2_all ? __ldcg(fp.g2_all + k) : 0.0);
+      // stage with the whole CTA (loads in parallel), then the serial chain from smem
+      for (int k = threadIdx.x; k < fp.n_chunks; k += blockDim.x) {
+        s_tot[k] = __ldcg(totals + k);
+        s_g2[k] = fp.g2_all ? __ldcg(fp.g2_all + k) : 0.0;
       }
-      fp.status->total = off;
-      fp.status->g2_prev = g2;
-      fp.status->exhausted = !(off > 0.0);
-      *fp.counter = 0u;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double off = 0.0, g2 = 0.0;
+        for (int k = 0; k < fp.n_chunks; ++k) {
+          off = __dadd_rn(off, s_tot[k]);
+          s_tot[k] = off;
+          g2 = __dadd_rn(g2, s_g2[k]);
+        }
+        fp.status->total = off;
+        fp.status->g2_prev = g2;
+        fp.status->exhausted = !(off > 0.0);
+        *fp.counter = 0u;
+      }
+      __syncthreads();
+      for (int k = threadIdx.x; k < fp.n_chunks; k += blockDim.x) fp.chunk_end[k] = s_tot[k];
     }
   }
 }
