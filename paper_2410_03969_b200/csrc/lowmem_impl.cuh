@@ -115,11 +115,16 @@ __global__ void __launch_bounds__(256, MINB)
   int arow[2];
 #pragma unroll
   for (int fr = 0; fr < 2; ++fr) arow[fr] = wr * 16 + 8 * fr + pg;
-  uint32_t foff[4], foffw[4];
+  // foffs: the pivot-point operand of the register-path Gram is read at row sigma(g) =
+  // perm8^{-1}(g) of each 8-row group, so C-fragment column 2t+v of fragment j is chunk
+  // column 8j + 4v + t = 4(2j+v) + t: exactly the A-operand k order of k-step 2j+v, and the
+  // W operand keeps the conflict-free fragment loads (foff).
+  uint32_t foff[4], foffs[4];
+  const int sg = (g >> 1) + 4 * (g & 1);  // perm8^{-1}(g)
 #pragma unroll
   for (int s = 0; s < 4; ++s) {
     foff[s] = swz_off(pg, 4 * s + t);
-    foffw[s] = swz_off(pg, 8 * (s >> 1) + perm8(2 * t + (s & 1)));  // register-A k order
+    foffs[s] = swz_off(sg, 4 * s + t);
   }
   const uint32_t a_base = (uint32_t)(wr * 16) * 128u;
   const uint32_t b_base = (uint32_t)(wc * NFW) * 1024u;
@@ -165,10 +170,9 @@ __global__ void __launch_bounds__(256, MINB)
       const unsigned char* Bw = Bs + b_base;
       if constexpr (WC == 1) {
         // ---- one warp column: the warp's 16 x 16 kernel tile stays in registers ------
-        // Lane (g, t) generates rows arow[fr] x chunk columns kc(j, v) = 8j + perm8(2t + v),
-        // exactly the C-fragment positions of a Gram DMMA against the TMA-staged pivot rows;
-        // read as A operand with k-step s = 2j + v (the k order inside the chunk is free,
-        // the W operand is fetched with the same permutation, foffw).
+        // Lane (g, t) generates rows arow[fr] x chunk columns kc(j, v) = 8j + 4v + t, exactly
+        // the C-fragment positions of a Gram DMMA against the TMA-staged pivot rows read at
+        // foffs; these are the A operand of k-step s = 2j + v as they sit in registers.
         double gv[2][2][2];
         if constexpr (GRAM) {
           // pivot norms / ids of this lane's four columns: issued before the Gram products so
@@ -178,7 +182,7 @@ __global__ void __launch_bounds__(256, MINB)
           for (int j = 0; j < 2; ++j)
 #pragma unroll
             for (int v = 0; v < 2; ++v) {
-              const int col = 16 * c + 8 * j + perm8(2 * t + v);
+              const int col = 16 * c + 8 * j + 4 * v + t;
               const bool cin = col < knew;
               sqc4[j][v] = cin ? __ldg(p.piv + (int64_t)col * p.prec + 1) : 0.0;
               idc4[j][v] = cin ? __ldg(p.piv + (int64_t)col * p.prec) : -1.0;
@@ -198,7 +202,7 @@ __global__ void __launch_bounds__(256, MINB)
               for (int fr = 0; fr < 2; ++fr) a[fr] = *reinterpret_cast<const double*>(Xw + fr * 1024 + foff[s4]);
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
-                const double bv = *reinterpret_cast<const double*>(Sw + j * 1024 + foff[s4]);
+                const double bv = *reinterpret_cast<const double*>(Sw + j * 1024 + foffs[s4]);
 #pragma unroll
                 for (int fr = 0; fr < 2; ++fr) dmma884(gv[fr][j][0], gv[fr][j][1], a[fr], bv);
               }
@@ -237,7 +241,7 @@ __global__ void __launch_bounds__(256, MINB)
               for (int j = 0; j < 2; ++j)
 #pragma unroll
                 for (int v = 0; v < 2; ++v)
-                  xs[j][v] = *reinterpret_cast<const double*>(Sw + swz_off(8 * j + perm8(2 * t + v), jj));
+                  xs[j][v] = *reinterpret_cast<const double*>(Sw + swz_off(8 * j + 4 * v + t, jj));
 #pragma unroll
               for (int fr = 0; fr < 2; ++fr)
 #pragma unroll
@@ -263,7 +267,7 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
           for (int q = 0; q < NFW; ++q) {
             if (q < q_lo) continue;
-            const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foffw[s4]);
+            const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s4]);
 #pragma unroll
             for (int fr = 0; fr < 2; ++fr)
               dmma884(acc[fr][q][0], acc[fr][q][1], gv[fr][s4 >> 1][s4 & 1], bv);
