@@ -70,44 +70,52 @@ void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos
                                              ldfs, sqnS, idS);
 }
 
-// Tiled C[8 x 128] = L^{-1}[8 rows, :m] * F_S[:m, 128 columns]; each output summed over
-// c ascending (deterministic), negated.
+// B' = -L^{-1} F_S (m x kcur).  One CTA per 8-column slice of F_S: the slice (m x 8, one
+// gather of 64-byte row pieces) is staged in shared memory once, L^{-1} rows are read through
+// L1 (the 8 threads of a column group share each row), and each thread sums its outputs over
+// c ascending (deterministic; the zeros above L^{-1}'s diagonal are skipped, which leaves
+// every sum bitwise unchanged).
+constexpr int kBpCols = 8;
 __global__ void __launch_bounds__(256) bprime_kernel(const double* __restrict__ linv_rm,
                                                      int64_t ldl, int koff,
                                                      const double* __restrict__ prop,
                                                      RecordLayout lay, const int* __restrict__ pos,
                                                      const int* __restrict__ m_dev, int kcur,
                                                      double* __restrict__ bp, int64_t ldbp) {
-  __shared__ double sL[8][257];
-  __shared__ double sF[16][129];
+  extern __shared__ double sF[];  // [m][kBpCols]
   const int m = *m_dev;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int n = blockIdx.y * 8 + ty;
-  const int k0 = blockIdx.x * 128;
-  for (int i = threadIdx.x; i < 8 * m; i += 256) {
-    const int r = i / m, c = i % m;
-    sL[r][c] = linv_rm[(int64_t)perm_row(blockIdx.y * 8 + r) * ldl + c + koff];
+  const int k0 = blockIdx.x * kBpCols;
+  for (int i = threadIdx.x; i < m * kBpCols; i += blockDim.x) {
+    const int c = i / kBpCols, kk = i % kBpCols;
+    sF[i] = k0 + kk < kcur ? __ldg(prop + (int64_t)pos[c] * lay.rec + lay.foff + k0 + kk) : 0.0;
   }
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int c0 = 0; c0 < m; c0 += 16) {
-    __syncthreads();
-    for (int i = threadIdx.x; i < 16 * 128; i += 256) {
-      const int cc = i >> 7, kk = i & 127;
-      const int c = c0 + cc, k = k0 + kk;
-      sF[cc][kk] = (c < m && k < kcur) ? prop[(int64_t)pos[c] * lay.rec + lay.foff + k] : 0.0;
-    }
-    __syncthreads();
-    const int cend = min(16, m - c0);
-    for (int cc = 0; cc < cend; ++cc) {
-      const double l = sL[ty][c0 + cc];
+  __syncthreads();
+  const int kk = threadIdx.x % kBpCols, a0 = threadIdx.x / kBpCols;
+  constexpr int kRowStep = 256 / kBpCols;  // 32
+  const int k = k0 + kk;
+  for (int ab = 0; ab < m; ab += 4 * kRowStep) {
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+    const double* lr[4];
+    int amax = -1;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[j] = fma(l, sF[cc][tx + 32 * j], acc[j]);
+    for (int j = 0; j < 4; ++j) {
+      const int a = ab + a0 + kRowStep * j;
+      lr[j] = linv_rm + (int64_t)perm_row(a < m ? a : 0) * ldl + koff;
+      if (a < m) amax = a;
     }
-  }
+    for (int c = 0; c <= amax; ++c) {
+      const double f = sF[c * kBpCols + kk];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const int k = k0 + tx + 32 * j;
-    if (k < kcur) bp[(int64_t)perm_row(n) * ldbp + k] = -acc[j];
+      for (int j = 0; j < 4; ++j) {
+        const int a = ab + a0 + kRowStep * j;
+        if (c <= a && a < m) acc[j] = fma(__ldg(lr[j] + c), f, acc[j]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int a = ab + a0 + kRowStep * j;
+      if (a < m && k < kcur) bp[(int64_t)perm_row(a) * ldbp + k] = -acc[j];
+    }
   }
 }
 
@@ -115,8 +123,9 @@ void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* p
                    RecordLayout lay, const int* pos, const int* m_dev, int m_max, int kcur,
                    double* bp, int64_t ldbp, cudaStream_t st) {
   if (kcur <= 0 || m_max <= 0) return;
-  dim3 grid((unsigned)((kcur + 127) / 128), (unsigned)((m_max + 7) / 8));
-  bprime_kernel<<<grid, 256, 0, st>>>(linv_rm, ldl, koff, prop, lay, pos, m_dev, kcur, bp, ldbp);
+  const unsigned grid = (unsigned)((kcur + kBpCols - 1) / kBpCols);
+  bprime_kernel<<<grid, 256, sizeof(double) * kBpCols * m_max, st>>>(linv_rm, ldl, koff, prop, lay,
+                                                                       pos, m_dev, kcur, bp, ldbp);
 }
 
 }  // namespace rpcb
