@@ -84,6 +84,29 @@ void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d,
                                                         H);
 }
 
+#ifdef RPC_SWEEP_PROBE  // debug aid (tools/sweep_probe.cu): per-block phase clocks
+__device__ unsigned long long g_sweep_clk[32][4];
+__device__ unsigned long long g_step_clk[256][4];
+#define STEP_CLK_ON(i, k)                            \
+  {                                                  \
+    if (lane == 0) g_step_clk[i][k] = clock64();     \
+    __syncwarp();                                    \
+  }
+#ifdef RPC_SWEEP_STEP_PROBE
+#define STEP_CLK(i, k) STEP_CLK_ON(i, k)
+#else
+#define STEP_CLK(i, k)
+#endif
+#define SWEEP_CLK(blk, ph)                                   \
+  {                                                          \
+    if (threadIdx.x == 0) g_sweep_clk[blk][ph] = clock64(); \
+    __syncwarp();                                            \
+  }
+#else
+#define SWEEP_CLK(blk, ph)
+#define STEP_CLK(i, k)
+#endif
+
 constexpr int kSweepThreads = 512;
 constexpr int kSweepBlock = 16;
 
@@ -130,7 +153,13 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   __syncthreads();
   for (int i0 = 0; i0 < b; i0 += kSweepBlock) {
     const int i1 = min(b, i0 + kSweepBlock);
+    SWEEP_CLK(i0 / kSweepBlock, 0)
     // ---- 1. decisions on the diagonal block (warp 0, registers + shuffles) ----
+    // The per-step critical path is  h_ii -> sqrt -> l_(i+1) = h_(i+1,i) / root ->
+    // h_(i+1,i+1) -= l_(i+1)^2 -> next decision.  The next diagonal is therefore formed and
+    // broadcast right after the division, ahead of the block's other rank-1 updates (lane
+    // i+1 computes exactly the value its row update below produces), and the u_i r_i
+    // products of the block are read before the chain starts.
     if (warp == 0) {
       int nacc = 0;
       const int p = i0 + lane;               // this lane's row inside the block
@@ -139,29 +168,51 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
 #pragma unroll
       for (int q = 0; q < kSweepBlock; ++q)
         row[q] = (live && i0 + q <= p) ? hp[tri(p) + i0 + q] : 0.0;
+      double ur[kSweepBlock];                // u_i * r_i (rounded), uniform across lanes
+#pragma unroll
+      for (int q = 0; q < kSweepBlock; ++q)
+        ur[q] = i0 + q < i1 ? __dmul_rn(udiag[i0 + q], rdraw[i0 + q]) : 0.0;
+      double hnext = __shfl_sync(0xffffffffu, row[0], 0);
 #pragma unroll
       for (int ii = 0; ii < kSweepBlock; ++ii) {
         const int i = i0 + ii;
         if (i >= i1) break;
-        const double hii = __shfl_sync(0xffffffffu, row[ii], ii);  // lane ii holds h(i, i)
-        if (!(__dmul_rn(udiag[i], rdraw[i]) < hii)) continue;       // uniform in the warp
+        STEP_CLK(i, 0)
+        const double hii = hnext;                 // h(i, i) after the previous steps
+        if (!(ur[ii] < hii)) {                    // uniform in the warp
+          if (ii + 1 < kSweepBlock) hnext = __shfl_sync(0xffffffffu, row[ii + 1], ii + 1);
+          continue;
+        }
         const double root = __dsqrt_rn(hii);
-        const double lp = (live && p >= i) ? __ddiv_rn(row[ii], root) : 0.0;
+        // lanes outside the column divide 1.0: a zero dividend would send them down the
+        // division's slow path and leave the warp diverged for the shuffles below
+        const bool own = live && p >= i;
+        const double lp_div = __ddiv_rn(own ? row[ii] : 1.0, root);
+        const double lp = own ? lp_div : 0.0;
+        STEP_CLK(i, 2)
+        __syncwarp();
+        if (ii + 1 < kSweepBlock)
+          hnext = __shfl_sync(0xffffffffu, __dsub_rn(row[ii + 1], __dmul_rn(lp, lp)), ii + 1);
+        STEP_CLK(i, 3)
         if (live && p >= i) lblk[nacc * kSweepBlock + (p - i0)] = lp;
+        __syncwarp();
 #pragma unroll
         for (int q = 0; q < kSweepBlock; ++q) {
+          if (q <= ii) continue;
           const double lq = __shfl_sync(0xffffffffu, lp, q);
-          if (q > ii && live && i0 + q <= p) row[q] = __dsub_rn(row[q], __dmul_rn(lp, lq));
+          if (live && i0 + q <= p) row[q] = __dsub_rn(row[q], __dmul_rn(lp, lq));
         }
         if (lane == 0) {
           s_acc[nacc] = i;
           s_root[nacc] = root;
         }
+        STEP_CLK(i, 1)
         ++nacc;
       }
       if (lane == 0) s_nacc = nacc;
     }
     __syncthreads();
+    SWEEP_CLK(i0 / kSweepBlock, 1)
     const int nacc = s_nacc;
     const int m0 = s_m;
     if (nacc > 0) {
@@ -182,6 +233,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
         if (j < c) continue;
         lcol[(int64_t)(m0 + k) * b + j] = j < i1 ? lblk[k * kSweepBlock + (j - i0)] : lpan[k * b + j];
       }
+      SWEEP_CLK(i0 / kSweepBlock, 2)
       // ---- 3. trailing update, acceptance order per entry ----
       for (int p = i1 + warp; p < b; p += nwarps) {
         const int64_t base = tri(p);
@@ -195,6 +247,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
       if (tid == 0) s_m = m0 + nacc;
     }
     __syncthreads();
+    SWEEP_CLK(i0 / kSweepBlock, 3)
   }
   const int m = s_m;
   for (int a = tid; a < m; a += kSweepThreads) {
