@@ -33,6 +33,26 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 // sweep and stopping rules, but no N x k factor: the proposals' factor rows come from
 // A(S', S) L^{-T}, and the diagonal update regenerates A(R, S_all) inside the update
 // kernel (lowmem_impl.cuh).  State: X, u, pivot records, L and L^{-1} (k x k).
+// RPC_DEBUG_TRACE: print CTA 0's per-group phase clocks and tile 5's per-chunk clocks
+static void dump_trace(const DBuf& buf, int m, int64_t kcur, cudaStream_t st) {
+  std::vector<unsigned long long> h(buf.bytes / 8);
+  CK(cudaMemcpyAsync(h.data(), buf.p, buf.bytes, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::fprintf(stderr, "[trace] m=%d kcur=%lld\n", m, (long long)kcur);
+  for (int g = 0; g < 2; ++g)
+    for (int t = 0; t < 64; ++t) {
+      const unsigned long long* r = &h[(g * 64 + t) * 8];
+      if (!r[0]) continue;
+      std::fprintf(stderr, "[trace] %d %d %llu %llu %llu %llu %llu %llu %llu\n", g, t, r[0], r[1], r[2],
+                   r[3], r[4], r[5], r[6]);
+    }
+  for (int g = 0; g < 2; ++g) {
+    std::fprintf(stderr, "[chunks] %d", g);
+    for (int c = 0; c < 128; ++c) std::fprintf(stderr, " %llu", h[1024 + g * 128 + c]);
+    std::fprintf(stderr, "\n");
+  }
+}
+
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
                        int64_t d, int64_t ldx, int layout, const rpc_kernel_spec& kspec,
                        rpc_run_config cfg, rpc_result* res, bool lowmem, int algo,
@@ -216,6 +236,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   upd_ev.reserve(8);
   std::vector<std::pair<int, int64_t>> upd_info;
   const bool dbg_phase = std::getenv("RPC_DEBUG_PHASES") != nullptr;
+  const bool dbg_trace = std::getenv("RPC_DEBUG_TRACE") != nullptr;
+  DBuf trace_buf(ctx, dbg_trace ? sizeof(unsigned long long) * (2 * 64 * 8 + 256) : 8);
   DBuf phase_clk(ctx, dbg_phase ? sizeof(unsigned long long) * 8 * 4096 : 8);
   std::vector<double> upd_flops;
   double update_ms = 0.0, flops = 0.0, bytes = 0.0;
@@ -380,7 +402,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       launch_linv(lacc.as<double>(), mk, (int)nbl, ldl, (int)(kcur & 1), linv.as<double>(), st);
       launch_gather_accepted(propk.as<double>(), lay, pos.as<int>(), mk, 256, 0, (int)dpad,
                              xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
-                             idS.as<double>(), st);
+                             idS.as<double>(), st, nullptr, gram_xscale(kind));
       launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), propk.as<double>(), lay,
                     pos.as<int>(), &d_sweep->m, mk, (int)kcur, fs.as<double>(), ldf, st);
       launches += 3;
@@ -413,7 +435,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     if (!lowmem) {
       launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, 0, (int)dpad,
                              xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
-                             idS.as<double>(), st, &d_sweep->m);
+                             idS.as<double>(), st, &d_sweep->m, gram_xscale(kind));
       launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), prop.as<double>(), lay, pos.as<int>(),
                     &d_sweep->m, b, (int)kcur, fs.as<double>(), ldf, st);
       launches += 2;
@@ -529,6 +551,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.kind = kind;
         up.kfun = kernel_fun(kspec, &up.escale);
         up.tile_g2 = s.tile_g2.as<double>();
+        if (dbg_trace) {
+          CK(cudaMemsetAsync(trace_buf.p, 0, trace_buf.bytes, st));
+          up.trace = trace_buf.as<unsigned long long>();
+        }
         if (dbg_phase) {
           CK(cudaMemsetAsync(phase_clk.p, 0, phase_clk.bytes, st));
           up.phase_clk = phase_clk.as<unsigned long long>();
@@ -557,6 +583,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                        sum[1] / nb / 1e6,
                        sum[2] / nb / 1e6, sum[3] / nb / 1e6, sum[4] / nb / 1e6, sum[5] / nb / 1e6);
         }
+        if (dbg_trace) dump_trace(trace_buf, m, kcur, st);
         if (bm < 0) raise(RPC_ECUDA, "update kernel launch failed (code " + std::to_string(bm) + ")");
         launches += 1;  // per-tile ||G||^2 -> chunks: folded into the next chunk-totals pass
         ++upd_launches;
@@ -1169,7 +1196,7 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
                                                              lay, prop.as<double>());
               launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), nc, 256, 0, (int)dpad,
                                      xs.as<double>(), fs.as<double>(), 16, sqnS.as<double>(),
-                                     idS.as<double>(), st);
+                                     idS.as<double>(), st, nullptr, gram_xscale(kind));
               UpdateParams up{};
               up.X = X.as<double>();
               up.dpad = dpad;
@@ -1266,7 +1293,7 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       CK(cudaMemcpy2DAsync(prop.p, lay.rec * 8, ids.data(), 8, 8, nc, cudaMemcpyHostToDevice, st));
       launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), (int)nc, 256, 0, (int)dpad,
                              xs.as<double>(), fs.as<double>(), 16, sqnS.as<double>(),
-                             idS.as<double>(), st);
+                             idS.as<double>(), st, nullptr, gram_xscale(kind));
       UpdateParams up{};
       up.X = X.as<double>();
       up.dpad = dpad;

@@ -125,6 +125,9 @@ struct UpdateParams {
   int columns_only; double* cols_out; int64_t ld_out;
   // RPC_DEBUG_TIMING: per-CTA cycle counters per phase ([grid][8] u64), or null
   unsigned long long* phase_clk;
+  // RPC_DEBUG_TRACE: CTA 0 per-group phase clocks [G][64 tiles][8], then per-chunk clocks
+  // of tile 5 [G][128] (debug only)
+  unsigned long long* trace;
 };
 // Row-tile height used for m accepted columns (128 or 64), or -1 if m unsupported.
 int update_tile_rows(int m);
@@ -138,10 +141,13 @@ void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* p
                    double* bp, int64_t ldbp, cudaStream_t st);
 // Gathers the accepted pivots' X rows, F rows (first kcur columns), norms and ids from the
 // proposal records into the update kernel's operand buffers (rows at perm_row(n), n < nb).
+// X rows are multiplied by xscale: the Gram kernel passes -2 (gram_xscale), so the DMMA
+// product is -2 X(R,:) X(S,:)^T bit for bit (a power-of-two scale is exact).
 void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,
                             int kcur, int dpad, double* xs, double* fs, int64_t ldfs,
                             double* sqnS, double* idS, cudaStream_t st,
-                            const int* m_dev = nullptr);
+                            const int* m_dev = nullptr, double xscale = 1.0);
+inline double gram_xscale(int kind) { return kind == kGaussGram ? -2.0 : 1.0; }
 // per-chunk sum of per-tile partials (tile = rows_per_tile rows)
 void launch_tile_to_chunk(const double* tile_g2, int n_tiles, int tiles_per_chunk,
                           int n_chunks_local, double* chunk_g2, cudaStream_t st);

@@ -216,7 +216,7 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
               for (int fr = 0; fr < 2; ++fr) {
                 double dd = __dadd_rn(__dadd_rn(-2.0 * gv[fr][j][v], sqr[fr]), sqc);
-                dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
+                dd = clamp_pin(dd, gid[fr], idc);
                 gv[fr][j][v] = kfun_eval(dd, p.kfun, escale, s_exp2);
               }
             }
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256, MINB)
 #pragma unroll
             for (int fr = 0; fr < 2; ++fr) {
               double dd = __dadd_rn(__dadd_rn(-2.0 * ga[fr][j][v], sqr[fr]), sqc);
-              dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
+              dd = clamp_pin(dd, gid[fr], idc);
               *reinterpret_cast<double*>(As + swz_off(arow[fr], kc)) = kfun_eval(dd, p.kfun, escale, s_exp2);
             }
           }

@@ -38,7 +38,7 @@ __global__ void gather_accepted_kernel(const double* __restrict__ prop, RecordLa
                                        const int* __restrict__ m_dev, int kcur, int kpad,
                                        int dpad, double* __restrict__ xs, double* __restrict__ fs,
                                        int64_t ldfs, double* __restrict__ sqnS,
-                                       double* __restrict__ idS) {
+                                       double* __restrict__ idS, double xscale) {
   const int n = blockIdx.x;
   const int m = m_dev ? *m_dev : m_host;
   const int dst = perm_row(n);
@@ -46,7 +46,7 @@ __global__ void gather_accepted_kernel(const double* __restrict__ prop, RecordLa
   double* fr = fs + (int64_t)dst * ldfs;
   if (n < m) {
     const double* rec = prop + (int64_t)pos[n] * lay.rec;
-    for (int i = threadIdx.x; i < dpad; i += blockDim.x) xr[i] = rec[lay.xoff + i];
+    for (int i = threadIdx.x; i < dpad; i += blockDim.x) xr[i] = xscale * rec[lay.xoff + i];
     for (int k = threadIdx.x; k < kpad; k += blockDim.x) fr[k] = k < kcur ? rec[lay.foff + k] : 0.0;
     if (threadIdx.x == 0) {
       sqnS[n] = rec[1];
@@ -64,10 +64,11 @@ __global__ void gather_accepted_kernel(const double* __restrict__ prop, RecordLa
 
 void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos, int m, int nb,
                             int kcur, int dpad, double* xs, double* fs, int64_t ldfs,
-                            double* sqnS, double* idS, cudaStream_t st, const int* m_dev) {
+                            double* sqnS, double* idS, cudaStream_t st, const int* m_dev,
+                            double xscale) {
   const int kpad = std::min<int64_t>(ldfs, ((kcur + 15) / 16) * 16);
   gather_accepted_kernel<<<nb, 256, 0, st>>>(prop, lay, pos, m, m_dev, kcur, kpad, dpad, xs, fs,
-                                             ldfs, sqnS, idS);
+                                             ldfs, sqnS, idS, xscale);
 }
 
 // B' = -L^{-1} F_S (m x kcur).  One CTA per 8-column slice of F_S: the slice (m x 8, one

@@ -71,9 +71,14 @@ __constant__ double kExpC[8] = {92.332482616893656,        // 64 / ln 2
 // No FP64<->int conversion instructions (slow paths on this part): k = rint(x 64/ln2)
 // comes out of the low mantissa bits of x * 64/ln2 + 1.5 * 2^52 (one rounding, ties
 // to even, exact for |k| < 2^51).
+// The argument is clamped at -708 so every result is normal and 2^n is an exact integer
+// add to the exponent field (no FP64 multiplies: the FP64 pipe is the one the DMMA main
+// loop issues to).  Below -708 the value returned is exp(-708) = 3.3e-308 instead of a
+// subnormal or zero, an absolute difference below 3.3e-308.
 __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ tab) {
   constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
-  x = fmax(x, kExpC[7]);
+  // x <= 0 here: the clamp is an unsigned compare of the bit patterns (integer pipe)
+  if ((unsigned long long)__double_as_longlong(x) > 0xC086200000000000ull) x = -708.0;
   const double ks = fma(x, kExpC[0], kShift);
   const int k = __double2loint(ks);
   const double kd = ks - kShift;
@@ -84,11 +89,17 @@ __device__ __forceinline__ double exp_tab(double x, const double* __restrict__ t
   q = fma(q, r, kExpC[6]);
   q = fma(q * r, r, r);                                      // expm1(r)
   const double t = tab[k & 63];
-  const int n = k >> 6;                                      // floor(k / 64)
-  const int n1 = n >> 1, n2 = n - n1;
-  const double s1 = __hiloint2double((n1 + 1023) << 20, 0);
-  const double s2 = __hiloint2double((n2 + 1023) << 20, 0);
-  return fma(t, q, t) * s1 * s2;
+  const double y = fma(t, q, t);
+  return __hiloint2double(__double2hiint(y) + ((k >> 6) << 20), __double2loint(y));
+}
+
+// D := 0 where D < 0 (clamp) or where the row and column are the same point (pin),
+// oracle.hpp:84-88; integer tests on the bit patterns (ids are non-negative integers held
+// exactly in doubles; -0.0 maps to 0.0, which yields the same kernel value 1).
+__device__ __forceinline__ double clamp_pin(double dd, double gid, double idc) {
+  const bool neg = __double2hiint(dd) < 0;
+  const bool pin = __double_as_longlong(gid) == __double_as_longlong(idc);
+  return (neg || pin) ? 0.0 : dd;
 }
 
 // Kernel value from the distance term (KernelFun, kernels.hpp:60-79); s = host-computed scale.
@@ -360,8 +371,9 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       auto xform = [&](double& a, int col, int fr, double sqc, double idc) {
         double dd = a;
         if (GRAM) {
-          dd = __dadd_rn(__dadd_rn(-2.0 * dd, sqr[fr]), sqc);
-          dd = (dd < 0.0 || gid[fr] == idc) ? 0.0 : dd;
+          // dd = -2 x.y already (operand X(S,:) pre-scaled by -2, gram_xscale)
+          dd = __dadd_rn(__dadd_rn(dd, sqr[fr]), sqc);
+          dd = clamp_pin(dd, gid[fr], idc);
         }
         const double val = kfun_eval(dd, p.kfun, escale, s_exp2);
         a = (col < m && rin[fr]) ? -val : 0.0;
