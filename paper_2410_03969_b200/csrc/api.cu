@@ -33,7 +33,7 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 // sweep and stopping rules, but no N x k factor: the proposals' factor rows come from
 // A(S', S) L^{-T}, and the diagonal update regenerates A(R, S_all) inside the update
 // kernel (lowmem_impl.cuh).  State: X, u, pivot records, L and L^{-1} (k x k).
-// RPC_DEBUG_TRACE: print CTA 0's per-group phase clocks and tile 5's per-chunk clocks
+// RPC_DEBUG_TRACE: print CTA 0's per-group, per-tile phase clocks of each update launch
 static void dump_trace(const DBuf& buf, int m, int64_t kcur, cudaStream_t st) {
   std::vector<unsigned long long> h(buf.bytes / 8);
   CK(cudaMemcpyAsync(h.data(), buf.p, buf.bytes, cudaMemcpyDeviceToHost, st));
@@ -46,11 +46,6 @@ static void dump_trace(const DBuf& buf, int m, int64_t kcur, cudaStream_t st) {
       std::fprintf(stderr, "[trace] %d %d %llu %llu %llu %llu %llu %llu %llu\n", g, t, r[0], r[1], r[2],
                    r[3], r[4], r[5], r[6]);
     }
-  for (int g = 0; g < 2; ++g) {
-    std::fprintf(stderr, "[chunks] %d", g);
-    for (int c = 0; c < 128; ++c) std::fprintf(stderr, " %llu", h[1024 + g * 128 + c]);
-    std::fprintf(stderr, "\n");
-  }
 }
 
 void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int64_t n,
@@ -237,7 +232,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   std::vector<std::pair<int, int64_t>> upd_info;
   const bool dbg_phase = std::getenv("RPC_DEBUG_PHASES") != nullptr;
   const bool dbg_trace = std::getenv("RPC_DEBUG_TRACE") != nullptr;
-  DBuf trace_buf(ctx, dbg_trace ? sizeof(unsigned long long) * (2 * 64 * 8 + 256) : 8);
+  DBuf trace_buf(ctx, dbg_trace ? sizeof(unsigned long long) * 2 * 64 * 8 : 8);
   DBuf phase_clk(ctx, dbg_phase ? sizeof(unsigned long long) * 8 * 4096 : 8);
   std::vector<double> upd_flops;
   double update_ms = 0.0, flops = 0.0, bytes = 0.0;

@@ -125,8 +125,7 @@ struct UpdateParams {
   int columns_only; double* cols_out; int64_t ld_out;
   // RPC_DEBUG_TIMING: per-CTA cycle counters per phase ([grid][8] u64), or null
   unsigned long long* phase_clk;
-  // RPC_DEBUG_TRACE: CTA 0 per-group phase clocks [G][64 tiles][8], then per-chunk clocks
-  // of tile 5 [G][128] (debug only)
+  // RPC_DEBUG_TRACE: CTA 0 per-group phase clocks [G][64 tiles][8] (debug only)
   unsigned long long* trace;
 };
 // Row-tile height used for m accepted columns (128 or 64), or -1 if m unsupported.

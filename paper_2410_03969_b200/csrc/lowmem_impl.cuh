@@ -93,10 +93,13 @@ __global__ void __launch_bounds__(256, MINB)
 
   // producer: chunk i = (tile i / nK, pivot chunk i % nK); independent of the tile, so
   // the ring runs ahead across tile boundaries.
-  int issued = 0;
-  auto pump = [&](int done_w0) {
-    if (gtid != 0) return;
-    while (issued < total && issued < done_w0 + S) {
+  // Round robin over the group's warps (lane 0 of warp w issues chunks w, w + NCW, ...),
+  // one chunk behind the consumer so the stage is already released: the TMA issue cost is
+  // spread over the warps instead of stalling one of them every chunk (update_impl.cuh).
+  int issued = warp;
+  auto pump = [&](int done) {
+    if (lane != 0) return;
+    while (issued < total && issued < done + (S > 2 ? S - 1 : S)) {
       const int c = issued % nK, s = issued % S;
       if (issued >= S) mbar_wait(&empty[s], ((issued / S) & 1) ^ 1);
       unsigned char* Bs = stages + s * STAGE + C::A_BYTES;
@@ -104,7 +107,7 @@ __global__ void __launch_bounds__(256, MINB)
       mbar_arrive_expect_tx(&full[s], C::B_BYTES + nD * 2048);
       tma_load_2d(Bs, &tmW, 16 * c, 0, &full[s]);
       for (int dc = 0; dc < nD; ++dc) tma_load_2d(XSs + dc * 2048, &tmXS, 16 * dc, 16 * c, &full[s]);
-      ++issued;
+      issued += NCW;
     }
   };
   pump(0);
@@ -368,7 +371,7 @@ __global__ void __launch_bounds__(256, MINB)
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       ++cons;
-      if (warp == 0) pump(cons);
+      pump(cons);
     }
 
     if (p.out_mode) {  // product mode: out = A(R, S) W^T (+ add terms)

@@ -181,13 +181,20 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
   if (tid == 0) s_go = (G == 1);
   __syncthreads();
 
-  // ---- producer (thread 0 of the group): issue chunk `issued` when its stage is free and, for
-  // phase-2 chunks of tile k, once that tile's G is parked (parked > k).
-  int issued = 0;      // meaningful in thread 0 only
+  // ---- producers: lane 0 of every warp of the group, round robin: warp w issues chunks
+  // w, w + NCW, ...; chunk i goes out once the issuing warp has consumed chunk i - S + 1
+  // (the stage's previous occupant, chunk i - S, was released a chunk earlier, so the
+  // empty-barrier wait rarely blocks) and, for phase-2 chunks of tile k, once that tile's
+  // G is parked (parked > k).  Spreading the TMA issue (~0.4k cycles per chunk) over the
+  // warps keeps it off any single warp's critical path.
+  // (the standalone K5, COLS, keeps one producer, thread 0, and the full ring lookahead:
+  // its tiles are two chunks long and measured faster that way)
+  constexpr int PSTEP = COLS ? 1 : NCW;
+  int issued = COLS ? 0 : warp;  // next chunk this producer issues
   int parked = 0;      // tiles whose G has been parked (CTA-uniform)
-  auto pump = [&](int done_w0) {
-    if (gtid != 0) return;
-    while (issued < total && issued < done_w0 + S) {
+  auto pump = [&](int done) {
+    if (COLS ? gtid != 0 : lane != 0) return;
+    while (issued < total && issued < done + (COLS ? S : S - 1)) {
       const int k = issued / T, c = issued - k * T;
       if (c >= nX + nFk && parked <= k) break;
       const int s = issued % S;
@@ -206,7 +213,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
         tma_load_2d(As, &tmG, kcur - koff + 16 * (c - nX - nFk), r0, &full[s]);
         tma_load_2d(Bs, &tmL, 16 * (c - nX - nFk), 0, &full[s]);
       }
-      ++issued;
+      issued += PSTEP;
     }
   };
   if (G > 1 && grp == 1) {  // offset group 1 so the two groups' non-DMMA phases interleave
@@ -312,6 +319,10 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       tclk = now;
     }
   };
+  // RPC_DEBUG_TRACE: CTA 0 per-group, per-tile phase clocks
+  auto trc = [&](int k, int ph) {
+    if (p.trace && blockIdx.x == 0 && gtid == 0 && k < 64) p.trace[(grp * 64 + k) * 8 + ph] = clock64();
+  };
   int cons = 0;  // chunks consumed by this warp so far (CTA-uniform in practice)
   auto consume = [&](auto&& body) {
     const int s = cons % S;
@@ -321,13 +332,14 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     ++cons;
-    if (warp == 0) pump(cons);
+    if (!COLS || warp == 0) pump(cons);
   };
 
 #pragma unroll 1
   for (int k = 0; k < my_tiles; ++k) {
     const int tile = vb + k * vgrid;
     const int64_t tile_row0 = (int64_t)tile * BM;
+    trc(k, 0);
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr)
 #pragma unroll
@@ -340,6 +352,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       else consume([&](uint32_t so) { dist_stage(so); });
     }
     mark(0);
+    trc(k, 1);
     if (p.phase_clk) {  // debug: wait for every outstanding DMMA before timing the transform
       double s = 0.0;
 #pragma unroll
@@ -429,6 +442,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     }
     if (G > 1 && grp == 0 && k == 0 && gtid == 0) s_go = 1;
     mark(1);
+    trc(k, 2);
     if (COLS || p.columns_only) {  // standalone K5: A(R, S) -> column-major output
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) {
@@ -464,14 +478,16 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     fence_proxy_async_global();
     gsync();
     parked = k + 1;
-    if (warp == 0) pump(cons);
+    if (!COLS || warp == 0) pump(cons);
     mark(2);
+    trc(k, 3);
     // ---- phase 1b: acc = F(R,:) B'^T with B' = -L^{-1} F(S,:)  (K = kcur) -------------
     //   G L^{-T} = (A - F F_S^T) L^{-T} = A L^{-T} + F (-L^{-1} F_S)^T
 #pragma unroll 1
     for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0); });
 
     mark(3);
+    trc(k, 4);
     // ---- phase 2: acc += A L^{-T}  (K = m, A streamed back from F) --------------------
 #pragma unroll 1
     for (int j = 0; j < nL; ++j) {
@@ -482,6 +498,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     }
 
     mark(4);
+    trc(k, 5);
     // ---- epilogue ------------------------------------------------------------------
     double rs[2] = {0.0, 0.0};
 #pragma unroll
@@ -525,6 +542,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       p.tile_g2[tile] = s2;
     }
     mark(5);
+    trc(k, 6);
   }
 }
 

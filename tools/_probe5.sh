@@ -5,3 +5,5 @@ python tools/one_factor.py C2 3 >> $O/timing.txt 2>&1
 python tools/one_factor.py C3 3 >> $O/timing.txt 2>&1
 python bench.py --no-cpu --no-e2e --steps 3 --warmup 3 > $O/bench.json 2> $O/bench.err
 echo done
+python bench.py --variant lowmem --no-cpu --no-e2e --steps 3 --warmup 3 > gpurun_out/probe5/lowmem.json 2> gpurun_out/probe5/lowmem.err
+python tools/matvec_probe.py > gpurun_out/probe5/matvec.txt 2>&1
