@@ -272,14 +272,21 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     for (int s = 0; s < 4; ++s)
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) a[s][fr] = *reinterpret_cast<const double*>(Aw + fr * 1024 + foff[s]);
+    // fragment pairs (q, q+1), skipped whole below q_lo rounded down to even (at most one
+    // all-zero fragment computed): four independent accumulators per branch block
 #pragma unroll
-    for (int q = 0; q < NFW; ++q) {
-      if (q < q_lo) continue;
+    for (int q = 0; q < NFW; q += 2) {
+      if (q + 1 < q_lo) continue;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+        const double bv0 = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+        double bv1 = 0.0;
+        if (q + 1 < NFW) bv1 = *reinterpret_cast<const double*>(Bw + (q + 1) * 1024 + foff[s]);
 #pragma unroll
-        for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[s][fr], bv);
+        for (int fr = 0; fr < 2; ++fr) {
+          dmma884(acc[fr][q][0], acc[fr][q][1], a[s][fr], bv0);
+          if (q + 1 < NFW) dmma884(acc[fr][q + 1][0], acc[fr][q + 1][1], a[s][fr], bv1);
+        }
       }
     }
   };
