@@ -105,6 +105,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Non-blocking probe of a phase (no suspend): lets a consumer check the next stage's
+// barrier while its DMMAs for the current stage are still in flight.
+__device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+      "selp.u32 %0, 1, 0, p;\n"
+      "}\n"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
 // The retry loop is plain C++ so the compiler sees the branch and reconverges the
 // warp before any following .aligned instruction (mma.sync, shfl.sync).
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {

@@ -331,11 +331,15 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     if (p.trace && blockIdx.x == 0 && gtid == 0 && k < 64) p.trace[(grp * 64 + k) * 8 + ph] = clock64();
   };
   int cons = 0;  // chunks consumed by this warp so far (CTA-uniform in practice)
+  // next_ready: the next stage's data was seen complete during the previous body (probed
+  // with a non-blocking test right after that body's loads were issued), so its wait is skipped
+  bool next_ready = false;
   auto consume = [&](auto&& body) {
     const int s = cons % S;
-    mbar_wait(&full[s], (cons / S) & 1);
+    if (!next_ready) mbar_wait(&full[s], (cons / S) & 1);
     __syncwarp();
     body((uint32_t)(s * C::STAGE));
+    next_ready = mbar_test_wait(&full[(cons + 1) % S], ((cons + 1) / S) & 1);
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     ++cons;
