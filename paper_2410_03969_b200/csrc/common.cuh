@@ -146,6 +146,9 @@ __device__ __forceinline__ void fence_proxy_async_global() {
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
 }
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("bar.arrive %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 // ---- reductions -----------------------------------------------------------
 __device__ __forceinline__ double warp_sum_xor(double v) {

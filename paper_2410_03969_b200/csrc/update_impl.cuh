@@ -530,23 +530,41 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
         }
       rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 1);
       rs[fr] += __shfl_xor_sync(0xffffffffu, rs[fr], 2);
-      if (t == 0) s_rown[wc * BM + arow[fr]] = rs[fr];
-    }
-    gsync();
-    if (gtid < BM) {
-      const int64_t grow = tile_row0 + gtid;
-      double s2 = 0.0;
-#pragma unroll
-      for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + gtid]);
-      if (grow < p.n_loc) {
-        const double un = __dsub_rn(p.u[grow], s2);
-        p.u[grow] = un < 0.0 ? 0.0 : un;
-      } else {
-        s2 = 0.0;
+      if (WC == 1) {  // the quad's t == 0 lane holds the whole row: update u directly
+        if (t == 0) {
+          double s2 = rs[fr];
+          if (rin) {
+            const double un = __dsub_rn(p.u[grow], s2);
+            p.u[grow] = un < 0.0 ? 0.0 : un;
+          } else {
+            s2 = 0.0;
+          }
+          s_rowg2[arow[fr]] = s2;
+        }
+      } else if (t == 0) {
+        s_rown[wc * BM + arow[fr]] = rs[fr];
       }
-      s_rowg2[gtid] = s2;
     }
-    gsync();
+    if (WC > 1) {
+      gsync();
+      if (gtid < BM) {
+        const int64_t grow = tile_row0 + gtid;
+        double s2 = 0.0;
+#pragma unroll
+        for (int w = 0; w < WC; ++w) s2 = __dadd_rn(s2, s_rown[w * BM + gtid]);
+        if (grow < p.n_loc) {
+          const double un = __dsub_rn(p.u[grow], s2);
+          p.u[grow] = un < 0.0 ? 0.0 : un;
+        } else {
+          s2 = 0.0;
+        }
+        s_rowg2[gtid] = s2;
+      }
+    }
+    // only the summing warp waits for the row partials; the others go on to the next tile
+    // (s_rowg2 is next written after the next tile's park barrier)
+    if (warp == 0) named_bar_sync(1 + grp, GT);
+    else named_bar_arrive(1 + grp, GT);
     if (gtid == 0) {
       double s2 = 0.0;
       for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
