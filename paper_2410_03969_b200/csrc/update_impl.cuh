@@ -237,7 +237,9 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 #pragma unroll
   for (int s = 0; s < 4; ++s) foff[s] = swz_off(pg, 4 * s + t);
   const uint32_t a_base = (uint32_t)(wr * 16) * 128u;
-  const uint32_t b_base = (uint32_t)(wc * NFW) * 1024u;
+  // Two warp columns own interleaved fragments (global fragment q * WC + wc), so the skipped
+  // upper triangle of L^{-T} in phase 2 is shared evenly between them.
+  const uint32_t b_base = (uint32_t)wc * 1024u;
 
   double acc[2][NFW][2];
 
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
         if (q < q_lo) continue;
-        const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+        const double bv = *reinterpret_cast<const double*>(Bw + q * WC * 1024 + foff[s]);
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[fr], bv);
       }
@@ -279,9 +281,9 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       if (q + 1 < q_lo) continue;
 #pragma unroll
       for (int s = 0; s < 4; ++s) {
-        const double bv0 = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+        const double bv0 = *reinterpret_cast<const double*>(Bw + q * WC * 1024 + foff[s]);
         double bv1 = 0.0;
-        if (q + 1 < NFW) bv1 = *reinterpret_cast<const double*>(Bw + (q + 1) * 1024 + foff[s]);
+        if (q + 1 < NFW) bv1 = *reinterpret_cast<const double*>(Bw + (q + 1) * WC * 1024 + foff[s]);
 #pragma unroll
         for (int fr = 0; fr < 2; ++fr) {
           dmma884(acc[fr][q][0], acc[fr][q][1], a[s][fr], bv0);
@@ -302,7 +304,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       for (int fr = 0; fr < 2; ++fr) xr[fr] = *reinterpret_cast<const double*>(As + swz_off(arow[fr], j));
 #pragma unroll
       for (int q = 0; q < NFW; ++q) {
-        const int Q = wc * NFW + q;
+        const int Q = q * WC + wc;
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
           const double xs = *reinterpret_cast<const double*>(Bs + swz_off(8 * Q + perm8(2 * t + v), j));
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
         for (int h = 0; h < 2; ++h)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            const int col = 8 * (wc * NFW + it + h) + 2 * t + v;
+            const int col = 8 * ((it + h) * WC + wc) + 2 * t + v;
             const double sqc = s_sqnS[col], idc = s_idS[col];
 #pragma unroll
             for (int fr = 0; fr < 2; ++fr) xform(acc[fr][h][v], col, fr, sqc, idc);
@@ -433,7 +435,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       if (NFW & 1) {  // last fragment (now at position 0), then rotate by one
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int col = 8 * (wc * NFW + NFW - 1) + 2 * t + v;
+          const int col = 8 * ((NFW - 1) * WC + wc) + 2 * t + v;
           const double sqc = s_sqnS[col], idc = s_idS[col];
 #pragma unroll
           for (int fr = 0; fr < 2; ++fr) xform(acc[fr][0][v], col, fr, sqc, idc);
@@ -463,7 +465,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
         for (int q = 0; q < NFW; ++q)
 #pragma unroll
           for (int v = 0; v < 2; ++v) {
-            const int col = 8 * (wc * NFW + q) + 2 * t + v;
+            const int col = 8 * (q * WC + wc) + 2 * t + v;
             if (col < m) p.cols_out[(int64_t)col * p.ld_out + grow] = -acc[fr][q][v];
           }
       }
@@ -481,7 +483,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       for (int q = 0; q < NFW; ++q)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int col = 8 * (wc * NFW + q) + 2 * t + v;
+          const int col = 8 * (q * WC + wc) + 2 * t + v;
           if (col < m && grow < p.n_loc) frow[col] = -acc[fr][q][v];
           acc[fr][q][v] = 0.0;
         }
@@ -504,7 +506,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     for (int j = 0; j < nL; ++j) {
       // chunk j covers A columns [16j - koff, 16j + 16 - koff); L^{-T}[k][n] = 0 for n < k,
       // so fragments whose 8 columns all lie below 16j - koff contribute nothing.
-      const int q_lo = max(0, (16 * j - koff) / 8 - wc * NFW);
+      const int q_lo = max(0, ((16 * j - koff) / 8 - wc + WC - 1) / WC);
       consume([&](uint32_t so) { mma_stage_tri(so, q_lo); });
     }
 
@@ -521,7 +523,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       for (int q = 0; q < NFW; ++q)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int col = 8 * (wc * NFW + q) + 2 * t + v;
+          const int col = 8 * (q * WC + wc) + 2 * t + v;
           if (col < m && rin) {
             const double val = acc[fr][q][v];
             frow[col] = val;
