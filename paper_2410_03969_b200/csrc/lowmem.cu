@@ -29,53 +29,69 @@ int launch_lowmem(const LowmemParams& p, cudaStream_t st) {
   return -1;
 }
 
-// 64 x 64 output tile per CTA, 16-deep K slices, 4 x 4 outputs per thread; every output
-// accumulates its K terms in ascending order (deterministic).
+// C = alpha op(A) op(B) (+ beta C) for the low-memory path's small products (b x k x k,
+// m x k x k).  32 x 32 output tiles (enough CTAs for M ~ 120 rows), 32-wide k chunks staged
+// in shared memory with the next chunk prefetched into registers.  Each output is one
+// ascending-k FMA chain, the same operation order as before the retiling (bitwise equal).
 __global__ void __launch_bounds__(256) gemm_kernel(int M, int N, int K, double alpha,
                                                    const double* __restrict__ A, int64_t lda, int ta,
                                                    const double* __restrict__ B, int64_t ldb, int tb,
                                                    double beta, double* __restrict__ Cm, int64_t ldc) {
-  __shared__ double As[16][65];  // [k][i]
-  __shared__ double Bs[16][65];  // [k][j]
+  constexpr int T = 32, KC = 32;
+  __shared__ double As[KC][T + 1];  // [k][i]
+  __shared__ double Bs[KC][T + 1];  // [k][j]
   const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-  const int i0 = blockIdx.y * 64, j0 = blockIdx.x * 64;
-  double acc[4][4];
+  const int i0 = blockIdx.y * T, j0 = blockIdx.x * T;
+  double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  double ra[4], rb[4];
+  auto fetch = [&](int k0) {
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
-#pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = 0.0;
-  for (int k0 = 0; k0 < K; k0 += 16) {
-    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+    for (int r = 0; r < 4; ++r) {
+      const int e = threadIdx.x + 256 * r;
       int kk, ii;
-      if (ta) { ii = e & 63; kk = e >> 6; } else { kk = e & 15; ii = e >> 4; }
+      if (ta) { ii = e & 31; kk = e >> 5; } else { kk = e & 31; ii = e >> 5; }
       const int i = i0 + ii, k = k0 + kk;
-      As[kk][ii] = (i < M && k < K) ? (ta ? A[(int64_t)k * lda + i] : A[(int64_t)i * lda + k]) : 0.0;
+      ra[r] = (i < M && k < K) ? (ta ? A[(int64_t)k * lda + i] : A[(int64_t)i * lda + k]) : 0.0;
       int jj;
-      if (tb) { kk = e & 15; jj = e >> 4; } else { jj = e & 63; kk = e >> 6; }
+      if (tb) { kk = e & 31; jj = e >> 5; } else { jj = e & 31; kk = e >> 5; }
       const int j = j0 + jj, k2 = k0 + kk;
-      Bs[kk][jj] = (j < N && k2 < K) ? (tb ? B[(int64_t)j * ldb + k2] : B[(int64_t)k2 * ldb + j]) : 0.0;
+      rb[r] = (j < N && k2 < K) ? (tb ? B[(int64_t)j * ldb + k2] : B[(int64_t)k2 * ldb + j]) : 0.0;
     }
+  };
+  auto stash = [&]() {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = threadIdx.x + 256 * r;
+      int kk, ii;
+      if (ta) { ii = e & 31; kk = e >> 5; } else { kk = e & 31; ii = e >> 5; }
+      As[kk][ii] = ra[r];
+      int jj;
+      if (tb) { kk = e & 31; jj = e >> 5; } else { jj = e & 31; kk = e >> 5; }
+      Bs[kk][jj] = rb[r];
+    }
+  };
+  fetch(0);
+  for (int k0 = 0; k0 < K; k0 += KC) {
+    stash();
     __syncthreads();
+    if (k0 + KC < K) fetch(k0 + KC);  // in flight during this chunk's FMAs
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a[4], b[4];
-#pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = As[kk][ty + 16 * r];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) b[c] = Bs[kk][tx + 16 * c];
-#pragma unroll
-      for (int r = 0; r < 4; ++r)
-#pragma unroll
-        for (int c = 0; c < 4; ++c) acc[r][c] = fma(a[r], b[c], acc[r][c]);
+    for (int kk = 0; kk < KC; ++kk) {
+      const double a0 = As[kk][ty], a1 = As[kk][ty + 16];
+      const double b0 = Bs[kk][tx], b1 = Bs[kk][tx + 16];
+      acc[0][0] = fma(a0, b0, acc[0][0]);
+      acc[0][1] = fma(a0, b1, acc[0][1]);
+      acc[1][0] = fma(a1, b0, acc[1][0]);
+      acc[1][1] = fma(a1, b1, acc[1][1]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int r = 0; r < 4; ++r) {
+  for (int r = 0; r < 2; ++r) {
     const int i = i0 + ty + 16 * r;
     if (i >= M) continue;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       const int j = j0 + tx + 16 * c;
       if (j >= N) continue;
       double* o = Cm + (int64_t)i * ldc + j;
@@ -88,7 +104,7 @@ void launch_gemm(int M, int N, int K, double alpha, const double* A, int64_t lda
                  const double* B, int64_t ldb, int tb, double beta, double* C, int64_t ldc,
                  cudaStream_t st) {
   if (M <= 0 || N <= 0) return;
-  dim3 grid((unsigned)((N + 63) / 64), (unsigned)((M + 63) / 64));
+  dim3 grid((unsigned)((N + 31) / 32), (unsigned)((M + 31) / 32));
   gemm_kernel<<<grid, 256, 0, st>>>(M, N, K, alpha, A, lda, ta, B, ldb, tb, beta, C, ldc);
 }
 
