@@ -96,13 +96,21 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
       if (e == (last & 15)) v = s[e];
     totals[c] = __dadd_rn(base, v);
   }
-  if (tile_g2 && threadIdx.x == kScanThreads - 1) {
+  if (tile_g2) {
+    // previous update's per-tile ||G||^2 partials of this chunk: loaded by 64 threads in
+    // parallel, then summed in tile order by one thread (a dependent chain of global loads
+    // was most of this kernel's time)
     constexpr int kTilesPerChunk = kChunk / 64;
-    double g = 0.0;
+    __shared__ double s_tg[kTilesPerChunk];
     const int t0 = c * kTilesPerChunk;
     const int t1 = min(n_tiles, t0 + kTilesPerChunk);
-    for (int t = t0; t < t1; ++t) g = __dadd_rn(g, tile_g2[t]);
-    chunk_g2[c] = g;
+    if (threadIdx.x < kTilesPerChunk) s_tg[threadIdx.x] = t0 + (int)threadIdx.x < t1 ? tile_g2[t0 + threadIdx.x] : 0.0;
+    __syncthreads();
+    if (threadIdx.x == kScanThreads - 1) {
+      double g = 0.0;
+      for (int t = 0; t < t1 - t0; ++t) g = __dadd_rn(g, s_tg[t]);
+      chunk_g2[c] = g;
+    }
   }
   if (fp.counter) {
     // single shard: the last CTA to finish runs the serial chunk-offset chain of
