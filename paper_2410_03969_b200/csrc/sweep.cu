@@ -217,13 +217,22 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     const int m0 = s_m;
     if (nacc > 0) {
       // ---- 2. panel: l_c(p) for rows p >= i1, accepted c in order ----
+      // (the row's l values stay in registers and both loops are unrolled to the block
+      // size, so the shared-memory operand loads issue ahead of the subtraction chain; the
+      // operation sequence per entry is unchanged)
       for (int p = i1 + tid; p < b; p += kSweepThreads) {
-        for (int k = 0; k < nacc; ++k) {
+        double lrow[kSweepBlock];
+        const int64_t bp = tri(p);
+#pragma unroll
+        for (int k = 0; k < kSweepBlock; ++k) {
+          if (k >= nacc) break;
           const int c = s_acc[k];
-          double t = hp[tri(p) + c];
+          double t = hp[bp + c];
+#pragma unroll
           for (int k2 = 0; k2 < k; ++k2)
-            t = __dsub_rn(t, __dmul_rn(lpan[k2 * b + p], lblk[k2 * kSweepBlock + (c - i0)]));
-          lpan[k * b + p] = __ddiv_rn(t, s_root[k]);
+            t = __dsub_rn(t, __dmul_rn(lrow[k2], lblk[k2 * kSweepBlock + (c - i0)]));
+          lrow[k] = __ddiv_rn(t, s_root[k]);
+          lpan[k * b + p] = lrow[k];
         }
       }
       __syncthreads();
@@ -237,9 +246,16 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
       // ---- 3. trailing update, acceptance order per entry ----
       for (int p = i1 + warp; p < b; p += nwarps) {
         const int64_t base = tri(p);
+        double lp[kSweepBlock];  // row p's l values (the same for the whole warp)
+#pragma unroll
+        for (int k = 0; k < kSweepBlock; ++k) lp[k] = k < nacc ? lpan[k * b + p] : 0.0;
         for (int q = i1 + lane; q <= p; q += 32) {
           double h = hp[base + q];
-          for (int k = 0; k < nacc; ++k) h = __dsub_rn(h, __dmul_rn(lpan[k * b + p], lpan[k * b + q]));
+#pragma unroll
+          for (int k = 0; k < kSweepBlock; ++k) {
+            if (k >= nacc) break;
+            h = __dsub_rn(h, __dmul_rn(lp[k], lpan[k * b + q]));
+          }
           hp[base + q] = h;
         }
       }
