@@ -246,16 +246,9 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
       // ---- 3. trailing update, acceptance order per entry ----
       for (int p = i1 + warp; p < b; p += nwarps) {
         const int64_t base = tri(p);
-        double lp[kSweepBlock];  // row p's l values (the same for the whole warp)
-#pragma unroll
-        for (int k = 0; k < kSweepBlock; ++k) lp[k] = k < nacc ? lpan[k * b + p] : 0.0;
         for (int q = i1 + lane; q <= p; q += 32) {
           double h = hp[base + q];
-#pragma unroll
-          for (int k = 0; k < kSweepBlock; ++k) {
-            if (k >= nacc) break;
-            h = __dsub_rn(h, __dmul_rn(lp[k], lpan[k * b + q]));
-          }
+          for (int k = 0; k < nacc; ++k) h = __dsub_rn(h, __dmul_rn(lpan[k * b + p], lpan[k * b + q]));
           hp[base + q] = h;
         }
       }
