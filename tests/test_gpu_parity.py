@@ -353,3 +353,20 @@ def test_matern_parity(ctx, kernel, dist):  # KernelKind::Matern32/52, kernels.h
     x = wl.gen_c2(6000, 8, 3)
     g, r, o = run_both(x, kernel, 2.5, k=250, b=60, ctx=ctx, dist=dist)
     assert_parity(g, r, o)
+
+
+def test_nccl_context_single_rank():
+    """rpc_create_nccl (the multi-GPU context) at world size 1 on this box: the NCCL
+    communicator initialises and the factorization is bitwise the plain context's."""
+    x = wl.gen_c1(6000, 8, 0)
+    spec = api.KernelSpec("gaussian", math.sqrt(8.0))
+    cfg = api.RunConfig.until_rank(60, 16, 5)
+    plain = api.Context(0)
+    ref = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, plain)
+    f_ref = ref.factor.copy()
+    plain.close()
+    nc = api.Context(0, nccl_id=api.nccl_unique_id(), nranks=1, rank=0)
+    got = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, nc)
+    assert np.array_equal(got.pivots, ref.pivots)
+    assert np.array_equal(got.factor, f_ref)
+    nc.close()
