@@ -564,9 +564,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       }
     }
     // only the summing warp waits for the row partials; the others go on to the next tile
-    // (s_rowg2 is next written after the next tile's park barrier)
-    if (warp == 0) named_bar_sync(1 + grp, GT);
-    else named_bar_arrive(1 + grp, GT);
+    // (s_rowg2 is next written after the next tile's park barrier).  A barrier id of its own
+    // (not gsync's): the early warps' arrivals can then never be counted toward a later
+    // gsync, and the next tile's epilogue arrivals come after warp 0 passed that tile's park.
+    if (warp == 0) named_bar_sync(1 + G + grp, GT);
+    else named_bar_arrive(1 + G + grp, GT);
     if (gtid == 0) {
       double s2 = 0.0;
       for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
