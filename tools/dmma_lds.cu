@@ -59,6 +59,20 @@ __global__ void __launch_bounds__(256, 1) kern(double* out, int iters) {
           for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[fr], bv);
         }
       }
+    } else if (V == 5) {
+      // fr-outer: consecutive DMMAs share the A register (operand reuse), all 15 B values live
+#pragma unroll
+      for (int s = 0; s < 4; ++s) {
+        double a[2], bq[NFW];
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr) a[fr] = *reinterpret_cast<const double*>(Aw + fr * 1024 + foff[s]);
+#pragma unroll
+        for (int q = 0; q < NFW; ++q) bq[q] = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+          for (int q = 0; q < NFW; ++q) dmma884(acc[fr][q][0], acc[fr][q][1], a[fr], bq[q]);
+      }
     } else if (V == 2) {
       double a[4][2];
 #pragma unroll
@@ -136,6 +150,7 @@ int main() {
   };
   for (int w : {4, 8}) {
     run(kern<1>, "V1", w);
+    run(kern<5>, "V5", w);
     run(kern<2>, "V2", w);
     run(kern<3>, "V3", w);
     run(kern<4>, "V4", w);
