@@ -61,12 +61,11 @@ struct UCfg {
 // exp(x) = 2^n * T[j] * (1 + expm1(r)), T[j] = 2^(j/64) from a shared-memory table,
 // expm1 by a degree-5 polynomial (truncation < 4e-17 relative).  ~1 ulp; about half
 // the FP64 work and dependency depth of a plain Cody-Waite + degree-13 Taylor.
-// Scaling by 2^n in two exact steps keeps subnormal results (x >= -745.5).
 __constant__ double kExpC[8] = {92.332482616893656,        // 64 / ln 2
                                 -1.0830424696249145e-02,   // -ln2/64 (high)
                                 -3.6235106466348430e-19,   // -ln2/64 (low)
                                 8.3333333333333333e-03, 4.1666666666666667e-02,
-                                1.6666666666666667e-01, 0.5, -745.5};
+                                1.6666666666666667e-01, 0.5, 0.0};
 
 // No FP64<->int conversion instructions (slow paths on this part): k = rint(x 64/ln2)
 // comes out of the low mantissa bits of x * 64/ln2 + 1.5 * 2^52 (one rounding, ties
