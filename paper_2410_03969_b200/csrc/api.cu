@@ -527,6 +527,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.X = s.X.as<double>();
         up.dpad = dpad;
         up.dchunks = (int)(dpad / 16);
+        up.d = (int)d;
         up.sqn = s.sqn.as<double>();
         up.F = s.F.as<double>();
         up.ldf = ldf;
@@ -1196,6 +1197,7 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
               up.X = X.as<double>();
               up.dpad = dpad;
               up.dchunks = (int)(dpad / 16);
+        up.d = (int)d;
               up.sqn = sqn.as<double>();
               up.F = X.as<double>();
               up.ldf = dpad;
@@ -1293,6 +1295,7 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.X = X.as<double>();
       up.dpad = dpad;
       up.dchunks = (int)(dpad / 16);
+        up.d = (int)d;
       up.sqn = sqn.as<double>();
       up.F = X.as<double>();
       up.ldf = dpad;

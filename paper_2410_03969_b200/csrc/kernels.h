@@ -109,6 +109,7 @@ void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb,
 // ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
 struct UpdateParams {
   const double* X; int64_t dpad; int dchunks;   // X shard [n_loc][dpad]
+  int d;                                        // true dimension (distance loops skip the padding)
   const double* sqn;                            // ||x||^2 [n_loc]
   double* F; int64_t ldf; int kcur;             // F shard [n_loc][ldf]
   double* u;                                    // residual diagonal [n_loc]

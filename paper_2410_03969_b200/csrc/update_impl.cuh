@@ -292,12 +292,15 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     }
   };
 
-  auto dist_stage = [&](uint32_t st_off) {
+  // c: the 16-coordinate chunk; its zero-padded coordinates (>= d) are skipped (they would
+  // add exact zeros)
+  auto dist_stage = [&](uint32_t st_off, int c) {
     const unsigned char* As = stages + st_off;
     const unsigned char* Bs = As + C::A_BYTES;
     const bool l1 = p.kind == kL1;
+    const int jn = min(16, p.d - 16 * c);
 #pragma unroll 1
-    for (int j = 0; j < 16; ++j) {
+    for (int j = 0; j < jn; ++j) {
       double xr[2];
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) xr[fr] = *reinterpret_cast<const double*>(As + swz_off(arow[fr], j));
@@ -361,7 +364,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 #pragma unroll 1
     for (int c = 0; c < nX; ++c) {
       if constexpr (GRAM) consume([&](uint32_t so) { mma_stage(so, 0); });
-      else consume([&](uint32_t so) { dist_stage(so); });
+      else consume([&](uint32_t so) { dist_stage(so, c); });
     }
     mark(0);
     trc(k, 1);
