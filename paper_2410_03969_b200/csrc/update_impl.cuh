@@ -244,11 +244,14 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 
   // q_lo: first fragment that can be non-zero (phase 2 skips the zero upper triangle
   // of L^{-T}; phase 1 passes 0).
-  auto mma_stage = [&](uint32_t st_off, int q_lo) {
+  // ks: k steps of the chunk that hold data (the Gram chunks skip steps made only of the
+  // zero padding of X beyond d; the residual GEMM always passes 4)
+  auto mma_stage = [&](uint32_t st_off, int q_lo, int ks) {
     const unsigned char* Aw = stages + st_off + a_base;
     const unsigned char* Bw = stages + st_off + C::A_BYTES + b_base;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
+      if (s >= ks) break;
       double a[2];
 #pragma unroll
       for (int fr = 0; fr < 2; ++fr) a[fr] = *reinterpret_cast<const double*>(Aw + fr * 1024 + foff[s]);
@@ -363,7 +366,10 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     // ---- phase 1a: kernel-column distances / Gram products (X tiles) -------------
 #pragma unroll 1
     for (int c = 0; c < nX; ++c) {
-      if constexpr (GRAM) consume([&](uint32_t so) { mma_stage(so, 0); });
+      if constexpr (GRAM) {
+        const int ks = min(4, (min(16, p.d - 16 * c) + 3) / 4);
+        consume([&](uint32_t so) { mma_stage(so, 0, ks); });
+      }
       else consume([&](uint32_t so) { dist_stage(so, c); });
     }
     mark(0);
@@ -499,7 +505,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     // ---- phase 1b: acc = F(R,:) B'^T with B' = -L^{-1} F(S,:)  (K = kcur) -------------
     //   G L^{-T} = (A - F F_S^T) L^{-T} = A L^{-T} + F (-L^{-1} F_S)^T
 #pragma unroll 1
-    for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0); });
+    for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0, 4); });
 
     mark(3);
     trc(k, 4);
