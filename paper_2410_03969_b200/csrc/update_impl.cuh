@@ -505,7 +505,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     // ---- phase 1b: acc = F(R,:) B'^T with B' = -L^{-1} F(S,:)  (K = kcur) -------------
     //   G L^{-T} = (A - F F_S^T) L^{-T} = A L^{-T} + F (-L^{-1} F_S)^T
 #pragma unroll 1
-    for (int c = 0; c < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0, 4); });
+    for (int c = 0; c + 1 < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0, 4); });
+    if (nFk > 0) {  // last chunk: only the k steps below kcur hold data (TMA zero fill above)
+      const int ks = (kcur - 16 * (nFk - 1) + 3) / 4;
+      consume([&](uint32_t so) { mma_stage(so, 0, ks); });
+    }
 
     mark(3);
     trc(k, 4);
