@@ -17,10 +17,10 @@
 // and l1 distances run on the FP64 CUDA cores from the same staged X tiles in
 // ascending coordinate order (bit-identical distances to the reference's sums).
 //
-// Execution: persistent CTAs (one per SM) of 8 warps walk row tiles; thread 0
-// streams [rows][16] fp64 tiles with 2D TMA (cp.async.bulk.tensor, 128B swizzle)
-// into an S-stage ring guarded by full/empty mbarriers, running ahead across tile
-// boundaries (the next tile's first tiles load during this tile's epilogue); all
+// Execution: persistent CTAs of 8 warps (two ping-pong groups of 4 for m <= 128) walk row
+// tiles; [rows][16] fp64 tiles are streamed with 2D TMA (cp.async.bulk.tensor, 128B
+// swizzle) into an S-stage ring per group guarded by full/empty mbarriers, issued round
+// robin by lane 0 of the group's warps and running ahead across tile boundaries; all
 // warps run mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4).  Operand rows are permuted inside 8-row
 // groups (perm8, common.cuh) so every fragment load is bank-conflict free.
 #include <cuda.h>
