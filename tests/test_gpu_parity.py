@@ -370,3 +370,20 @@ def test_nccl_context_single_rank():
     assert np.array_equal(got.pivots, ref.pivots)
     assert np.array_equal(got.factor, f_ref)
     nc.close()
+
+
+# Dimensions around the 16-coordinate chunk and 4-wide k-step boundaries: the update
+# kernel skips the zero padding of X (Gram k steps with no data, distance coordinates
+# >= d), so every residue of d mod 16 and mod 4 must still give the reference's result.
+@pytest.mark.parametrize("d", [1, 3, 4, 5, 15, 16, 17, 20, 31, 33, 47, 48])
+@pytest.mark.parametrize("kernel,dist", [("gaussian", "gram"), ("gaussian", "direct"),
+                                         ("l1laplace", None)])
+def test_dimension_padding_boundaries(ctx, d, kernel, dist):
+    rng = np.random.default_rng(100 + d)
+    x = rng.standard_normal((3000, d))
+    sigma = math.sqrt(d) if kernel == "gaussian" else float(d)
+    # FixedRounds keeps the run bounded and, for the smooth kernel in very low d, inside the
+    # kernel's numerical rank (past it both implementations factor rounding noise)
+    rounds = 1 if (kernel == "gaussian" and d <= 3) else 3
+    g, r, o = run_both(x, kernel, sigma, b=16, seed=d, rounds=rounds, ctx=ctx, dist=dist)
+    assert_parity(g, r, o)
