@@ -7,6 +7,7 @@ golden fixtures): accelerated (fast and replay scan), low-memory and block varia
 Bars as in test_gpu_parity.py / test_lowmem.py / test_baselines.py.
 """
 import math
+import os
 
 import numpy as np
 import pytest
@@ -45,6 +46,8 @@ def draw_case(i):
 # well-posed regime where the 1e-10 factor bar is meaningful; the pivots stay identical
 # either way.
 STOP_TOL = 1e-4
+# RPC_FUZZ_EXTRA=n adds n more draws per variant (a longer sweep than the default suite)
+EXTRA = int(os.environ.get("RPC_FUZZ_EXTRA", "0"))
 
 
 def cfg_of(api, c):
@@ -71,7 +74,7 @@ def ctx():
     c.close()
 
 
-@pytest.mark.parametrize("i", range(24))
+@pytest.mark.parametrize("i", list(range(24)) + list(range(1000, 1000 + EXTRA)))
 def test_fuzz_accelerated(ctx, i):
     from paper_2410_03969_b200 import api
     c = draw_case(i)
@@ -91,7 +94,7 @@ def test_fuzz_accelerated(ctx, i):
         assert np.max(np.abs(g.residual_diag - r.residual_diag)) <= 1e-10
 
 
-@pytest.mark.parametrize("i", range(24, 36))
+@pytest.mark.parametrize("i", list(range(24, 36)) + list(range(2000, 2000 + EXTRA)))
 def test_fuzz_lowmem(ctx, i):
     from paper_2410_03969_b200 import api
     c = draw_case(i)
@@ -106,7 +109,7 @@ def test_fuzz_lowmem(ctx, i):
     assert np.max(np.abs(g.residual_diag - r.residual_diag)) <= 1e-8
 
 
-@pytest.mark.parametrize("i", range(36, 48))
+@pytest.mark.parametrize("i", list(range(36, 48)) + list(range(3000, 3000 + EXTRA)))
 def test_fuzz_block(ctx, i):
     from paper_2410_03969_b200 import api
     c = draw_case(i)
