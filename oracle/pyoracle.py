@@ -13,6 +13,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import subprocess
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -105,6 +106,10 @@ def lib() -> C.CDLL:
         L.rpo_relative_trace_error.argtypes = [C.POINTER(_Oracle), C.c_void_p, C.c_int64,
                                                C.c_int64]
         L.rpo_last_error.restype = C.c_char_p
+        L.rpo_free.argtypes = [C.c_void_p]
+        L.rpo_margins_reset.argtypes = [C.c_int]
+        L.rpo_margins_get.argtypes = [C.POINTER(C.c_double), C.POINTER(C.c_double),
+                                      C.POINTER(C.c_int64), C.POINTER(C.c_int64)]
         _LIB = L
     return _LIB
 
@@ -215,11 +220,23 @@ class Result:
         return len(self.pivots)
 
 
-def _unpack(res) -> Result:
+def _adopt_buffer(ptr, count: int) -> np.ndarray:
+    """A numpy view of a C-allocated double buffer that frees it when the last view goes
+    (used to keep a multi-GB oracle factor without a second copy)."""
+    addr = C.cast(ptr, C.c_void_p).value
+    holder = (C.c_double * count).from_address(addr)
+    weakref.finalize(holder, lib().rpo_free, addr)
+    return np.ctypeslib.as_array(holder)
+
+
+def _unpack(res, copy_factor: bool = True) -> Result:
     try:
         n, k, b, nr = res.n, res.rank, res.block_size, res.n_rounds
         if not res.factor:
             factor = None  # LowMemResult
+        elif k and not copy_factor:
+            factor = _adopt_buffer(res.factor, k * n).reshape(n, k, order="F")
+            res.factor = C.POINTER(C.c_double)()  # ownership moved to the view
         else:
             factor = np.ctypeslib.as_array(res.factor, shape=(k * n,)).reshape(n, k, order="F").copy() \
                 if k else np.zeros((n, 0), order="F")
@@ -243,12 +260,36 @@ def _unpack(res) -> Result:
 
 def accelerated_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "until_rank",
                            rounds: int = 0, target_rank: int = 0, seed: int = 0,
-                           stop_tol: float = 0.0, max_rounds: int = -1) -> Result:
+                           stop_tol: float = 0.0, max_rounds: int = -1,
+                           copy_factor: bool = True) -> Result:
+    """copy_factor=False keeps the C factor buffer behind a numpy view (no second copy of
+    a multi-GB factor); it is freed with the last view."""
     cfg = _Cfg(block_size, MODES[mode], rounds, target_rank, seed, stop_tol)
     res = _Res()
     _check(lib().rpo_accelerated_rpcholesky_bounded(C.byref(oracle._o), C.byref(cfg),
                                                     max_rounds, C.byref(res)))
-    return _unpack(res)
+    return _unpack(res, copy_factor)
+
+
+@dataclass
+class Margins:
+    """Smallest decision margins seen since margins_reset() (rpc_oracle.c recorder):
+    draw = distance of a sampling target to the nearer cumsum bucket edge / total;
+    sweep = |u_i r_i - h_ii| / u_i over every accept test."""
+    min_draw: float
+    min_sweep: float
+    n_draws: int
+    n_decisions: int
+
+
+def margins_reset(on: bool = True) -> None:
+    lib().rpo_margins_reset(int(on))
+
+
+def margins_get() -> Margins:
+    a, b, c, d = C.c_double(), C.c_double(), C.c_int64(), C.c_int64()
+    lib().rpo_margins_get(C.byref(a), C.byref(b), C.byref(c), C.byref(d))
+    return Margins(a.value, b.value, c.value, d.value)
 
 
 def block_rpcholesky(oracle: Oracle, *, block_size: int, mode: str = "until_rank",

@@ -39,6 +39,9 @@ static int fail(int code, const char* fmt, ...) {
 
 const char* rpo_last_error(void) { return g_err; }
 
+/* Releases one buffer a result handed over (a factor kept without copying). */
+void rpo_free(void* p) { free(p); }
+
 /* ---- rng.hpp:27-42  SplitMix64::next_u64 / next_double --------------- */
 static inline uint64_t mix64(uint64_t z) {
   z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
@@ -64,6 +67,31 @@ void rpo_cumulative_sums(const double* w, int64_t n, double* out) {
   }
 }
 
+/* ---- decision-margin recorder (instrumentation for the parity tests) --
+ * Not part of the reference: records how far each random decision was from
+ * flipping, so a pivot match between two implementations whose sums differ
+ * only by association can be shown to be robust rather than lucky.
+ *   draw margin  = min(target - cumsum[i-1], cumsum[i] - target) / total
+ *                  (distance of the target to the nearer bucket edge)
+ *   sweep margin = |u_i * r - h_ii| / u_i   (rpcholesky.hpp:179 accept test)
+ * Off by default; rpo_margins_reset() turns it on and clears the minima. */
+static int g_margins_on;
+static double g_min_draw = 1.0 / 0.0, g_min_sweep = 1.0 / 0.0;
+static int64_t g_n_draws, g_n_decisions;
+
+void rpo_margins_reset(int on) {
+  g_margins_on = on;
+  g_min_draw = g_min_sweep = 1.0 / 0.0;
+  g_n_draws = g_n_decisions = 0;
+}
+
+void rpo_margins_get(double* min_draw, double* min_sweep, int64_t* n_draws, int64_t* n_decisions) {
+  *min_draw = g_min_draw;
+  *min_sweep = g_min_sweep;
+  *n_draws = g_n_draws;
+  *n_decisions = g_n_decisions;
+}
+
 /* ---- rng.hpp:80-96  sample_discrete ---------------------------------- */
 int rpo_sample_discrete(const double* cumsum, int64_t n, double u01, int64_t* idx) {
   if (n == 0) return fail(RPO_EINVAL, "sample_discrete: empty weights");
@@ -80,6 +108,12 @@ int rpo_sample_discrete(const double* cumsum, int64_t n, double u01, int64_t* id
   if (i >= n) i = n - 1;
   while (i > 0 && cumsum[i] == cumsum[i - 1]) --i;
   *idx = i;
+  if (g_margins_on) {
+    const double below = target - (i > 0 ? cumsum[i - 1] : 0.0), above = cumsum[i] - target;
+    const double mg = (below < above ? below : above) / total;
+    if (mg < g_min_draw) g_min_draw = mg;
+    ++g_n_draws;
+  }
   return RPO_OK;
 }
 
@@ -268,6 +302,11 @@ int rpo_rejection_sweep(double* h, int64_t b, const int64_t* proposals, uint64_t
   int64_t m = 0;
   for (int64_t i = 0; i < b; ++i) {
     const double r = rpo_u01(rpo_splitmix64_draw(seed, draw0 + (uint64_t)i));
+    if (g_margins_on && u[i] > 0.0) {
+      const double mg = fabs(u[i] * r - h[i * b + i]) / u[i];
+      if (mg < g_min_sweep) g_min_sweep = mg;
+      ++g_n_decisions;
+    }
     if (u[i] * r < h[i * b + i]) {
       const double root = sqrt(h[i * b + i]);
       for (int64_t j = i; j < b; ++j) l[i * b + j] = h[i * b + j] / root;

@@ -43,6 +43,9 @@ uint64_t rpo_splitmix64_draw(uint64_t seed, uint64_t n); /* n-th next_u64(), 0-b
 double rpo_u01(uint64_t z);                              /* next_double() mapping */
 void rpo_cumulative_sums(const double* w, int64_t n, double* out);
 int rpo_sample_discrete(const double* cumsum, int64_t n, double u01, int64_t* idx);
+/* Decision-margin instrumentation (not in the reference; see rpc_oracle.c). */
+void rpo_margins_reset(int on);
+void rpo_margins_get(double* min_draw, double* min_sweep, int64_t* n_draws, int64_t* n_decisions);
 
 /* ---- oracle.hpp ------------------------------------------------------- */
 /* A PSD oracle: either a kernel over X (N x d, column-major) or a dense
@@ -117,6 +120,7 @@ int rpo_accelerated_rpcholesky_lowmem(const rpo_oracle* o, const rpo_run_config*
 int rpo_block_rpcholesky(const rpo_oracle* o, const rpo_run_config* cfg, rpo_result* res);
 int rpo_simple_rpcholesky(const rpo_oracle* o, int64_t k, uint64_t seed, rpo_result* res);
 void rpo_result_free(rpo_result* res);
+void rpo_free(void* p); /* one buffer taken out of a result */
 double rpo_relative_trace_error(const rpo_oracle* o, const double* factor, int64_t n,
                                 int64_t k);
 const char* rpo_last_error(void);

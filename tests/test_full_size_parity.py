@@ -1,0 +1,131 @@
+"""Full-size parity at the BASELINE.json configurations (SURVEY §8(d) "Parity checks
+(same run)"): the CUDA path through the C-ABI against the CPU restatement of the
+reference (oracle/, all host threads) on the *same* seeded inputs at the sizes the
+bench measures — C2, C3 and C4 in full, C5 bounded to FixedRounds(3).
+
+Bars (BASELINE.json north_star): pivots and the whole PivotTrace identical (replay
+mode: same RNG stream, same accept decisions — rpcholesky.hpp:338-401, rng.hpp:67-96),
+||F_gpu - F_cpu||_F / ||F_cpu||_F <= 1e-10 over the *entire* factor (accumulated in
+column blocks, no probes), |trace_err_gpu - trace_err_cpu| <= 1e-8 (577-583), plus the
+reference's invariants on the GPU output (u >= 0, surplus semantics, rank).
+
+Fast mode (the benched path) uses a fixed two-level cumsum association instead of the
+sequential scan; it is held to the same bars here.  Every run logs the
+oracle's decision margins (rpc_oracle.c recorder): the smallest relative distance of a
+sampling target to a cumsum bucket edge and the smallest |u_i r_i - h_ii| / u_i, which
+say how far each matched decision was from flipping.  With RPC_PARITY_LOG set, one JSON
+line per case is appended there (profiles/r02_full_parity.jsonl is such a log).
+"""
+import json
+import os
+import time
+
+import numpy as np
+import pytest
+
+import pyoracle as po
+from paper_2410_03969_b200 import workloads as wl
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+F_TOL = 1e-10
+TRACE_TOL = 1e-8
+THREADS = os.cpu_count() or 1
+
+_cache = {}
+
+
+def oracle_run(name, rounds=None):
+    """CPU restatement on the full workload, cached for the fast/replay pair (one config at
+    a time: the C4 factor alone is 9 GB of host memory)."""
+    key = (name, rounds)
+    if key not in _cache:
+        _cache.clear()
+        w = wl.CONFIGS[name]
+        x = w.points()
+        o = po.Oracle(x=x, kernel=w.kernel, sigma=w.sigma, n_threads=THREADS)
+        kw = dict(mode="fixed_rounds", rounds=rounds) if rounds else dict(target_rank=w.k)
+        po.margins_reset(True)
+        t0 = time.perf_counter()
+        r = po.accelerated_rpcholesky(o, block_size=w.b, seed=w.seed, copy_factor=False, **kw)
+        dt = time.perf_counter() - t0
+        mg = po.margins_get()
+        po.margins_reset(False)
+        err = po.relative_trace_error(o, r.factor)
+        _cache[key] = (w, x, r, err, mg, dt)
+    return _cache[key]
+
+
+def blocked_rel(a, b, blk=64):
+    """||a - b||_F / ||b||_F over column blocks (no N x k temporaries)."""
+    num = den = 0.0
+    for j in range(0, b.shape[1], blk):
+        d = a[:, j:j + blk] - b[:, j:j + blk]
+        num += float(np.einsum("ij,ij->", d, d))
+        bb = b[:, j:j + blk]
+        den += float(np.einsum("ij,ij->", bb, bb))
+    return (num / den) ** 0.5 if den > 0 else num ** 0.5
+
+
+def check(name, replay, rounds=None):
+    from paper_2410_03969_b200 import api
+    w, x, r, err_o, mg, t_cpu = oracle_run(name, rounds)
+    cfg = (api.RunConfig.fixed_rounds(rounds, w.b, w.seed) if rounds
+           else api.RunConfig.until_rank(w.k, w.b, w.seed))
+    cfg.replay_scan = replay
+    t0 = time.perf_counter()
+    g = api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec(w.kernel, w.sigma)), cfg)
+    t_gpu = time.perf_counter() - t0
+    try:
+        pivots_equal = bool(np.array_equal(g.pivots, r.pivots))
+        trace_equal = (len(g.proposed) == len(r.proposed)
+                       and all(np.array_equal(a, b) for a, b in zip(g.proposed, r.proposed))
+                       and all(np.array_equal(a, b) for a, b in zip(g.accepted, r.accepted)))
+        rec = {"config": name, "rounds_bound": rounds, "mode": "replay" if replay else "fast",
+               "n": w.n, "k": w.k, "b": w.b, "rank": int(g.rank),
+               "pivots_equal": pivots_equal, "trace_equal": bool(trace_equal),
+               "min_draw_margin": mg.min_draw, "min_sweep_margin": mg.min_sweep,
+               "draws": mg.n_draws, "decisions": mg.n_decisions,
+               "cpu_threads": THREADS, "cpu_s": round(t_cpu, 2), "gpu_call_s": round(t_gpu, 3)}
+        f_rel = None
+        if pivots_equal:
+            f = g.factor_into(np.empty((w.n, g.rank), order="F"))
+            f_rel = blocked_rel(f, r.factor)
+            del f
+            rec["f_rel"] = f_rel
+            rec["chol_rel"] = float(np.linalg.norm(g.chol_factor - r.chol) / np.linalg.norm(r.chol))
+            u = g.residual_diag
+            rec["u_maxabs"] = float(np.max(np.abs(u - r.residual_diag)))
+            rec["u_min"] = float(u.min())
+        rec["trace_err_gpu"] = g.relative_trace_error
+        rec["trace_err_cpu"] = err_o
+        rec["trace_diff"] = abs(g.relative_trace_error - err_o)
+        log = os.environ.get("RPC_PARITY_LOG")
+        if log:
+            with open(log, "a") as fh:
+                fh.write(json.dumps(rec) + "\n")
+        print(json.dumps(rec))
+        assert pivots_equal and trace_equal, rec
+        assert g.rank_exhausted == r.rank_exhausted and g.surplus == r.surplus
+        if not rounds:
+            assert g.rank >= w.k and g.surplus == g.rank - w.k
+        assert f_rel <= F_TOL, rec
+        assert rec["chol_rel"] <= F_TOL, rec
+        assert rec["u_maxabs"] <= 1e-10 and rec["u_min"] >= 0.0, rec
+        assert rec["trace_diff"] <= TRACE_TOL, rec
+    finally:
+        g.free()
+
+
+@pytest.mark.parametrize("replay", [True, False], ids=["replay", "fast"])
+@pytest.mark.parametrize("name", ["C2", "C3", "C4"])
+def test_full_size_parity(name, replay):
+    check(name, replay)
+
+
+@pytest.mark.parametrize("replay", [True, False], ids=["replay", "fast"])
+def test_c5_bounded_parity(replay):
+    """C5 (N = 2e6, d = 100, l1, b = 200) bounded to three rounds: its full UntilRank(4000)
+    factor is 67 GB, beyond a host comparison; three rounds still run every kernel at full
+    N and d with kcur up to 400."""
+    check("C5", replay, rounds=3)
