@@ -8,15 +8,24 @@ the configuration the metric names.  Points are synthetic and seeded
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
 
+--gpus N    : without torchrun, spawns N ranks (one process per GPU, NCCL, row-sharded);
+              under torchrun (WORLD_SIZE set) each process is one rank
 value       : device wall time (s) of one factorization with the points resident in HBM
-              (CUDA events, max over ranks); lower is better
+              (CUDA events per step, median over the K steps, max over ranks)
 e2e         : same call through the host C-ABI entry (host X in, pinned) plus the
               device->host copy of the full factor, pivots and chol_factor
 roofline    : the fused K5+K6 update kernel (FP64 DMMA bound) against the FP64
               tensor peak measured on this pool (profiles/r01_fp64_peaks.json)
-cpu_baseline: the CPU oracle restatement timed on this host on a bounded sample
---impl reference: the reference path's CPU implementation (oracle port, all host
-              threads) on the same config, extrapolated from a bounded sample
+parity      : after the timed region, the full workload is factored by the CPU restatement
+              of the reference (oracle/, all host threads) and compared with the GPU result
+              in fast (benched) and replay mode: pivots, trace, ||dF||/||F||, trace error,
+              the oracle's decision margins
+cpu_baseline: that same oracle run on the full workload (no extrapolation)
+--impl reference: the reference's own CPU code (oracle/_ref: its headers compiled against
+              the Eigen-API shim, single thread as its path runs) on a bounded sample of the
+              workload (first N'=1e5 rows, same k/b/seed), scaled by N/N'; the line declares
+              the extrapolation and quotes the committed full-N calibration
+              (profiles/r02_reference_calibration_<config>.json, tools/reference_calibration.py)
 """
 from __future__ import annotations
 
@@ -124,15 +133,27 @@ def cpu_sample(w, threads: int, n_sample: int, lowmem: bool = False):
     return dt, dt * (w.n / n_sample)
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def reference_arm(w, args):
     """The reference's own CPU accelerated_rpcholesky: its headers compiled against the
     Eigen-API shim (oracle/_ref, built where /root/reference exists; prebuilt .so here),
-    single-threaded as the reference's KernelOracle path is (one 256-wide panel).  Each
-    step runs a bounded sample: the first N' rows of the workload with the same k, b, seed;
-    the value is scaled by N/N' (the path is linear in N at fixed k).  Falls back to the C
-    restatement when the reference build is absent."""
+    single-threaded as the reference's KernelOracle path is (one 256-wide panel, Eigen
+    without OpenMP).  Each step runs a bounded sample: the first N' rows of the workload
+    with the same k, b, seed; the value is scaled by N/N' (the path is linear in N at fixed
+    k: residual GEMM, TRSM and kernel columns are all O(N)).  A CPU path has no warm-up
+    state, so at most one warm-up sample runs.  Falls back to the C restatement when the
+    reference build is absent."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    n_sample = args.cpu_sample or min(w.n, 20_000)
+    n_sample = args.cpu_sample or min(w.n, 100_000)
     x = w.points(n_sample)
     try:
         import pyref
@@ -140,7 +161,8 @@ def reference_arm(w, args):
     except Exception:
         use_ref = False
     times = []
-    for i in range(args.warmup + args.steps):
+    warm = min(args.warmup, 1)
+    for i in range(warm + args.steps):
         t0 = time.perf_counter()
         if use_ref:
             pyref.accelerated_rpcholesky_kernel(x, w.kernel, w.sigma, block_size=w.b,
@@ -150,16 +172,105 @@ def reference_arm(w, args):
             po.accelerated_rpcholesky(po.Oracle(x=x, kernel=w.kernel, sigma=w.sigma, n_threads=1),
                                       block_size=w.b, target_rank=w.k, seed=w.seed)
         dt = time.perf_counter() - t0
-        if i >= args.warmup:
+        if i >= warm:
             times.append(dt)
     dt = statistics.median(times)
-    v = dt * (w.n / n_sample)
+    factor = w.n / n_sample
+    v = dt * factor
     kind = "reference" if use_ref else "port"
+    calib = None
+    cp = os.path.join(ROOT, "profiles", f"r02_reference_calibration_{w.name}.json")
+    if os.path.exists(cp):
+        c = json.load(open(cp))
+        calib = {"measured_full_n_s": c.get("full_n_s"), "cpu_model": c.get("cpu_model"),
+                 "sample_extrapolated_s": c.get("extrapolated_s"),
+                 "extrapolation_over_measured": c.get("extrapolation_over_measured"),
+                 "file": os.path.relpath(cp, ROOT)}
     cpu = {"value": v, "unit": "s", "cores": 1, "kind": kind,
+           "cpu_model": cpu_model(), "nproc": os.cpu_count(),
            "sample": (f"{'reference headers (oracle/_ref, Eigen-API shim)' if use_ref else 'C restatement'}"
                       f" single-threaded on the first N'={n_sample} rows of {w.name} (same k/b/seed): "
-                      f"{dt:.2f} s median of {len(times)}, x N/N'={w.n / n_sample:g}")}
+                      f"{dt:.2f} s median of {len(times)} (warm-up {warm}), x N/N'={factor:g}"),
+           "extrapolation": {"n_sample": n_sample, "factor": factor, "sample_median_s": dt,
+                             "calibration": calib}}
     return v, cpu
+
+
+def same_run_parity(w, x, spec, cfg_base, ctx, x_dev, threads):
+    """SURVEY §8(d) "Parity checks (same run)": the full workload through the CPU restatement
+    of the reference (oracle/, test infrastructure, the checker) against the GPU result in
+    fast (benched) and replay mode.  Returns (parity dict, oracle seconds)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as po
+    from paper_2410_03969_b200 import api
+    from paper_2410_03969_b200 import _lib as L
+    o = po.Oracle(x=x, kernel=w.kernel, sigma=w.sigma, n_threads=threads)
+    po.margins_reset(True)
+    t0 = time.perf_counter()
+    r = po.accelerated_rpcholesky(o, block_size=w.b, target_rank=w.k, seed=w.seed,
+                                  copy_factor=False)
+    t_cpu = time.perf_counter() - t0
+    mg = po.margins_get()
+    po.margins_reset(False)
+    err_o = po.relative_trace_error(o, r.factor)
+    out = {"oracle": f"C restatement (oracle/rpc_oracle.c), {threads} threads, full workload",
+           "oracle_s": round(t_cpu, 3), "min_draw_margin": mg.min_draw,
+           "min_sweep_margin": mg.min_sweep, "draws": mg.n_draws, "decisions": mg.n_decisions}
+    for mode in ("fast", "replay"):
+        cfg = api.RunConfig(**{**cfg_base.__dict__, "replay_scan": mode == "replay"})
+        g = api.accelerated_rpcholesky_device(x_dev.data_ptr(), w.n, w.d, w.d, L.RPC_ROW_MAJOR,
+                                              spec, cfg, ctx)
+        try:
+            piv = bool(np.array_equal(g.pivots, r.pivots))
+            tr = (len(g.proposed) == len(r.proposed)
+                  and all(np.array_equal(a, b) for a, b in zip(g.proposed, r.proposed))
+                  and all(np.array_equal(a, b) for a, b in zip(g.accepted, r.accepted)))
+            rec = {"pivots_equal": piv, "trace_equal": bool(tr),
+                   "trace_diff": abs(g.relative_trace_error - err_o),
+                   "factorize_ms": g.timing["factorize_ms"]}
+            if piv:
+                f = g.factor_into(np.empty((w.n, g.rank), order="F"))
+                num = den = 0.0
+                for j in range(0, g.rank, 64):
+                    dd = f[:, j:j + 64] - r.factor[:, j:j + 64]
+                    num += float(np.einsum("ij,ij->", dd, dd))
+                    rr = r.factor[:, j:j + 64]
+                    den += float(np.einsum("ij,ij->", rr, rr))
+                del f
+                rec["f_rel"] = (num / den) ** 0.5
+            rec["ok"] = bool(piv and tr and rec.get("f_rel", 1.0) <= 1e-10
+                             and rec["trace_diff"] <= 1e-8)
+            out[mode] = rec
+        finally:
+            g.free()
+    return out, t_cpu
+
+
+def spawn_ranks(args) -> int:
+    """--gpus N without torchrun: one process per GPU (RANK / LOCAL_RANK / WORLD_SIZE /
+    MASTER_* as torchrun sets them); rank 0 prints the JSON line."""
+    import socket
+    import torch
+    n = args.gpus
+    if torch.cuda.device_count() < n:
+        print(f"bench.py --gpus {n}: only {torch.cuda.device_count()} CUDA device(s) visible",
+              file=sys.stderr)
+        return 2
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(n),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        env.setdefault("NCCL_DEBUG", "INFO")
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:],
+                                      env=env, stdout=None if r == 0 else subprocess.DEVNULL))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
 
 
 def main():
@@ -174,7 +285,10 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0, help="N' for the CPU sample (0=auto)")
     ap.add_argument("--variant", default="standard", choices=["standard", "lowmem"],
                     help="lowmem: accelerated_rpcholesky_lowmem (rpcholesky.hpp:408-485)")
+    ap.add_argument("--no-parity", action="store_true", help="skip the same-run oracle parity")
     args = ap.parse_args()
+    if args.impl == "b200" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
 
     from paper_2410_03969_b200 import workloads
     w = workloads.CONFIGS[args.config]
@@ -195,7 +309,8 @@ def main():
             return
         v, cpu = reference_arm(w, args)
         print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": "s",
-                          "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+                          "n_gpus": max(world, args.gpus), "steps": args.steps,
+                          "warmup": args.warmup,
                           "ms_per_step": v * 1e3, "higher_is_better": False, "scaling": "strong",
                           "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                           "config": cfg_json, "cpu_baseline": cpu,
@@ -239,23 +354,25 @@ def main():
     for _ in range(args.warmup):
         one_step().free()
     barrier()
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # per-step CUDA events on torch's stream: each library call returns with its result
+    # complete (it synchronises its own stream), so the events bracket whole factorizations
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     results = []
     with ClockSampler(local_rank) as clk:
         barrier()
-        ev0.record()
-        for _ in range(args.steps):
+        evs[0].record()
+        for i in range(args.steps):
             r = one_step()
+            evs[i + 1].record()
             results.append((r.timing, r.rank, [len(a) for a in r.accepted], r.relative_trace_error))
             r.free()
-        ev1.record()
         barrier()
-    total_ms = ev0.elapsed_time(ev1)
-    t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+    step_ms = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    t = torch.tensor([sum(step_ms), statistics.median(step_ms)], device=dev, dtype=torch.float64)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
-    sec_per_step = total_ms / args.steps / 1e3
+    total_ms, median_ms = float(t[0].item()), float(t[1].item())
+    sec_per_step = median_ms / 1e3
     timing, k_final, m_seq, trace_err = results[-1]
     upd_ms = timing["update_ms"]
     flops = timing["update_flops"]
@@ -328,18 +445,30 @@ def main():
         e2e = {"value": float(tt.item()), "unit": "s",
                "h2d_bytes_per_step": int(nr * w.d * 8), "d2h_bytes_per_step": int(d2h)}
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
+    # same-run parity on the full workload; the oracle run is also the CPU baseline
+    cpu, parity = None, None
+    if rank == 0 and world == 1 and not lowmem and not args.no_parity:
+        parity, t_cpu = same_run_parity(w, x, spec, cfg, ctx, x_dev, n_cores)
+        if not args.no_cpu:
+            cpu = {"value": t_cpu, "unit": "s", "cores": n_cores, "kind": "port",
+                   "cpu_model": cpu_model(),
+                   "sample": f"full {w.name} workload (N={w.n}, no extrapolation): the C "
+                             f"restatement of the reference (oracle/rpc_oracle.c, OpenMP over "
+                             f"rows, {n_cores} threads), the same run that checks parity"}
+    elif rank == 0 and world == 1 and not args.no_cpu:
         n_sample = args.cpu_sample or min(w.n, 10_000 if lowmem else 100_000)
         dt, ext = cpu_sample(w, n_cores, n_sample, lowmem)
         cpu = {"value": ext, "unit": "s", "cores": n_cores, "kind": "port",
+               "cpu_model": cpu_model(),
                "sample": f"oracle restatement on the first N'={n_sample} rows of {w.name}, same "
                          f"k/b/seed, {dt:.2f} s measured, x N/N' to the full N"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": sec_per_step, "unit": "s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec_per_step * 1e3,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "step_ms": {"median": median_ms, "mean": total_ms / args.steps,
+                        "min": min(step_ms), "max": max(step_ms)},
             "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded, workloads.py)", "config": cfg_json,
             "kernel_col_gbs": col_gbs,
@@ -359,7 +488,7 @@ def main():
                          "per_launch_flops": flops / max(1, timing["update_launches"]),
                          "update_ms_per_step": upd_ms,
                          "update_share_of_step": upd_ms / (sec_per_step * 1e3)},
-            "cpu_baseline": cpu, "e2e": e2e,
+            "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": int(timing["kernel_launches"]) * args.steps,
             "clocks": clk.summary(),
         }

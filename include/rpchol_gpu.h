@@ -62,7 +62,8 @@ typedef struct {
 /* RunConfig (rpcholesky.hpp:36-67) plus B200 execution flags. */
 enum {
   RPC_FLAG_REPLAY_SCAN = 1u /* sequential cumulative_sums + upper_bound exactly as
-                               rng.hpp:67-96 (single shard only; slower) */
+                               rng.hpp:67-96 over the global residual diagonal (gathered
+                               on every shard when sharded); slower */
 };
 typedef struct {
   int64_t block_size;  /* b >= 1 (this build: b <= 256) */
@@ -85,6 +86,23 @@ int rpc_create_virtual(int device, int n_shards, rpc_ctx** out);
  * by the caller (e.g. over torch.distributed / MPI / files). */
 int rpc_nccl_unique_id(void* id128);
 int rpc_create_nccl(int device, const void* id128, int nranks, int rank, rpc_ctx** out);
+/* One rank of an nranks-process job whose collectives the caller provides on the host
+ * (e.g. torch.distributed over gloo, MPI): the library synchronises its stream, stages the
+ * data through pinned memory and calls back.  Same protocol, results and p-invariance as
+ * the NCCL context, at host-link speed — meant for CPU-transport jobs and for running
+ * several ranks on one GPU in tests (the kernels never wait on another rank).
+ * Callbacks return 0 on success; `ops` is copied, `user` must outlive the context. */
+typedef struct {
+  void* user;
+  /* every rank contributes `bytes` from send; recv receives nranks * bytes, rank order */
+  int (*allgather)(void* user, const void* send, void* recv, size_t bytes);
+  /* in place: word i becomes the bitwise OR of word i over all ranks (the library only
+   * reduces buffers in which at most one rank holds a non-zero word, so any exact
+   * combine — OR, unsigned max — is valid) */
+  int (*allreduce_or_u64)(void* user, uint64_t* buf, size_t count);
+} rpc_host_collectives;
+int rpc_create_hostcoll(int device, int nranks, int rank, const rpc_host_collectives* ops,
+                        rpc_ctx** out);
 void rpc_destroy(rpc_ctx* ctx);
 /* Message of the last failing call on this thread (or on ctx when non-null). */
 const char* rpc_last_error(const rpc_ctx* ctx);

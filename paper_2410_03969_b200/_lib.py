@@ -35,8 +35,17 @@ EXPORTS = [
     "rpc_krr_precond_rank", "rpc_krr_precond_pivots", "rpc_krr_predict", "rpc_krr_free",
     "rpc_block_rpcholesky", "rpc_block_rpcholesky_device", "rpc_simple_rpcholesky",
     "rpc_simple_rpcholesky_device", "rpc_result_write_rpcf", "rpc_result_write_trace_csv",
-    "rpc_bench_column_throughput", "rpc_accelerated_rpcholesky_into",
+    "rpc_bench_column_throughput", "rpc_accelerated_rpcholesky_into", "rpc_create_hostcoll",
 ]
+
+# rpc_host_collectives (include/rpchol_gpu.h): callbacks the library calls for each collective
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t)
+ALLREDUCE_OR_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_uint64), C.c_size_t)
+
+
+class HostCollectivesC(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("allgather", ALLGATHER_FN),
+                ("allreduce_or_u64", ALLREDUCE_OR_FN)]
 
 
 class KernelSpecC(C.Structure):
@@ -94,6 +103,8 @@ def load() -> C.CDLL:
         "rpc_create_virtual": (C.c_int, [C.c_int, C.c_int, C.POINTER(vp)]),
         "rpc_nccl_unique_id": (C.c_int, [C.c_char_p]),
         "rpc_create_nccl": (C.c_int, [C.c_int, C.c_char_p, C.c_int, C.c_int, C.POINTER(vp)]),
+        "rpc_create_hostcoll": (C.c_int, [C.c_int, C.c_int, C.c_int,
+                                          C.POINTER(HostCollectivesC), C.POINTER(vp)]),
         "rpc_destroy": (None, [vp]),
         "rpc_last_error": (C.c_char_p, [vp]),
         "rpc_shard_rows": (C.c_int, [vp, i64, C.c_int, pi64, pi64]),

@@ -63,13 +63,18 @@ class RunConfig:
 
 class Context:
     """One GPU (optionally holding `virtual_shards` row shards), or one rank of
-    an NCCL job (`nccl_id`, `nranks`, `rank`)."""
+    an NCCL job (`nccl_id`, `nranks`, `rank`), or one rank of a job whose collectives
+    run on the host (`host_collectives`, see hostcoll.py; rpc_create_hostcoll)."""
 
     def __init__(self, device: int = 0, virtual_shards: int = 1, nccl_id: bytes | None = None,
-                 nranks: int = 1, rank: int = 0):
+                 nranks: int = 1, rank: int = 0, host_collectives=None):
         lib = L.load()
         h = C.c_void_p()
-        if nccl_id is not None:
+        if host_collectives is not None:
+            self._hc = _host_collectives_c(host_collectives)  # keeps the callbacks alive
+            L.check(lib.rpc_create_hostcoll(device, host_collectives.nranks,
+                                            host_collectives.rank, C.byref(self._hc), C.byref(h)))
+        elif nccl_id is not None:
             L.check(lib.rpc_create_nccl(device, nccl_id, nranks, rank, C.byref(h)))
         elif virtual_shards > 1:
             L.check(lib.rpc_create_virtual(device, virtual_shards, C.byref(h)))
@@ -100,6 +105,31 @@ class Context:
         r0, nr = C.c_int64(), C.c_int64()
         L.check(L.load().rpc_shard_rows(self.handle, n, local, C.byref(r0), C.byref(nr)))
         return r0.value, nr.value
+
+
+def _host_collectives_c(hc) -> L.HostCollectivesC:
+    """Wraps an object with allgather(send: uint8 array) -> uint8 array (nranks x bytes) and
+    allreduce_or(buf: uint64 array, in place) as rpc_host_collectives callbacks."""
+
+    def allgather(user, send, recv, nbytes):
+        try:
+            src = np.ctypeslib.as_array(C.cast(send, C.POINTER(C.c_uint8)), shape=(nbytes,))
+            dst = np.ctypeslib.as_array(C.cast(recv, C.POINTER(C.c_uint8)),
+                                        shape=(nbytes * hc.nranks,))
+            dst[:] = np.asarray(hc.allgather(src.copy()), dtype=np.uint8).reshape(-1)
+            return 0
+        except Exception:  # reported as RPC_ENCCL by the library
+            return 1
+
+    def allreduce_or(user, buf, count):
+        try:
+            a = np.ctypeslib.as_array(buf, shape=(count,))
+            hc.allreduce_or(a)
+            return 0
+        except Exception:
+            return 1
+
+    return L.HostCollectivesC(None, L.ALLGATHER_FN(allgather), L.ALLREDUCE_OR_FN(allreduce_or))
 
 
 def plan_shards(n: int, n_shards: int, shard: int) -> dict:

@@ -62,8 +62,6 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: this build supports d <= 128");
   if (layout != RPC_COL_MAJOR && layout != RPC_ROW_MAJOR) raise(RPC_EINVAL, "unknown layout");
   const bool replay = (cfg.flags & RPC_FLAG_REPLAY_SCAN) != 0;
-  if (replay && ctx->nshards() != 1)
-    raise(RPC_EINVAL, "replay scan requires a single shard (sequential cumulative_sums)");
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->stream;
   const int b = (int)cfg.block_size;
@@ -78,6 +76,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   lay.foff = 2 + dpad;
   lay.rec = 2 + dpad + ldf;
 
+  NvtxRange nv_all(lowmem ? "rpc:accelerated_rpcholesky_lowmem"
+                           : algo == kAlgoBlock  ? "rpc:block_rpcholesky"
+                           : algo == kAlgoSimple ? "rpc:simple_rpcholesky"
+                                                 : "rpc:accelerated_rpcholesky");
   using clk = std::chrono::steady_clock;
   const auto h0 = clk::now();
   auto ms_since = [](clk::time_point a) {
@@ -96,8 +98,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   Ev ev_up0, ev_up1, ev_t0, ev_t1;
   CK(cudaEventRecord(ev_up0.e, st));
   res->shards.resize(ctx->nvirt);
-  DBuf nonfinite(ctx, sizeof(int));
-  CK(cudaMemsetAsync(nonfinite.p, 0, sizeof(int), st));
+  DBuf nonfinite(ctx, sizeof(uint64_t));  // int flag in a zeroed 64-bit word (owner reduce)
+  CK(cudaMemsetAsync(nonfinite.p, 0, sizeof(uint64_t), st));
   int64_t max_tiles = 0;
   for (int v = 0; v < ctx->nvirt; ++v) {
     Shard& s = res->shards[v];
@@ -143,20 +145,17 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     }
     launch_pack_points(dsrc, s.n_loc, (int)d, ld_src, layout == RPC_ROW_MAJOR, dpad,
                        s.X.as<double>(), s.sqn.as<double>(), nonfinite.as<int>(), st);
+    CK(cudaGetLastError());
     launch_fill(s.u.as<double>(), s.n_loc, 1.0, st);  // u = max(diag, 0) = 1 (oracle.hpp:263)
     launches += 2;
     if (tmp.p) CK(cudaStreamSynchronize(st));  // tmp returns to the pool
   }
   CK(cudaEventRecord(ev_up1.e, st));
-  {  // DataMatrix rejects non-finite entries (data_matrix.hpp:26-28)
-    int bad = 0;
-    CK(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+  {  // DataMatrix rejects non-finite entries (data_matrix.hpp:26-28); every rank agrees
+    allreduce_owner(ctx, nonfinite.p, 1);
+    uint64_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, nonfinite.p, sizeof bad, cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    if (ctx->world > 1) {
-      NK(ncclAllReduce(nonfinite.p, nonfinite.p, 1, ncclInt, ncclMax, ctx->comm, st));
-      CK(cudaMemcpyAsync(&bad, nonfinite.p, sizeof(int), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-    }
     if (bad) raise(RPC_EINVAL, "DataMatrix: non-finite entry");
   }
 
@@ -164,7 +163,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   const int P = L.P;
   DBuf totals_all(ctx, sizeof(double) * L.ncg), g2_all(ctx, sizeof(double) * L.ncg),
       chunk_end(ctx, sizeof(double) * L.ncg);
-  DBuf recv(ctx, sizeof(double) * (size_t)P * b * lay.rec), prop(ctx, sizeof(double) * b * lay.rec);
+  // proposal records: every draw's owner writes its slot; across processes the slots are
+  // combined by the owner reduce (zeroed first), so each GPU receives b records, not P b
+  DBuf prop(ctx, sizeof(double) * b * lay.rec);
   DBuf owner(ctx, sizeof(int) * b), Hbuf(ctx, sizeof(double) * b * b),
       lcol(ctx, sizeof(double) * b * b), lacc(ctx, sizeof(double) * b * b);
   const int64_t ldl = 272, nbl = 256;  // L^{-1} columns shifted by kcur & 1 (update.cu)
@@ -182,8 +183,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     kept_idx = DBuf(ctx, sizeof(int) * b);
     propk = DBuf(ctx, sizeof(double) * b * lay.rec);
   }
-  DBuf cumsum;
+  DBuf cumsum, u_all;
   if (replay) cumsum = DBuf(ctx, sizeof(double) * n);
+  // replay with several shards: the sequential scan needs the whole residual diagonal, so
+  // every shard gathers it (global row order = shard slot order) and scans it identically
+  if (replay && P > 1) u_all = DBuf(ctx, sizeof(double) * (size_t)L.ncg * kChunk);
   // low-memory state (replicated): pivot records, L and L^{-1} row-major [cap][ldf],
   // per-round scratch K(S', S), F_S and F_S L^{-1}
   const int64_t prec = 2 + dpad;
@@ -253,11 +257,21 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     sink_tmp[0] = DBuf(ctx, sizeof(double) * std::max<int64_t>(rows_here, 1) * b);
     sink_tmp[1] = DBuf(ctx, sizeof(double) * std::max<int64_t>(rows_here, 1) * b);
   }
+  // On every exit path (an exception mid-loop included) wait for the factor copies still
+  // queued on the copy stream before the staging halves, F (via the result) and the
+  // caller's registered buffer can be released or reused.
+  struct CopyDrain {
+    cudaStream_t s;
+    ~CopyDrain() {
+      if (s) cudaStreamSynchronize(s);
+    }
+  } copy_drain{sink.p ? cst : nullptr};
   const double setup_ms = ms_since(h0);
   const auto h1 = clk::now();
   CK(cudaEventRecord(ev_t0.e, st));
   for (int64_t round = 0;; ++round) {
     if (cfg.mode == RPC_FIXED_ROUNDS ? round >= cfg.rounds : kcur >= cfg.target_rank) break;
+    NvtxRange nv_round("rpc:round");
     // SplitMix64 draw counters: accelerated uses b proposal + b accept draws per round
     // (rpcholesky.hpp:362-364, 179), block b proposals (293-296), simple one (226)
     const uint64_t draw0 = (algo == kAlgoAccelerated ? 2ull : 1ull) * (uint64_t)b * (uint64_t)round;
@@ -288,9 +302,19 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     }
     dbg(st, "scan");
     if (replay) {
-      launch_replay_scan(res->shards[0].u.as<double>(), n, cumsum.as<double>(), d_scan, st);
+      const double* ug = res->shards[0].u.as<double>();
+      if (P > 1) {
+        for (Shard& s : res->shards)
+          if (s.n_loc)
+            CK(cudaMemcpyAsync(u_all.as<double>() + (size_t)s.gidx * L.cpr * kChunk, s.u.p,
+                               sizeof(double) * s.n_loc, cudaMemcpyDeviceToDevice, st));
+        allgather(ctx, u_all.as<double>(), (size_t)L.cpr * kChunk);
+        ug = u_all.as<double>();
+      }
+      launch_replay_scan(ug, n, cumsum.as<double>(), d_scan, st);
       ++launches;
     }
+    if (ctx->world > 1) CK(cudaMemsetAsync(prop.p, 0, sizeof(double) * b * lay.rec, st));
     // -- K1/K2: b proposals; owners write their records
     for (Shard& s : res->shards) {
       SampleParams sp{};
@@ -299,6 +323,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.sqn = s.sqn.as<double>();
       sp.F = lowmem ? nullptr : s.F.as<double>();
       sp.n_loc = s.n_loc;
+      sp.n_global = n;
       sp.dpad = dpad;
       sp.ldf = ldf;
       sp.kcur = lowmem ? 0 : (int)kcur;  // lowmem: factor rows are formed after selection
@@ -314,23 +339,16 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.draw0 = draw0;
       sp.b = b;
       sp.lay = lay;
-      // one shard: every draw is owned here, so records go straight to prop (no select)
-      sp.records = P == 1 ? prop.as<double>() : recv.as<double>() + (size_t)s.gidx * b * lay.rec;
+      sp.records = prop.as<double>();  // the owner of draw j writes slot j
       sp.owner = owner.as<int>();
-      // every shard runs the sampler, including shards without rows: it also fills the
-      // replicated owner[] table that the proposal selection reads
+      // every shard runs the sampler, including shards without rows (it returns early for
+      // draws it does not own)
       if (replay) launch_replay_sample(sp, cumsum.as<double>(), st);
       else launch_sample(sp, st);
       dbg(st, "sample");
       ++launches;
     }
-    if (P > 1) {
-      allgather(ctx, recv.as<double>(), (size_t)b * lay.rec);
-      const int64_t words = 2 + dpad + (lowmem ? 0 : kcur);
-      launch_select(recv.as<double>(), (int64_t)b * lay.rec, owner.as<int>(), b, lay.rec, words,
-                    prop.as<double>(), st);
-      ++launches;
-    }
+    allreduce_owner(ctx, prop.p, (size_t)b * lay.rec);
     if (lowmem && kcur > 0) {
       // F(S', :) = A(S', S) L^{-T}  (= W_prop^T of rpcholesky.hpp:441-444)
       launch_kprop(prop.as<double>(), lay, b, piv.as<double>(), prec, (int)kcur, (int)d, kind, kfun,
@@ -622,6 +640,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   const double loop_ms = ms_since(h1);
   const auto h2 = clk::now();
   // ---- finalize ----------------------------------------------------------------
+  NvtxRange nv_fin("rpc:finalize");
   if (pending_g2) {  // last round's ||G||^2 (no further scan consumed it)
     for (Shard& s : res->shards) {
       if (s.n_loc == 0) continue;
@@ -663,9 +682,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                                                           res->chol_dev.as<double>());
       ++launches;
     }
-    if (ctx->world > 1)  // each pivot row lives on exactly one rank: sum the zeros away
-      NK(ncclAllReduce(res->chol_dev.p, res->chol_dev.p, (size_t)kcur * kcur, ncclDouble, ncclSum,
-                       ctx->comm, st));
+    // each pivot row lives on exactly one rank: the owner reduce keeps its words
+    allreduce_owner(ctx, res->chol_dev.p, (size_t)kcur * kcur);
     CK(cudaStreamSynchronize(st));  // piv returns to the pool
   }
   float ms = 0.f;
@@ -777,6 +795,22 @@ int rpc_create_nccl(int device, const void* id128, int nranks, int rank, rpc_ctx
   return rc;
 }
 
+int rpc_create_hostcoll(int device, int nranks, int rank, const rpc_host_collectives* ops,
+                        rpc_ctx** out) {
+  if (!ops || !ops->allgather || !ops->allreduce_or_u64)
+    return fail(nullptr, RPC_EINVAL, "rpc_create_hostcoll: missing collective callbacks");
+  if (nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(nullptr, RPC_EINVAL, "rpc_create_hostcoll: bad rank");
+  int rc = make_ctx(device, 1, out);
+  if (rc) return rc;
+  rpc_ctx* ctx = *out;
+  ctx->world = nranks;
+  ctx->rank = rank;
+  ctx->hostcoll = true;
+  ctx->hc = *ops;
+  return RPC_OK;
+}
+
 void rpc_destroy(rpc_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -785,6 +819,7 @@ void rpc_destroy(rpc_ctx* ctx) {
   ctx->trim();
   if (ctx->host_pinned) cudaFreeHost(ctx->host_pinned);
   if (ctx->io_pinned) cudaFreeHost(ctx->io_pinned);
+  if (ctx->hc_pinned) cudaFreeHost(ctx->hc_pinned);
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
@@ -1114,6 +1149,7 @@ void rpc_result_free(rpc_result* r) {
   if (r->ctx) {
     std::lock_guard<std::mutex> lk(r->ctx->mu);
     cudaStreamSynchronize(r->ctx->stream);
+    cudaStreamSynchronize(r->ctx->copy_stream);
     r->shards.clear();  // buffers return to the ctx pool
     r->chol_dev.release();
   }
@@ -1358,6 +1394,7 @@ int rpc_sample_discrete(rpc_ctx* ctx, const double* u, int64_t n, int64_t b, uin
     sp.sqn = zeros.as<double>();
     sp.F = zeros.as<double>();
     sp.n_loc = n;
+    sp.n_global = n;
     sp.dpad = 0;
     sp.ldf = 0;
     sp.kcur = 0;

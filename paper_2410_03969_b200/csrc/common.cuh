@@ -13,7 +13,70 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 namespace rpcb {
+
+// ---- per-device launch settings (host) --------------------------------------
+// cudaFuncSetAttribute is per device, so the opt-in to > 48 KB of dynamic shared memory,
+// the occupancy that sizes persistent grids and the SM count are cached per (kernel,
+// device[, smem]) under one mutex: several contexts on different GPUs may launch from
+// different threads of one process (rpchol_b200.hpp).
+struct LaunchCache {
+  std::mutex mu;
+  std::map<std::tuple<const void*, int, size_t>, int> occ;
+  std::map<std::pair<const void*, int>, int> smem;
+  std::map<int, int> sms;
+};
+inline LaunchCache& launch_cache() {
+  static LaunchCache c;
+  return c;
+}
+inline int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev;
+}
+// Raise the kernel's dynamic shared-memory limit on the current device to at least `bytes`.
+inline cudaError_t ensure_smem_attr(const void* fn, int bytes) {
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  int& have = c.smem[{fn, current_device()}];
+  if (have >= bytes) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) have = bytes;
+  return e;
+}
+// Resident CTAs per SM for (kernel, threads, smem) on the current device (>= 1).
+inline int cached_occupancy(const void* fn, int threads, size_t smem, int fallback) {
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  auto key = std::make_tuple(fn, current_device(), smem);
+  auto it = c.occ.find(key);
+  if (it != c.occ.end()) return it->second;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, threads, smem) != cudaSuccess ||
+      occ < 1) {
+    cudaGetLastError();
+    occ = fallback;
+  }
+  c.occ[key] = occ;
+  return occ;
+}
+inline int num_sms() {
+  LaunchCache& c = launch_cache();
+  std::lock_guard<std::mutex> lk(c.mu);
+  const int dev = current_device();
+  int& n = c.sms[dev];
+  if (!n) {
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
 
 constexpr int kChunk = 4096;       // rows per scan chunk (global, p-invariant)
 constexpr int kScanThreads = 256;  // 16 elements per thread

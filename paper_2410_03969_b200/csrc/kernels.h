@@ -53,6 +53,7 @@ struct SampleParams {
   const double* sqn;      // [n_loc]
   const double* F;        // [n_loc][ldf]
   int64_t n_loc, dpad, ldf;
+  int64_t n_global;       // N (replay mode searches the global cumsum)
   int kcur;
   int64_t row0;           // global row of local row 0 (multiple of kChunk)
   int chunk0;             // first global chunk of this shard
@@ -69,14 +70,12 @@ struct SampleParams {
   int* owner;               // [b]
 };
 void launch_sample(const SampleParams& p, cudaStream_t st);
-// Replay mode (single shard): strictly sequential cumulative_sums (rng.hpp:67-75)
-// and std::upper_bound + clamp + plateau walk (rng.hpp:80-96), reference rounding.
+// Replay mode: strictly sequential cumulative_sums (rng.hpp:67-75) over the global
+// residual diagonal and std::upper_bound + clamp + plateau walk (rng.hpp:80-96), reference
+// rounding; the shard owning the drawn row writes its record.
 void launch_replay_scan(const double* u, int64_t n, double* cumsum, ScanStatus* status,
                         cudaStream_t st);
 void launch_replay_sample(const SampleParams& p, const double* cumsum, cudaStream_t st);
-// prop[j] = records of owner[j]'s slot
-void launch_select(const double* recv, int64_t slot_stride, const int* owner, int b,
-                   int64_t rec, int64_t words, double* prop, cudaStream_t st);
 
 // ---- K3/K4: H block, rejection sweep, L^{-1} ------------------------------
 void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d, int kcur,
@@ -200,6 +199,18 @@ void launch_lowmem_append(const double* prop, RecordLayout lay, const int* pos, 
                           int64_t ldw, cudaStream_t st);
 // chol (k x k column-major, lower) from the row-major L.
 void launch_lowmem_chol(const double* Lrm, int64_t ldw, int k, double* chol, cudaStream_t st);
+
+// ---- KRR preconditioner core (krr.hpp:30-70), krr_core.cu: row-major [kc][kc] ----------
+// kc = k rounded up to 64; entries beyond k hold the identity.  Lower triangle only.
+int64_t core_dim(int k);
+size_t core_syrk_scratch_doubles(int k);
+// core = F^T F + mu I  (F row-major [n][ldf], first k columns; DMMA, deterministic)
+void launch_core_syrk(const double* F, int64_t ldf, int64_t n, int k, double mu, double* core,
+                      double* scratch, cudaStream_t st);
+// core <- L (Cholesky, lower); *info = 1 + first failing column block start (caller zeroes it)
+void launch_core_potrf(double* core, int64_t kc, int* info, cudaStream_t st);
+// t <- (L L^T)^{-1} t   (t: kc doubles, zero beyond k)
+void launch_core_potrs(const double* L, int64_t kc, double* t, cudaStream_t st);
 
 // X (host layout already on device as col-major or row-major) -> padded row-major + norms
 // *nonfinite is set to 1 if any input coordinate is NaN/Inf (DataMatrix, data_matrix.hpp:26-28)

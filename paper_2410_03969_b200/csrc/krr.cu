@@ -8,10 +8,10 @@
 //                                    it into V on the tensor cores.  N^2 kernel entries per
 //                                    product, no N^2 storage, HBM traffic O(N d).
 //   Preconditioner krr.hpp:30-70     P = F F^T + mu I through Woodbury on the device-resident
-//                                    F: core = F^T F + mu I (cuBLAS DSYRK, a plain library
-//                                    GEMM) factored by cuSOLVER DPOTRF; apply_inverse is two
-//                                    HBM-bound F passes (hand-written, deterministic) around
-//                                    a DPOTRS.
+//                                    F: core = F^T F + mu I by a DMMA SYRK, its blocked
+//                                    Cholesky and the solves with it (krr_core.cu, no
+//                                    library); apply_inverse is two HBM-bound F passes
+//                                    (deterministic) around that solve.
 //   pcg_solve      krr.hpp:87-123    textbook PCG, every vector on the device; one 24-byte
 //                                    status read per iteration feeds the residual history.
 //   fit_krr        krr.hpp:177-224   centre targets, accelerated_rpcholesky (UntilRank
@@ -22,9 +22,6 @@
 //
 // Every reduction runs over a fixed partition of the rows and is summed in a fixed order,
 // so results are bit-reproducible run to run.
-#include <cublas_v2.h>
-#include <cusolverDn.h>
-
 #include <memory>
 
 #include "runtime.h"
@@ -35,36 +32,6 @@ namespace {
 
 constexpr int kRedBlocks = 296;  // 2 x 148 SMs: fixed partition for every reduction
 constexpr int kRedThreads = 256;
-
-void blas_check(cublasStatus_t s, const char* what) {
-  if (s != CUBLAS_STATUS_SUCCESS) raise(RPC_ECUDA, std::string(what) + ": cuBLAS status " + std::to_string((int)s));
-}
-void solver_check(cusolverStatus_t s, const char* what) {
-  if (s != CUSOLVER_STATUS_SUCCESS)
-    raise(RPC_ECUDA, std::string(what) + ": cuSOLVER status " + std::to_string((int)s));
-}
-
-void destroy_handles(rpc_ctx* ctx) {
-  if (ctx->blas) cublasDestroy(static_cast<cublasHandle_t>(ctx->blas));
-  if (ctx->solver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(ctx->solver));
-  ctx->blas = ctx->solver = nullptr;
-}
-
-void ensure_handles(rpc_ctx* ctx) {
-  if (!ctx->blas) {
-    cublasHandle_t h;
-    blas_check(cublasCreate(&h), "cublasCreate");
-    blas_check(cublasSetStream(h, ctx->stream), "cublasSetStream");
-    ctx->blas = h;
-    ctx->on_destroy.push_back(destroy_handles);
-  }
-  if (!ctx->solver) {
-    cusolverDnHandle_t h;
-    solver_check(cusolverDnCreate(&h), "cusolverDnCreate");
-    solver_check(cusolverDnSetStream(h, ctx->stream), "cusolverDnSetStream");
-    ctx->solver = h;
-  }
-}
 
 // ---- small device kernels ---------------------------------------------------
 __global__ void records_kernel(const double* __restrict__ X, const double* __restrict__ sqn,
@@ -219,11 +186,6 @@ __global__ void woodbury_z_kernel(const double* __restrict__ F, int64_t ldf, int
     s = warp_sum_xor(s);
     if (lane == 0) z[i] = (r[i] - s) / mu;
   }
-}
-
-__global__ void add_diag_kernel(double* a, int k, double mu) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < k) a[(int64_t)i * k + i] += mu;
 }
 
 // X (host, any layout) -> packed device points [n][dpad] + norms; rejects non-finite.
@@ -436,31 +398,24 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
     // ---- preconditioner core = F^T F + mu I, Cholesky (krr.hpp:33-44) ----
     const double* F = k > 0 ? res->shards[0].F.as<double>() : nullptr;
     const int64_t ldf = k > 0 ? res->ldf : 0;
-    DBuf core, work, info, tvec, part_k;
-    int lwork = 0;
+    DBuf core, scratch, info, tvec, part_k;
+    int64_t kc = 0;
     if (k > 0) {
-      ensure_handles(ctx);
-      auto hb = static_cast<cublasHandle_t>(ctx->blas);
-      auto hs2 = static_cast<cusolverDnHandle_t>(ctx->solver);
-      core = DBuf(ctx, sizeof(double) * k * k);
-      const double one = 1.0, zero = 0.0;
-      // row-major F [n][ldf] is the column-major k x n matrix F^T (lda = ldf): F^T F = A A^T
-      blas_check(cublasDsyrk(hb, CUBLAS_FILL_MODE_LOWER, CUBLAS_OP_N, (int)k, (int)n, &one, F,
-                             (int)ldf, &zero, core.as<double>(), (int)k), "cublasDsyrk");
-      add_diag_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(core.as<double>(), (int)k, mu);
-      solver_check(cusolverDnDpotrf_bufferSize(hs2, CUBLAS_FILL_MODE_LOWER, (int)k,
-                                               core.as<double>(), (int)k, &lwork),
-                   "potrf_bufferSize");
-      work = DBuf(ctx, sizeof(double) * std::max(lwork, 1));
+      kc = core_dim((int)k);
+      core = DBuf(ctx, sizeof(double) * kc * kc);
+      scratch = DBuf(ctx, sizeof(double) * core_syrk_scratch_doubles((int)k));
+      launch_core_syrk(F, ldf, n, (int)k, mu, core.as<double>(), scratch.as<double>(), st);
       info = DBuf(ctx, sizeof(int));
-      solver_check(cusolverDnDpotrf(hs2, CUBLAS_FILL_MODE_LOWER, (int)k, core.as<double>(), (int)k,
-                                    work.as<double>(), lwork, info.as<int>()),
-                   "cusolverDnDpotrf");
+      CK(cudaMemsetAsync(info.p, 0, sizeof(int), st));
+      launch_core_potrf(core.as<double>(), kc, info.as<int>(), st);
       int hinfo = 0;
       CK(cudaMemcpyAsync(&hinfo, info.p, sizeof(int), cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
+      CK(cudaGetLastError());
       if (hinfo != 0) raise(RPC_ENUMERIC, "Preconditioner: core factorization failed");
-      tvec = DBuf(ctx, sizeof(double) * k);
+      scratch.release();
+      tvec = DBuf(ctx, sizeof(double) * kc);
+      CK(cudaMemsetAsync(tvec.p, 0, sizeof(double) * kc, st));  // padding stays 0
       part_k = DBuf(ctx, sizeof(double) * (size_t)nb * k);
     }
     const double pmu = k > 0 ? mu : 1.0;  // Preconditioner::identity() has mu = 1
@@ -472,16 +427,11 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
       ft_r_partial_kernel<<<nb, 256, 0, st>>>(F, ldf, n, (int)k, r, part_k.as<double>());
       ft_r_finish_kernel<<<(unsigned)((k + 255) / 256), 256, 0, st>>>(part_k.as<double>(), nb,
                                                                       (int)k, tvec.as<double>());
-      solver_check(cusolverDnDpotrs(static_cast<cusolverDnHandle_t>(ctx->solver),
-                                    CUBLAS_FILL_MODE_LOWER, (int)k, 1, core.as<double>(), (int)k,
-                                    tvec.as<double>(), (int)k, info.as<int>()),
-                   "cusolverDnDpotrs");
+      launch_core_potrs(core.as<double>(), kc, tvec.as<double>(), st);
       woodbury_z_kernel<<<nb, 256, sizeof(double) * k, st>>>(F, ldf, n, (int)k, tvec.as<double>(),
                                                              r, mu, z);
     };
-    if (k > 0 && sizeof(double) * k > 48 * 1024)
-      CK(cudaFuncSetAttribute(woodbury_z_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(sizeof(double) * k)));
+    if (k > 0) ensure_smem_attr((const void*)woodbury_z_kernel, (int)(sizeof(double) * k));
 
     // ---- PCG on (A + mu I) beta = y (krr.hpp:87-123) ----
     const int64_t ldv = round_up(n, 16);

@@ -436,13 +436,8 @@ int launch_lowmem_t(const LowmemParams& p, cudaStream_t st) {
   int S = C::kMaxStages;
   while (S >= 2 && C::smem_bytes(S, nD) > kMaxSmem) --S;
   if (S < 2) return -1;  // dimension too large for a resident tile
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(lowmem_kernel<WC, NFW, GRAM, G, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             kMaxSmem) != cudaSuccess)
-      return -2;
-    attr = true;
-  }
+  const void* kfn = (const void*)lowmem_kernel<WC, NFW, GRAM, G, MINB>;
+  if (ensure_smem_attr(kfn, kMaxSmem) != cudaSuccess) return -2;
   CUtensorMap mX, mXS, mW;
   bool ok = make_map(&mX, p.X, p.dpad, p.n_loc, p.dpad, C::BM) &&
             make_map(&mXS, p.piv + 2, p.dpad, p.knew, p.prec, 16) &&
@@ -451,12 +446,7 @@ int launch_lowmem_t(const LowmemParams& p, cudaStream_t st) {
   const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
   // persistent grid: as many CTAs per SM as registers and shared memory allow (small m, as in
   // the KRR product mode, fits two, which hides the latency of the short per-chunk chains)
-  int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, lowmem_kernel<WC, NFW, GRAM, G, MINB>, C::NT,
-                                                    C::smem_bytes(S, nD)) != cudaSuccess || occ < 1) {
-    cudaGetLastError();
-    occ = 1;
-  }
+  const int occ = cached_occupancy(kfn, C::NT, C::smem_bytes(S, nD), 1);
   const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
   if (grid)
     lowmem_kernel<WC, NFW, GRAM, G, MINB><<<grid, C::NT, C::smem_bytes(S, nD), st>>>(p, S, mX, mXS, mW);

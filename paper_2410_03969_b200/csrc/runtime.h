@@ -3,6 +3,7 @@
 // buffers, the row-shard layout and the factorization result handle.
 #pragma once
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <chrono>
@@ -67,6 +68,14 @@ inline void dbg(cudaStream_t st, const char* what) {
 
 inline int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
 
+// NVTX range for profilers (header-only NVTX v3; a no-op unless a tool is attached).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 }  // namespace rpcb_rt
 using namespace rpcb_rt;
 
@@ -76,6 +85,10 @@ struct rpc_ctx {
   cudaStream_t copy_stream = nullptr;  // factor streaming to the host (overlaps the rounds)
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
+  bool hostcoll = false;      // collectives through caller-provided host callbacks
+  rpc_host_collectives hc{};
+  void* hc_pinned = nullptr;  // staging for host collectives (send | recv)
+  size_t hc_pinned_bytes = 0;
   int nvirt = 1;
   std::mutex mu;
   std::string err;
@@ -84,8 +97,6 @@ struct rpc_ctx {
   size_t host_pinned_bytes = 0;
   void* io_pinned = nullptr;  // RPCF writer staging (2 halves), grown on demand
   size_t io_pinned_bytes = 0;
-  void* blas = nullptr;    // cublasHandle_t (KRR preconditioner, created on first use)
-  void* solver = nullptr;  // cusolverDnHandle_t
   std::vector<void (*)(rpc_ctx*)> on_destroy;
 
   int nshards() const { return world * nvirt; }
@@ -115,6 +126,7 @@ struct rpc_ctx {
   }
   void trim() {
     cudaStreamSynchronize(stream);
+    if (copy_stream) cudaStreamSynchronize(copy_stream);
     for (auto& kv : pool) cudaFree(kv.second);
     pool.clear();
   }
@@ -229,11 +241,68 @@ inline int guarded(rpc_ctx* ctx, F&& f) {
   }
 }
 
+// ---- collectives across the ranks of a context ------------------------------------
+// Two are needed: an in-place allgather of per-shard slots (chunk totals,
+// ||G||^2 partials, the replay-mode residual diagonal) and an in-place "owner" reduce, where
+// at most one rank holds a non-zero word per position (proposal records, chol rows, flags):
+// NCCL reduces the bit patterns as uint64 with max, which returns the owner's word bit for
+// bit (signed zeros and NaN payloads included).  World 1 (virtual shards) needs neither.
+inline void* hc_staging(rpc_ctx* ctx, size_t bytes) {
+  if (bytes > ctx->hc_pinned_bytes) {
+    if (ctx->hc_pinned) cudaFreeHost(ctx->hc_pinned);
+    ctx->hc_pinned = nullptr;
+    ctx->hc_pinned_bytes = 0;
+    CK(cudaMallocHost(&ctx->hc_pinned, bytes));
+    ctx->hc_pinned_bytes = bytes;
+  }
+  return ctx->hc_pinned;
+}
+
 // Allgather of `count` doubles per global shard, in place in buf[P][count].
 inline void allgather(rpc_ctx* ctx, double* buf, size_t count) {
   if (ctx->world == 1) return;  // virtual shards already write into buf directly
-  NK(ncclAllGather(buf + (size_t)ctx->rank * ctx->nvirt * count, buf, count * ctx->nvirt,
-                   ncclDouble, ctx->comm, ctx->stream));
+  const size_t mine = count * ctx->nvirt, off = (size_t)ctx->rank * mine;
+  if (!ctx->hostcoll) {
+    NK(ncclAllGather(buf + off, buf, mine, ncclDouble, ctx->comm, ctx->stream));
+    return;
+  }
+  const size_t bytes = sizeof(double) * mine;
+  char* h = static_cast<char*>(hc_staging(ctx, bytes * (1 + ctx->world)));
+  CK(cudaMemcpyAsync(h, buf + off, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->hc.allgather(ctx->hc.user, h, h + bytes, bytes) != 0)
+    raise(RPC_ENCCL, "host collective allgather failed");
+  CK(cudaMemcpyAsync(buf, h + bytes, bytes * ctx->world, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // h is reused by the next collective
+}
+
+// In-place owner reduce of `words` 64-bit words (see above).
+inline void allreduce_owner(rpc_ctx* ctx, void* buf, size_t words) {
+  if (ctx->world == 1 || words == 0) return;
+  if (!ctx->hostcoll) {
+    NK(ncclAllReduce(buf, buf, words, ncclUint64, ncclMax, ctx->comm, ctx->stream));
+    return;
+  }
+  const size_t bytes = sizeof(uint64_t) * words;
+  uint64_t* h = static_cast<uint64_t*>(hc_staging(ctx, bytes));
+  CK(cudaMemcpyAsync(h, buf, bytes, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  if (ctx->hc.allreduce_or_u64(ctx->hc.user, h, words) != 0)
+    raise(RPC_ENCCL, "host collective allreduce failed");
+  CK(cudaMemcpyAsync(buf, h, bytes, cudaMemcpyHostToDevice, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));  // h is reused by the next collective
+}
+
+// Host flag agreed by every rank (OR): lets all ranks raise together instead of leaving
+// the others blocked in the next collective.  `scratch` is an 8-byte device word.
+inline bool any_rank(rpc_ctx* ctx, bool flag, void* scratch) {
+  if (ctx->world == 1) return flag;
+  uint64_t v = flag ? 1 : 0;
+  CK(cudaMemcpyAsync(scratch, &v, sizeof v, cudaMemcpyHostToDevice, ctx->stream));
+  allreduce_owner(ctx, scratch, 1);
+  CK(cudaMemcpyAsync(&v, scratch, sizeof v, cudaMemcpyDeviceToHost, ctx->stream));
+  CK(cudaStreamSynchronize(ctx->stream));
+  return v != 0;
 }
 
 inline void validate(int64_t n, int64_t d, const rpc_kernel_spec& k, rpc_run_config& cfg, int& kind) {

@@ -155,46 +155,45 @@ void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* t
                                                            chunk_g2, fp);
 }
 
-// Serial chunk-offset chain (fixed order => p-invariant).  The totals are first staged
-// in shared memory by the whole CTA so the single-thread chain never waits on HBM.
+// Serial chunk-offset chain (fixed order => p-invariant).  The totals are staged in
+// shared memory by the whole CTA, one fixed-size tile at a time, so the single-thread
+// chain never waits on HBM and any number of chunks (any N) fits; the chain carries
+// across tiles in the same order, so the results do not depend on the tile size.
+constexpr int kPrefixTile = 2048;
 __global__ void __launch_bounds__(1024) chunk_prefix_kernel(const double* __restrict__ totals,
                                                             const double* g2_all, int n_chunks,
                                                             double* __restrict__ chunk_end,
                                                             ScanStatus* status) {
-  extern __shared__ double st[];  // [n_chunks] totals, [n_chunks] g2 partials
-  double* sg = st + n_chunks;
-  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) {
-    st[c] = totals[c];
-    sg[c] = g2_all ? g2_all[c] : 0.0;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double off = 0.0, g2 = 0.0;
-    for (int c = 0; c < n_chunks; ++c) {
-      off = __dadd_rn(off, st[c]);
-      st[c] = off;
-      g2 = __dadd_rn(g2, sg[c]);
+  __shared__ double st[kPrefixTile], sg[kPrefixTile];
+  double off = 0.0, g2 = 0.0;  // live in thread 0
+  for (int t0 = 0; t0 < n_chunks; t0 += kPrefixTile) {
+    const int nt = min(kPrefixTile, n_chunks - t0);
+    for (int c = threadIdx.x; c < nt; c += blockDim.x) {
+      st[c] = totals[t0 + c];
+      sg[c] = g2_all ? g2_all[t0 + c] : 0.0;
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int c = 0; c < nt; ++c) {
+        off = __dadd_rn(off, st[c]);
+        st[c] = off;
+        g2 = __dadd_rn(g2, sg[c]);
+      }
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nt; c += blockDim.x) chunk_end[t0 + c] = st[c];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
     status->total = off;
     status->g2_prev = g2;
     status->exhausted = !(off > 0.0);
   }
-  __syncthreads();
-  for (int c = threadIdx.x; c < n_chunks; c += blockDim.x) chunk_end[c] = st[c];
 }
 
 void launch_chunk_prefix(const double* totals_all, const double* g2_all, int n_chunks,
                          double* chunk_end, ScanStatus* status, cudaStream_t st) {
-  const size_t smem = sizeof(double) * 2 * (size_t)n_chunks;
-  if (smem > 48 * 1024) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(chunk_prefix_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-      attr = true;
-    }
-  }
-  chunk_prefix_kernel<<<1, 1024, smem, st>>>(totals_all, g2_all, n_chunks, chunk_end, status);
+  chunk_prefix_kernel<<<1, 1024, 0, st>>>(totals_all, g2_all, n_chunks, chunk_end, status);
 }
 
 // Copies the sampled point's record (id, ||x||^2, x, F row) into rec.
@@ -310,9 +309,10 @@ void launch_replay_scan(const double* u, int64_t n, double* cumsum, ScanStatus* 
 
 __global__ void replay_sample_kernel(SampleParams p, const double* __restrict__ cumsum) {
   __shared__ int64_t s_idx;
+  __shared__ int s_owner;
   const int j = blockIdx.x;
   if (threadIdx.x == 0) {
-    const int64_t n = p.n_loc;
+    const int64_t n = p.n_global;
     const double total = cumsum[n - 1];
     const double target = __dmul_rn(u01(splitmix64_draw(p.seed, p.draw0 + (uint64_t)j)), total);
     int64_t lo = 0, hi = n;
@@ -323,29 +323,21 @@ __global__ void replay_sample_kernel(SampleParams p, const double* __restrict__ 
     int64_t idx = lo;
     if (idx >= n) idx = n - 1;
     while (idx > 0 && cumsum[idx] == cumsum[idx - 1]) --idx;
+    // owner: the shard whose chunk range holds the drawn row
+    const int64_t chunk = idx / kChunk;
+    int o = 0;
+    while (o + 1 < p.n_shards && p.shard_chunk0[o + 1] <= chunk) ++o;
     s_idx = idx;
-    p.owner[j] = 0;
+    s_owner = o;
+    p.owner[j] = o;
   }
   __syncthreads();
-  write_record(p, s_idx, p.records + (int64_t)j * p.lay.rec);
+  if (s_owner != p.shard) return;
+  write_record(p, s_idx - p.row0, p.records + (int64_t)j * p.lay.rec);
 }
 
 void launch_replay_sample(const SampleParams& p, const double* cumsum, cudaStream_t st) {
   replay_sample_kernel<<<p.b, 128, 0, st>>>(p, cumsum);
-}
-
-__global__ void select_kernel(const double* __restrict__ recv, int64_t slot_stride,
-                              const int* __restrict__ owner, int64_t rec, int64_t words,
-                              double* __restrict__ prop) {
-  const int j = blockIdx.x;
-  const double* src = recv + (int64_t)owner[j] * slot_stride + (int64_t)j * rec;
-  double* dst = prop + (int64_t)j * rec;
-  for (int64_t i = threadIdx.x; i < words; i += blockDim.x) dst[i] = src[i];
-}
-
-void launch_select(const double* recv, int64_t slot_stride, const int* owner, int b,
-                   int64_t rec, int64_t words, double* prop, cudaStream_t st) {
-  select_kernel<<<b, 256, 0, st>>>(recv, slot_stride, owner, rec, words, prop);
 }
 
 // ---- utilities ---------------------------------------------------------------
@@ -423,39 +415,43 @@ void launch_f_to_colmajor(const double* F, int64_t ldf, int64_t n_loc, int c0, i
 
 // src: this shard's rows, either row-major [n_loc][ld_src] or column-major
 // [d][ld_src].  Output padded row-major X and ||x||^2 in ascending coordinate
-// order without FMA contraction (oracle.hpp:252).  A CTA stages kPackRows rows
-// through shared memory so both the read and the padded write are coalesced.
+// order without FMA contraction (oracle.hpp:252).  A CTA stages `rows` rows
+// through shared memory so both the read and the padded write are coalesced; the
+// row count shrinks with d so the tile fits, and very wide points (one row > the
+// shared-memory budget) take the per-row kernel below.
 constexpr int kPackRows = 64;
+constexpr int kPackSmem = 200 * 1024;
 __global__ void __launch_bounds__(256) pack_points_kernel(const double* __restrict__ src,
                                                           int64_t n_loc, int d, int64_t ld_src,
                                                           int src_row_major, int64_t dpad,
-                                                          double* __restrict__ X,
+                                                          int rows, double* __restrict__ X,
                                                           double* __restrict__ sqn,
                                                           int* nonfinite) {
-  extern __shared__ double tile[];  // [kPackRows][dpad]
-  const int64_t r0 = (int64_t)blockIdx.x * kPackRows;
-  const int nr = (int)lmin(kPackRows, n_loc - r0);
+  extern __shared__ double tile[];  // [rows][dpad]
+  const int64_t r0 = (int64_t)blockIdx.x * rows;
+  const int nr = (int)lmin(rows, n_loc - r0);
   const int tid = threadIdx.x;
   bool bad = false;
+  const int64_t tot = (int64_t)nr * dpad;
   if (src_row_major) {
-    for (int i = tid; i < nr * (int)dpad; i += blockDim.x) {
-      const int r = i / (int)dpad, c = i % (int)dpad;
+    for (int64_t i = tid; i < tot; i += blockDim.x) {
+      const int64_t r = i / dpad, c = i % dpad;
       double v = 0.0;
       if (c < d) v = src[(r0 + r) * ld_src + c];
       bad |= !isfinite(v);
       tile[i] = v;
     }
   } else {
-    for (int i = tid; i < nr * (int)dpad; i += blockDim.x) {
-      const int c = i / nr, r = i % nr;
+    for (int64_t i = tid; i < tot; i += blockDim.x) {
+      const int64_t c = i / nr, r = i % nr;
       double v = 0.0;
-      if (c < d) v = src[(int64_t)c * ld_src + r0 + r];
+      if (c < d) v = src[c * ld_src + r0 + r];
       bad |= !isfinite(v);
       tile[r * dpad + c] = v;
     }
   }
   __syncthreads();
-  for (int i = tid; i < nr * (int)dpad; i += blockDim.x) X[r0 * dpad + i] = tile[i];
+  for (int64_t i = tid; i < tot; i += blockDim.x) X[r0 * dpad + i] = tile[i];
   if (tid < nr) {
     double s = 0.0;
     for (int c = 0; c < d; ++c) {
@@ -467,19 +463,44 @@ __global__ void __launch_bounds__(256) pack_points_kernel(const double* __restri
   if (bad && nonfinite) atomicOr(nonfinite, 1);
 }
 
+// One CTA per point for dpad beyond the shared-memory tile: copy (coalesced for row-major
+// sources), then the ascending-order norm by one thread from the packed row.
+__global__ void __launch_bounds__(256) pack_row_kernel(const double* __restrict__ src, int d,
+                                                       int64_t ld_src, int src_row_major,
+                                                       int64_t dpad, double* __restrict__ X,
+                                                       double* __restrict__ sqn, int* nonfinite) {
+  const int64_t r = blockIdx.x;
+  bool bad = false;
+  double* xr = X + r * dpad;
+  for (int64_t c = threadIdx.x; c < dpad; c += blockDim.x) {
+    double v = 0.0;
+    if (c < d) v = src_row_major ? src[r * ld_src + c] : src[c * ld_src + r];
+    bad |= !isfinite(v);
+    xr[c] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int c = 0; c < d; ++c) s = __dadd_rn(s, __dmul_rn(xr[c], xr[c]));
+    sqn[r] = s;
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+}
+
 void launch_pack_points(const double* src, int64_t n_loc, int d, int64_t ld_src,
                         int src_row_major, int64_t dpad, double* X, double* sqn,
                         int* nonfinite, cudaStream_t st) {
   if (n_loc <= 0) return;
-  const size_t smem = sizeof(double) * kPackRows * (size_t)dpad;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(pack_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         200 * 1024);
-    attr = true;
+  const int rows = (int)lmin(kPackRows, kPackSmem / (int64_t)(sizeof(double) * dpad));
+  if (rows < 1) {
+    pack_row_kernel<<<(unsigned)n_loc, 256, 0, st>>>(src, d, ld_src, src_row_major, dpad, X, sqn,
+                                                     nonfinite);
+    return;
   }
-  pack_points_kernel<<<(unsigned)((n_loc + kPackRows - 1) / kPackRows), 256, smem, st>>>(
-      src, n_loc, d, ld_src, src_row_major, dpad, X, sqn, nonfinite);
+  const size_t smem = sizeof(double) * rows * (size_t)dpad;
+  ensure_smem_attr((const void*)pack_points_kernel, kPackSmem);
+  pack_points_kernel<<<(unsigned)((n_loc + rows - 1) / rows), 256, smem, st>>>(
+      src, n_loc, d, ld_src, src_row_major, dpad, rows, X, sqn, nonfinite);
 }
 
 __global__ void fill_kernel(double* p, int64_t n, double v) {

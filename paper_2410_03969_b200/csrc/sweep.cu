@@ -300,11 +300,7 @@ void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const d
   } else {
     hpg = scratch_hp;  // global (L2-resident) fallback for large blocks
   }
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(sweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 214 * 1024);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)sweep_kernel, 214 * 1024);
   sweep_kernel<<<1, kSweepThreads, smem, st>>>(H, b, seed, draw0, prop, lay, pos, acc_ids, lcol,
                                                 lacc_cm, out, hpg, accept_all, pub_scan,
                                                 pub_host);
@@ -394,11 +390,7 @@ __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __r
 template <int NQ>
 static void linv_launch(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
                         int64_t ldl, int koff, double* linv_rm, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(linv_kernel<NQ>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  ensure_smem_attr((const void*)linv_kernel<NQ>, 200 * 1024);
   const size_t bytes = sizeof(double) * (size_t)m_max * m_max;
   const int in_smem = bytes <= 200 * 1024;
   linv_kernel<NQ><<<(m_max + kLinvWarps - 1) / kLinvWarps, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(

@@ -623,27 +623,11 @@ inline bool make_map(CUtensorMap* m, const double* base, uint64_t inner, uint64_
   return r == CUDA_SUCCESS;
 }
 
-inline int num_sms() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
-
 template <int WC, int NFW, bool GRAM, int MINB, int G, bool COLS = false>
 int launch_t(const UpdateParams& p, cudaStream_t st) {
   using C = UCfg<WC, NFW, G>;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(update_kernel<WC, NFW, GRAM, MINB, G, COLS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             C::SMEM) != cudaSuccess)
-      return -2;
-    attr = true;
-  }
+  const void* kfn = (const void*)update_kernel<WC, NFW, GRAM, MINB, G, COLS>;
+  if (ensure_smem_attr(kfn, C::SMEM) != cudaSuccess) return -2;
   CUtensorMap mX, mXS, mF, mFS, mG, mL;
   bool ok = make_map(&mX, p.X, p.dpad, p.n_loc, p.dpad, C::BM) &&
             make_map(&mXS, p.xs, p.dpad, C::NB, p.dpad, C::NB) &&
@@ -656,14 +640,7 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
   const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
   // persistent grid sized by occupancy: small m (early rounds, kernel-column bench) fits two
   // CTAs per SM, which hides the latency of the short per-tile chains
-  static int occ = 0;
-  if (!occ) {
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, update_kernel<WC, NFW, GRAM, MINB, G, COLS>,
-                                                      C::NT, C::SMEM) != cudaSuccess || occ < 1) {
-      cudaGetLastError();
-      occ = MINB;
-    }
-  }
+  const int occ = cached_occupancy(kfn, C::NT, C::SMEM, MINB);
   const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
   if (grid)
     update_kernel<WC, NFW, GRAM, MINB, G, COLS><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);

@@ -238,3 +238,39 @@ def test_two_rank_factorization_matches_one_rank_and_reference(kernel, sigma):
     assert [list(a) for a in ref.accepted] == [list(a) for a in two["accepted"]]
     assert np.linalg.norm(ref.factor - f2) <= 1e-10 * np.linalg.norm(ref.factor)
     assert np.max(np.abs(ref.residual_diag - u2)) <= 1e-10
+
+
+def _hostcoll_main(rank, world, port, out_q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2410_03969_b200.hostcoll import TorchHostCollectives
+    hc = TorchHostCollectives()
+    send = np.arange(10, dtype=np.uint8) + 16 * rank
+    gathered = hc.allgather(send)
+    # owner reduce: rank r owns words r, r+2, ...; negative doubles, -0.0 and NaN payloads
+    # must come back bit for bit (the library reduces fp64 records this way)
+    vals = np.array([-1.5, -0.0, np.nan, 3.25, -np.inf, 1e-310], dtype=np.float64)
+    buf = np.zeros(vals.size, dtype=np.uint64)
+    own = np.arange(vals.size) % world == rank
+    buf[own] = vals.view(np.uint64)[own]
+    hc.allreduce_or(buf)
+    out_q.put((rank, gathered.tolist(), buf.tolist()))
+    dist.destroy_process_group()
+
+
+def test_host_collectives_adapter_two_ranks():
+    """paper_2410_03969_b200/hostcoll.py, the transport of rpc_create_hostcoll, at world 2."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_hostcoll_main, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = [q.get(timeout=120) for _ in ps]
+    for p in ps:
+        p.join(timeout=60)
+    vals = np.array([-1.5, -0.0, np.nan, 3.25, -np.inf, 1e-310], dtype=np.float64)
+    for rank, gathered, buf in res:
+        assert gathered == list(range(10)) + list(range(16, 26))
+        assert np.array_equal(np.array(buf, dtype=np.uint64), vals.view(np.uint64))
