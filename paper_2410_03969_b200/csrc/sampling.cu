@@ -279,32 +279,64 @@ void launch_sample(const SampleParams& p, cudaStream_t st) {
 }
 
 // ---- replay mode -----------------------------------------------------------
-__global__ void replay_scan_kernel(const double* __restrict__ u, int64_t n,
-                                   double* __restrict__ cumsum, ScanStatus* status) {
-  if (threadIdx.x != 0) return;
-  double acc = 0.0;
-  int64_t i = 0;
-  for (; i + 8 <= n; i += 8) {
-    double v[8];
+// The reference's strictly sequential scan (acc += w[i], rng.hpp:67-75) on one thread,
+// fed from shared memory: while thread 0 runs the dependent add chain over block b, the
+// other warps stage block b+1 from HBM and write block b-1's prefix out (coalesced), so
+// the chain never waits on a global load.
+constexpr int kReplayBlk = 1024;
+__global__ void __launch_bounds__(256) replay_scan_kernel(const double* __restrict__ u, int64_t n,
+                                                          double* __restrict__ cumsum,
+                                                          ScanStatus* status) {
+  __shared__ double in[2][kReplayBlk], out[2][kReplayBlk];
+  const int64_t nblk = (n + kReplayBlk - 1) / kReplayBlk;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < kReplayBlk; i += blockDim.x) in[0][i] = i < n ? __ldg(u + i) : 0.0;
+  __syncthreads();
+  double acc = 0.0;  // thread 0
+  for (int64_t b = 0; b < nblk; ++b) {
+    const int cur = (int)(b & 1);
+    if (tid == 0) {
+      const int nv = (int)lmin(kReplayBlk, n - b * kReplayBlk);
+      const double* src = in[cur];
+      double* dst = out[cur];
+      int i = 0;
+      for (; i + 16 <= nv; i += 16) {
+        double v[16];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) v[q] = __ldg(u + i + q);
+        for (int q = 0; q < 16; ++q) v[q] = src[i + q];
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      acc = __dadd_rn(acc, v[q]);
-      cumsum[i + q] = acc;
+        for (int q = 0; q < 16; ++q) {
+          acc = __dadd_rn(acc, v[q]);
+          dst[i + q] = acc;
+        }
+      }
+      for (; i < nv; ++i) {
+        acc = __dadd_rn(acc, src[i]);
+        dst[i] = acc;
+      }
+    } else if (tid >= 32) {
+      const int t = tid - 32, nt = blockDim.x - 32;
+      const int64_t nb0 = (b + 1) * kReplayBlk;  // stage the next block
+      if (b + 1 < nblk)
+        for (int i = t; i < kReplayBlk; i += nt) in[cur ^ 1][i] = nb0 + i < n ? __ldg(u + nb0 + i) : 0.0;
+      if (b > 0) {  // write the previous block's prefix
+        const int64_t pb0 = (b - 1) * kReplayBlk;
+        for (int i = t; i < kReplayBlk; i += nt) cumsum[pb0 + i] = out[cur ^ 1][i];
+      }
     }
+    __syncthreads();
   }
-  for (; i < n; ++i) {
-    acc = __dadd_rn(acc, u[i]);
-    cumsum[i] = acc;
+  const int64_t lb0 = (nblk - 1) * kReplayBlk;  // last block
+  for (int64_t i = tid; i < n - lb0; i += blockDim.x) cumsum[lb0 + i] = out[(nblk - 1) & 1][i];
+  if (tid == 0) {
+    status->total = acc;
+    status->exhausted = !(acc > 0.0);
   }
-  status->total = acc;
-  status->exhausted = !(acc > 0.0);
 }
 
 void launch_replay_scan(const double* u, int64_t n, double* cumsum, ScanStatus* status,
                         cudaStream_t st) {
-  replay_scan_kernel<<<1, 32, 0, st>>>(u, n, cumsum, status);
+  replay_scan_kernel<<<1, 256, 0, st>>>(u, n, cumsum, status);
 }
 
 __global__ void replay_sample_kernel(SampleParams p, const double* __restrict__ cumsum) {

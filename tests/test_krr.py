@@ -4,7 +4,7 @@ Pins: tests/golden/ref_krr_*.npz were produced by the reference's own fit_krr + 
 (krr.hpp:177-250, compiled here against the Eigen-API shim: tests/golden/make_ref_fixtures.py),
 for its dense-matvec path (n <= materialize_threshold) and its on-the-fly path ("lazy").
 The GPU computes every matvec on the fly with a different summation order, and builds the
-Woodbury core with cuBLAS/cuSOLVER, so PCG iterates differ from the reference's in the last
+Woodbury core with its own DMMA SYRK and blocked Cholesky (krr_core.cu), so PCG iterates differ from the reference's in the last
 bits and those differences are amplified by the solve.  Bars: coefficients and predictions
 within 1e-6 relative (the reference's own bar between its two matvec paths,
 test_krr.cpp:172-189; measured ~1e-8); iteration count within 1; residual histories within
