@@ -443,7 +443,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // queue them before the status read so they run while the host waits.
     CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
     launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, lowmem ? 0 : (int)(kcur & 1),
-                    linv.as<double>(), st);
+                    linv.as<double>(), st, lowmem ? 0 : 1);
     ++launches;
     if (!lowmem) {
       launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, 0, (int)dpad,

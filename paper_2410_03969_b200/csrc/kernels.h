@@ -96,14 +96,28 @@ void launch_add_diag(double* H, int b, double shift, cudaStream_t st);
 // out[j] = first `words` of record prop[idx[j]] (stride rec), j < m
 void launch_gather_records(const double* prop, int64_t rec, int64_t words, const int* idx, int m,
                            double* out, cudaStream_t st);
-// linv_rm[perm_row(a)][c + koff] = (L^{-1})[a][c], [nb][ldl], zero elsewhere (koff = kcur & 1,
-// matching the update kernel's 16-byte-aligned phase-2 tiles).
+// The update kernel forms A(R,S) L^{-T} with A(R,S) still in registers when it runs with a
+// single warp column (m <= 128): the C-fragment columns a lane holds become its A-operand k
+// values, so L^{-1}'s columns are stored in that order inside each 16-column chunk (kslot16).
+// Otherwise (m > 128) A(R,S) is parked in F and streamed back from column kcur - koff,
+// koff = kcur & 1 (16-byte-aligned TMA boxes), and L^{-1} is stored shifted by koff.
+__host__ __device__ inline bool update_regp2(int m) { return m >= 1 && m <= 128; }
+// slot of column c inside its 16-column chunk: c % 16 = 8h + 2t + v  ->  4 (2h + v) + t
+__host__ __device__ inline int kslot16(int c) {
+  return (c & ~15) + 4 * (2 * ((c >> 3) & 1) + (c & 1)) + ((c >> 1) & 3);
+}
+// column of the [nb][ldl] L^{-1} buffer holding L^{-1}(:, c); perm = 0 forces natural + koff
+// (the low-memory path's own use of L^{-1})
+__host__ __device__ inline int linv_slot(int c, int m, int koff, int perm) {
+  return (perm && update_regp2(m)) ? kslot16(c) : c + koff;
+}
+// linv_rm[perm_row(a)][linv_slot(c)] = (L^{-1})[a][c], [nb][ldl], zero elsewhere.
 void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
-                 cudaStream_t st);
+                 cudaStream_t st, int perm = 1);
 // Same with the accepted count read on the device (*m_dev <= m_max): launched right after
 // the sweep, before the host learns m.
 void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb, int64_t ldl,
-                     int koff, double* linv_rm, cudaStream_t st);
+                     int koff, double* linv_rm, cudaStream_t st, int perm = 1);
 
 // ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
 struct UpdateParams {

@@ -317,7 +317,7 @@ template <int NQ>
 __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __restrict__ lacc_cm,
                                                                int m_host, const int* m_dev,
                                                                int nb, int64_t ldl, int koff,
-                                                               int in_smem,
+                                                               int perm, int in_smem,
                                                                double* __restrict__ linv_rm) {
   extern __shared__ double smem_l[];  // column-major m x m copy when it fits
   const int m = m_dev ? *m_dev : m_host;
@@ -379,42 +379,43 @@ __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __r
       x[q] = (a == t) ? xt : ((a > t) ? nx : x[q]);
     }
   }
+  const int col = linv_slot(c, m, koff, perm);
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     const int a = lane + 32 * q;
-    if (a < nb) linv_rm[(int64_t)perm_row(a) * ldl + c + koff] = (a >= c && a < m) ? x[q] : 0.0;
+    if (a < nb) linv_rm[(int64_t)perm_row(a) * ldl + col] = (a >= c && a < m) ? x[q] : 0.0;
   }
-  for (int a = lane + 32 * NQ; a < nb; a += 32) linv_rm[(int64_t)perm_row(a) * ldl + c + koff] = 0.0;
+  for (int a = lane + 32 * NQ; a < nb; a += 32) linv_rm[(int64_t)perm_row(a) * ldl + col] = 0.0;
 }
 
 template <int NQ>
 static void linv_launch(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
-                        int64_t ldl, int koff, double* linv_rm, cudaStream_t st) {
+                        int64_t ldl, int koff, int perm, double* linv_rm, cudaStream_t st) {
   ensure_smem_attr((const void*)linv_kernel<NQ>, 200 * 1024);
   const size_t bytes = sizeof(double) * (size_t)m_max * m_max;
   const int in_smem = bytes <= 200 * 1024;
   linv_kernel<NQ><<<(m_max + kLinvWarps - 1) / kLinvWarps, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(
-      lacc_cm, m_host, m_dev, nb, ldl, koff, in_smem, linv_rm);
+      lacc_cm, m_host, m_dev, nb, ldl, koff, perm, in_smem, linv_rm);
 }
 
 static void linv_dispatch(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
-                          int64_t ldl, int koff, double* linv_rm, cudaStream_t st) {
-  if (m_max <= 32) linv_launch<1>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, linv_rm, st);
-  else if (m_max <= 64) linv_launch<2>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, linv_rm, st);
-  else if (m_max <= 128) linv_launch<4>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, linv_rm, st);
-  else linv_launch<8>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, linv_rm, st);
+                          int64_t ldl, int koff, int perm, double* linv_rm, cudaStream_t st) {
+  if (m_max <= 32) linv_launch<1>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, perm, linv_rm, st);
+  else if (m_max <= 64) linv_launch<2>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, perm, linv_rm, st);
+  else if (m_max <= 128) linv_launch<4>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, perm, linv_rm, st);
+  else linv_launch<8>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, perm, linv_rm, st);
 }
 
 void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, double* linv_rm,
-                 cudaStream_t st) {
+                 cudaStream_t st, int perm) {
   if (m <= 0) return;
-  linv_dispatch(lacc_cm, m, nullptr, m, nb, ldl, koff, linv_rm, st);
+  linv_dispatch(lacc_cm, m, nullptr, m, nb, ldl, koff, perm, linv_rm, st);
 }
 
 void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb, int64_t ldl,
-                     int koff, double* linv_rm, cudaStream_t st) {
+                     int koff, double* linv_rm, cudaStream_t st, int perm) {
   if (m_max <= 0) return;
-  linv_dispatch(lacc_cm, 0, m_dev, m_max, nb, ldl, koff, linv_rm, st);
+  linv_dispatch(lacc_cm, 0, m_dev, m_max, nb, ldl, koff, perm, linv_rm, st);
 }
 
 }  // namespace rpcb

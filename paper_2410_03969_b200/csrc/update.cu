@@ -23,10 +23,9 @@ int update_tile_rows(int m) {
 int launch_update(const UpdateParams& p, cudaStream_t st) {
   const int nf = std::max(1, (p.m + 7) / 8);
   if (p.columns_only && nf <= 16) return launch_update_cols(p, nf, st);
-  // 64 < m <= 96: two warp columns of half the accumulators, two CTAs per SM (measured
-  // 9% faster than the ping-pong pair at C4 rounds 1-2; slower for m > 96)
-  if (nf > 8 && nf <= 12) return launch_update_wc2(p, (nf + 1) / 2, st);
-  if (nf <= 16) return launch_update_wc1(p, nf, st);
+  // m <= 128: two ping-pong groups, one warp column, A(R,S) L^{-T} from registers
+  // (update_regp2: L^{-1} was stored in that path's column order)
+  if (update_regp2(p.m)) return launch_update_wc1(p, nf, st);
   if (nf <= 32) return launch_update_wc2(p, (nf + 1) / 2, st);
   return -1;
 }
@@ -101,15 +100,16 @@ __global__ void __launch_bounds__(256) bprime_kernel(const double* __restrict__ 
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int a = ab + a0 + kRowStep * j;
-      lr[j] = linv_rm + (int64_t)perm_row(a < m ? a : 0) * ldl + koff;
+      lr[j] = linv_rm + (int64_t)perm_row(a < m ? a : 0) * ldl;
       if (a < m) amax = a;
     }
     for (int c = 0; c <= amax; ++c) {
       const double f = sF[c * kBpCols + kk];
+      const int col = linv_slot(c, m, koff, 1);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const int a = ab + a0 + kRowStep * j;
-        if (c <= a && a < m) acc[j] = fma(__ldg(lr[j] + c), f, acc[j]);
+        if (c <= a && a < m) acc[j] = fma(__ldg(lr[j] + col), f, acc[j]);
       }
     }
 #pragma unroll

@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <cstdio>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -115,6 +116,15 @@ __device__ __forceinline__ double kfun_eval(double dd, int f, double s, const do
   return exp_tab(dd * s, tab);
 }
 
+// f(integral_constant<J>) for J = N-1 down to 0 (compile-time indices into register arrays).
+template <int J, class F>
+__device__ __forceinline__ void static_for_desc(F&& f) {
+  if constexpr (J >= 0) {
+    f(std::integral_constant<int, J>{});
+    static_for_desc<J - 1>(f);
+  }
+}
+
 // COLS: compiled for the standalone K5 only (p.columns_only): phases 1-2, the park and the
 // epilogue are compiled out, so registers go to more resident CTAs instead.
 template <int WC, int NFW, bool GRAM, int MINB, int G, bool COLS = false>
@@ -125,6 +135,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
                   const __grid_constant__ CUtensorMap tmL) {
   using C = UCfg<WC, NFW, G>;
   constexpr int BM = C::BM, S = C::S, NCW = C::NCW, GT = C::GT;
+  // REGP2 (one warp column, m <= 128): A(R,S) L^{-T} is formed in place from the registers
+  // that hold A(R,S) after the transform (no park in F, no phase-2 reload): chunk J of the
+  // triangular product only feeds output columns >= 16 J, so walking J downwards lets every
+  // chunk read its operand columns before they are overwritten by output columns.
+  constexpr bool REGP2 = (WC == 1) && !COLS;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1024-byte aligned ring (128B-swizzle atoms).  Offsets stay relative to the
   // __shared__ array so every fragment load is an LDS with an immediate offset.
@@ -152,7 +167,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
   // aligned in the inner dimension, so for odd kcur one extra leading column is
   // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
   const int koff = kcur & 1;
-  const int nL = (COLS || p.columns_only) ? 0 : (m + koff + 15) >> 4;
+  const int nL = (COLS || p.columns_only) ? 0 : REGP2 ? (m + 15) >> 4 : (m + koff + 15) >> 4;
   const int T = nX + nFk + nL;               // chunks per tile
   const int ntiles = (int)((p.n_loc + BM - 1) / BM);
   const int vb = (int)blockIdx.x * G + grp, vgrid = (int)gridDim.x * G;  // virtual block per group
@@ -195,16 +210,22 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     if (COLS ? gtid != 0 : lane != 0) return;
     while (issued < total && issued < done + (COLS ? S : S - 1)) {
       const int k = issued / T, c = issued - k * T;
-      if (c >= nX + nFk && parked <= k) break;
+      if (!REGP2 && c >= nX + nFk && parked <= k) break;
       const int s = issued % S;
       if (issued >= S) mbar_wait(&empty[s], ((issued / S) & 1) ^ 1);
       unsigned char* As = stages + s * C::STAGE;
       unsigned char* Bs = As + C::A_BYTES;
       const int r0 = (int)((vb + (int64_t)k * vgrid) * BM);
-      mbar_arrive_expect_tx(&full[s], C::STAGE);
+      const bool l_only = REGP2 && c >= nX && c < nX + nL;  // phase 2: the L^{-1} chunk only
+      mbar_arrive_expect_tx(&full[s], l_only ? C::B_BYTES : C::STAGE);
       if (c < nX) {
         tma_load_2d(As, &tmX, 16 * c, r0, &full[s]);
         tma_load_2d(Bs, &tmXS, 16 * c, 0, &full[s]);
+      } else if (l_only) {  // chunks J = nL-1 .. 0 (descending, see REGP2)
+        tma_load_2d(Bs, &tmL, 16 * (nL - 1 - (c - nX)), 0, &full[s]);
+      } else if (REGP2) {
+        tma_load_2d(As, &tmF, 16 * (c - nX - nL), r0, &full[s]);
+        tma_load_2d(Bs, &tmFS, 16 * (c - nX - nL), 0, &full[s]);
       } else if (c < nX + nFk) {
         tma_load_2d(As, &tmF, 16 * (c - nX), r0, &full[s]);
         tma_load_2d(Bs, &tmFS, 16 * (c - nX), 0, &full[s]);
@@ -410,7 +431,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
           dd = clamp_pin(dd, gid[fr], idc);
         }
         const double val = kfun_eval(dd, p.kfun, escale, s_exp2);
-        a = (col < m && rin[fr]) ? -val : 0.0;
+        a = (col < m && rin[fr]) ? (REGP2 ? val : -val) : 0.0;
       };
 #pragma unroll 1
       for (int it = 0; it + 1 < NFW; it += 2) {
@@ -480,6 +501,58 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       continue;
     }
 
+    if constexpr (REGP2) {
+      // every warp of the group passes here before the group's next epilogue (s_rowg2)
+      gsync();
+      mark(2);
+      trc(k, 3);
+      // ---- phase 2 first, in place: acc = A(R, S) L^{-T} ---------------------------
+      // Chunk J holds L^{-1}(:, 16J..16J+15) in kslot16 order, i.e. k step s of lane t is
+      // column 16J + 8(s>>1) + 2t + (s&1): exactly the accumulator element
+      // acc[fr][2J + (s>>1)][s&1] this lane holds, so the A operand needs no data movement.
+      static_for_desc<(NFW + 1) / 2 - 1>([&](auto JC) {
+        constexpr int J = decltype(JC)::value;
+        constexpr int q0 = 2 * J, q1 = 2 * J + 1;
+        if (J >= nL) return;
+        consume([&](uint32_t so) {
+          const unsigned char* Bw = stages + so + C::A_BYTES;
+          double a[4][2];
+#pragma unroll
+          for (int fr = 0; fr < 2; ++fr) {
+            a[0][fr] = acc[fr][q0][0];
+            a[1][fr] = acc[fr][q0][1];
+            acc[fr][q0][0] = acc[fr][q0][1] = 0.0;
+            if constexpr (q1 < NFW) {
+              a[2][fr] = acc[fr][q1][0];
+              a[3][fr] = acc[fr][q1][1];
+              acc[fr][q1][0] = acc[fr][q1][1] = 0.0;
+            } else {
+              a[2][fr] = a[3][fr] = 0.0;
+            }
+          }
+#pragma unroll
+          for (int q = q0; q < NFW; ++q)
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+              if (q1 >= NFW && s >= 2) continue;
+              const double bv = *reinterpret_cast<const double*>(Bw + q * 1024 + foff[s]);
+#pragma unroll
+              for (int fr = 0; fr < 2; ++fr) dmma884(acc[fr][q][0], acc[fr][q][1], a[s][fr], bv);
+            }
+        });
+      });
+      mark(4);
+      trc(k, 4);
+      // ---- phase 1: acc += F(R,:) B'^T with B' = -L^{-1} F(S,:)  (K = kcur) ----------
+#pragma unroll 1
+      for (int c = 0; c + 1 < nFk; ++c) consume([&](uint32_t so) { mma_stage(so, 0, 4); });
+      if (nFk > 0) {
+        const int ks = (kcur - 16 * (nFk - 1) + 3) / 4;
+        consume([&](uint32_t so) { mma_stage(so, 0, ks); });
+      }
+      mark(3);
+      trc(k, 5);
+    } else {
     // ---- park A(R, S) in F(R, kcur:kcur+m): phase 2 streams it back as the A operand
     // of A L^{-T}.  Parking right after the transform lets the TMA round trip hide
     // behind the residual GEMM instead of stalling the end of the tile.
@@ -524,6 +597,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 
     mark(4);
     trc(k, 5);
+    }  // !REGP2
     // ---- epilogue ------------------------------------------------------------------
     double rs[2] = {0.0, 0.0};
 #pragma unroll

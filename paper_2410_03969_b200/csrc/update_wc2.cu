@@ -9,7 +9,6 @@ int launch_update_wc2(const UpdateParams& p, int nfw, cudaStream_t st) {
   case N:                                                                       \
     return p.kind == kGaussGram ? launch_t<2, N, true, MB, 1>(p, st) : launch_t<2, N, false, MB, 1>(p, st);
   switch (nfw) {
-    RPCB_CASE(5, 2) RPCB_CASE(6, 2)
     RPCB_CASE(9, 1) RPCB_CASE(10, 1)
     RPCB_CASE(11, 1) RPCB_CASE(12, 1) RPCB_CASE(13, 1) RPCB_CASE(14, 1) RPCB_CASE(15, 1)
     RPCB_CASE(16, 1)
