@@ -66,7 +66,7 @@ enum {
                                on every shard when sharded); slower */
 };
 typedef struct {
-  int64_t block_size;  /* b >= 1 (this build: b <= 256) */
+  int64_t block_size;  /* b >= 1 (this build: b <= 1024; low-memory variant b <= 256) */
   int mode;            /* rpc_run_mode */
   int64_t rounds;      /* FixedRounds: t >= 1 */
   int64_t target_rank; /* UntilRank: k >= 1 */

@@ -60,6 +60,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   if (sink.p && lowmem) raise(RPC_EINVAL, "low-memory result has no factor to stream");
   if (lowmem && round_up(d, 16) > 128)
     raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: this build supports d <= 128");
+  if (lowmem && cfg.block_size > 256)
+    raise(RPC_EINVAL, "accelerated_rpcholesky_lowmem: this build supports block size <= 256");
   if (layout != RPC_COL_MAJOR && layout != RPC_ROW_MAJOR) raise(RPC_EINVAL, "unknown layout");
   const bool replay = (cfg.flags & RPC_FLAG_REPLAY_SCAN) != 0;
   CK(cudaSetDevice(ctx->device));
@@ -176,6 +178,14 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   DBuf xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * ldf),
       sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
   DBuf shard_c0(ctx, sizeof(int) * (P + 1));
+  // Blocks beyond 256 proposals: a round's accepted set is appended in groups of at most
+  // kGroup pivots (block Cholesky: group g is eliminated against F extended by the earlier
+  // groups' columns, whose rows at S_g are L(S_g, S_<g) from the sweep), each group one
+  // update launch; L_gg is copied out of the sweep's L for its inverse.
+  constexpr int kGroup = 128;
+  const bool grouped = b > 256 && !lowmem;
+  DBuf lsub;
+  if (grouped) lsub = DBuf(ctx, sizeof(double) * kGroup * kGroup);
   DBuf prefix_counter(ctx, sizeof(unsigned));
   CK(cudaMemsetAsync(prefix_counter.p, 0, sizeof(unsigned), st));
   DBuf kept_idx, propk;  // block / simple: kept proposals (first draw of each distinct id)
@@ -411,14 +421,16 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         res->exhausted = true;
         break;
       }
-      CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
-      launch_linv(lacc.as<double>(), mk, (int)nbl, ldl, (int)(kcur & 1), linv.as<double>(), st);
-      launch_gather_accepted(propk.as<double>(), lay, pos.as<int>(), mk, 256, 0, (int)dpad,
-                             xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
-                             idS.as<double>(), st, nullptr, gram_xscale(kind));
-      launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), propk.as<double>(), lay,
-                    pos.as<int>(), &d_sweep->m, mk, (int)kcur, fs.as<double>(), ldf, st);
-      launches += 3;
+      if (!grouped) {
+        CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+        launch_linv(lacc.as<double>(), mk, (int)nbl, ldl, (int)(kcur & 1), linv.as<double>(), st);
+        launch_gather_accepted(propk.as<double>(), lay, pos.as<int>(), mk, 256, 0, (int)dpad,
+                               xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
+                               idS.as<double>(), st, nullptr, gram_xscale(kind));
+        launch_bprime(linv.as<double>(), ldl, (int)(kcur & 1), propk.as<double>(), lay,
+                      pos.as<int>(), &d_sweep->m, mk, (int)kcur, fs.as<double>(), ldf, st);
+        launches += 3;
+      }
       CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * mk, cudaMemcpyDeviceToHost, st));
       CK(cudaStreamSynchronize(st));
     } else {
@@ -440,12 +452,15 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       CK(cudaEventRecord(ev_pub.e, st));
     }
     // L^{-1} and the accepted-pivot operands only need the sweep's device-side outputs:
-    // queue them before the status read so they run while the host waits.
-    CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
-    launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, lowmem ? 0 : (int)(kcur & 1),
-                    linv.as<double>(), st, lowmem ? 0 : 1);
-    ++launches;
-    if (!lowmem) {
+    // queue them before the status read so they run while the host waits (grouped rounds
+    // build them per group once m is known).
+    if (!grouped) {
+      CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+      launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl,
+                      lowmem ? 0 : (int)(kcur & 1), linv.as<double>(), st, lowmem ? 0 : 1);
+      ++launches;
+    }
+    if (!lowmem && !grouped) {
       launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), 0, 256, 0, (int)dpad,
                              xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
                              idS.as<double>(), st, &d_sweep->m, gram_xscale(kind));
@@ -539,6 +554,23 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           bytes += 8.0 * (N * d + 2.0 * N);
         }
       }
+      const double* recs = algo == kAlgoAccelerated ? prop.as<double>() : propk.as<double>();
+      for (int g0 = 0; g0 < m && !lowmem; g0 += grouped ? kGroup : m) {
+      const int mg = grouped ? std::min(kGroup, m - g0) : m;
+      const int64_t kg = kcur + g0;  // F columns already holding earlier groups of this round
+      if (grouped) {
+        CK(cudaMemcpy2DAsync(lsub.p, sizeof(double) * mg, lacc.as<double>() + (int64_t)g0 * m + g0,
+                             sizeof(double) * m, sizeof(double) * mg, mg, cudaMemcpyDeviceToDevice,
+                             st));
+        CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+        launch_linv(lsub.as<double>(), mg, (int)nbl, ldl, (int)(kg & 1), linv.as<double>(), st);
+        launch_gather_accepted(recs, lay, pos.as<int>() + g0, mg, 256, (int)kg, (int)dpad,
+                               xs.as<double>(), fs.as<double>(), ldf, sqnS.as<double>(),
+                               idS.as<double>(), st, nullptr, gram_xscale(kind));
+        launch_bprime(linv.as<double>(), ldl, (int)(kg & 1), recs, lay, pos.as<int>() + g0, nullptr,
+                      mg, (int)kg, fs.as<double>(), ldf, st, lacc.as<double>(), m, g0, (int)kcur);
+        launches += 3;
+      }
       for (Shard& s : res->shards) {
         if (s.n_loc == 0 || lowmem) continue;
         UpdateParams up{};
@@ -549,7 +581,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.sqn = s.sqn.as<double>();
         up.F = s.F.as<double>();
         up.ldf = ldf;
-        up.kcur = (int)kcur;
+        up.kcur = (int)kg;
         up.u = s.u.as<double>();
         up.n_loc = s.n_loc;
         up.row0 = s.row0;
@@ -558,13 +590,14 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.ldfs = ldf;
         up.sqnS = sqnS.as<double>();
         up.idS = idS.as<double>();
-        up.m = m;
+        up.m = mg;
         up.linv = linv.as<double>();
         up.ldl = ldl;
         up.sigma = kspec.sigma;
         up.kind = kind;
         up.kfun = kernel_fun(kspec, &up.escale);
         up.tile_g2 = s.tile_g2.as<double>();
+        up.g2_accum = g0 > 0;  // later groups add their ||G||^2 to the round's tile partials
         if (dbg_trace) {
           CK(cudaMemsetAsync(trace_buf.p, 0, trace_buf.bytes, st));
           up.trace = trace_buf.as<unsigned long long>();
@@ -602,12 +635,13 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         launches += 1;  // per-tile ||G||^2 -> chunks: folded into the next chunk-totals pass
         ++upd_launches;
         const double N = (double)s.n_loc;
-        const double fl = 2.0 * N * m * kcur + N * (double)m * m + 2.0 * N * m * d;
+        const double fl = 2.0 * N * mg * kg + N * (double)mg * mg + 2.0 * N * mg * d;
         flops += fl;
-        upd_info.emplace_back(m, kcur);
+        upd_info.emplace_back(mg, kg);
         upd_flops.push_back(fl);
-        bytes += 8.0 * (N * kcur + N * m + N * d + 2.0 * N);
+        bytes += 8.0 * (N * kg + N * mg + N * d + 2.0 * N);
       }
+      }  // groups
       pending_g2 = true;
       if (sink.p) {
         const auto hs0 = clk::now();
@@ -1443,7 +1477,7 @@ int rpc_rejection_sweep(rpc_ctx* ctx, const double* h, int64_t b, const int64_t*
   if (!ctx) return fail(nullptr, RPC_EINVAL, "null context");
   std::lock_guard<std::mutex> lk(ctx->mu);
   return guarded(ctx, [&] {
-    if (b < 1 || b > 256) raise(RPC_EINVAL, "rejection_sample_submatrix: size mismatch");
+    if (b < 1 || b > kMaxBlock) raise(RPC_EINVAL, "rejection_sample_submatrix: size mismatch");
     CK(cudaSetDevice(ctx->device));
     cudaStream_t st = ctx->stream;
     std::vector<double> hrm((size_t)b * b), rec((size_t)2 * b);

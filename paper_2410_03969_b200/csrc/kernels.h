@@ -12,6 +12,10 @@ enum DistKind { kGaussGram = 0, kGaussDirect = 1, kL1 = 2 };
 // Matern 5/2 (scale 1/sigma^2) of the squared l2 distance.
 enum KernelFun { kFunExp = 0, kFunMatern32 = 1, kFunMatern52 = 2 };
 
+// Largest block size b (proposals per round) this build accepts; rounds with more than 256
+// accepted pivots are appended in groups (api.cu).
+constexpr int kMaxBlock = 1024;
+
 // Proposal record layout (one per draw, fp64 words):
 //   [0] global id (exact in fp64), [1] ||x||^2, [2, 2+dpad) x, [2+dpad, 2+dpad+ldf) F row
 struct RecordLayout {
@@ -135,6 +139,7 @@ struct UpdateParams {
   double escale;            // kernel-function scale (KernelFun), host-computed
   int kfun;                 // KernelFun
   double* tile_g2;                              // [n_tiles] per-CTA ||G||^2 partial (row order)
+  int g2_accum;                                 // add to tile_g2 instead of storing (grouped rounds)
   // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
   int columns_only; double* cols_out; int64_t ld_out;
   // RPC_DEBUG_TIMING: per-CTA cycle counters per phase ([grid][8] u64), or null
@@ -149,9 +154,12 @@ int launch_update(const UpdateParams& p, cudaStream_t st);
 // B'[perm_row(n)][k] = -(L^{-1} F_S)[n][k] for k < kcur (the residual GEMM's B operand with
 // the triangular solve folded in); linv_rm as written by launch_linv*, F_S rows from the
 // proposal records of the accepted positions.  *m_dev = accepted count (<= m_max).
+// m_dev == nullptr: m = m_max.  Grouped rounds (lext != nullptr): F_S columns
+// [kprop, kcur) are L(g0 + a, k - kprop), read from the sweep's column-major m_full x m_full L.
 void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* prop,
                    RecordLayout lay, const int* pos, const int* m_dev, int m_max, int kcur,
-                   double* bp, int64_t ldbp, cudaStream_t st);
+                   double* bp, int64_t ldbp, cudaStream_t st, const double* lext = nullptr,
+                   int m_full = 0, int g0 = 0, int kprop = -1);
 // Gathers the accepted pivots' X rows, F rows (first kcur columns), norms and ids from the
 // proposal records into the update kernel's operand buffers (rows at perm_row(n), n < nb).
 // X rows are multiplied by xscale: the Gram kernel passes -2 (gram_xscale), so the DMMA

@@ -324,8 +324,9 @@ inline void validate(int64_t n, int64_t d, const rpc_kernel_spec& k, rpc_run_con
     raise(RPC_EINVAL, "unknown kernel kind");
   }
   if (cfg.block_size < 1) raise(RPC_EINVAL, "accelerated_rpcholesky: block size must be >= 1");
-  if (cfg.block_size > 256)
-    raise(RPC_EINVAL, "accelerated_rpcholesky: this build supports block size <= 256");
+  if (cfg.block_size > kMaxBlock)
+    raise(RPC_EINVAL, "accelerated_rpcholesky: this build supports block size <= " +
+                          std::to_string(kMaxBlock));
   if (cfg.mode == RPC_FIXED_ROUNDS) {
     if (cfg.rounds < 1) raise(RPC_EINVAL, "RunConfig: t, b must be >= 1");
   } else if (cfg.mode == RPC_UNTIL_RANK) {

@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
   extern __shared__ double sm[];
   __shared__ int s_m, s_nacc, s_acc[kSweepBlock];
   __shared__ double s_root[kSweepBlock];
-  __shared__ int s_pos[256];
+  __shared__ int s_pos[kMaxBlock];
   double* rdraw = sm;
   double* udiag = sm + b;
   double* lblk = sm + 2 * b;                       // [kSweepBlock][kSweepBlock] in-block l values

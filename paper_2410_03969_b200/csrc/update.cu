@@ -80,14 +80,19 @@ __global__ void __launch_bounds__(256) bprime_kernel(const double* __restrict__ 
                                                      int64_t ldl, int koff,
                                                      const double* __restrict__ prop,
                                                      RecordLayout lay, const int* __restrict__ pos,
-                                                     const int* __restrict__ m_dev, int kcur,
-                                                     double* __restrict__ bp, int64_t ldbp) {
+                                                     const int* __restrict__ m_dev, int m_host,
+                                                     int kcur, double* __restrict__ bp,
+                                                     int64_t ldbp, const double* __restrict__ lext,
+                                                     int m_full, int g0, int kprop) {
   extern __shared__ double sF[];  // [m][kBpCols]
-  const int m = *m_dev;
+  const int m = m_dev ? *m_dev : m_host;
   const int k0 = blockIdx.x * kBpCols;
   for (int i = threadIdx.x; i < m * kBpCols; i += blockDim.x) {
-    const int c = i / kBpCols, kk = i % kBpCols;
-    sF[i] = k0 + kk < kcur ? __ldg(prop + (int64_t)pos[c] * lay.rec + lay.foff + k0 + kk) : 0.0;
+    const int c = i / kBpCols, kk = i % kBpCols, k = k0 + kk;
+    double v = 0.0;
+    if (k < kprop) v = __ldg(prop + (int64_t)pos[c] * lay.rec + lay.foff + k);
+    else if (k < kcur) v = __ldg(lext + (int64_t)(k - kprop) * m_full + g0 + c);
+    sF[i] = v;
   }
   __syncthreads();
   const int kk = threadIdx.x % kBpCols, a0 = threadIdx.x / kBpCols;
@@ -122,11 +127,13 @@ __global__ void __launch_bounds__(256) bprime_kernel(const double* __restrict__ 
 
 void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* prop,
                    RecordLayout lay, const int* pos, const int* m_dev, int m_max, int kcur,
-                   double* bp, int64_t ldbp, cudaStream_t st) {
+                   double* bp, int64_t ldbp, cudaStream_t st, const double* lext, int m_full,
+                   int g0, int kprop) {
   if (kcur <= 0 || m_max <= 0) return;
   const unsigned grid = (unsigned)((kcur + kBpCols - 1) / kBpCols);
-  bprime_kernel<<<grid, 256, sizeof(double) * kBpCols * m_max, st>>>(linv_rm, ldl, koff, prop, lay,
-                                                                       pos, m_dev, kcur, bp, ldbp);
+  bprime_kernel<<<grid, 256, sizeof(double) * kBpCols * m_max, st>>>(
+      linv_rm, ldl, koff, prop, lay, pos, m_dev, m_max, kcur, bp, ldbp, lext, m_full, g0,
+      lext ? kprop : kcur);
 }
 
 }  // namespace rpcb

@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     if (gtid == 0) {
       double s2 = 0.0;
       for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
-      p.tile_g2[tile] = s2;
+      p.tile_g2[tile] = p.g2_accum ? __dadd_rn(p.tile_g2[tile], s2) : s2;
     }
     mark(5);
     trc(k, 6);

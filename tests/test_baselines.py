@@ -127,9 +127,10 @@ def test_gpu_matches_reference_fixture(ctx, name, replay):
 @pytest.mark.gpu
 @pytest.mark.parametrize("kw", [dict(mode="fixed_rounds", rounds=4, b=64, seed=2),
                                 dict(b=300 // 2, k=200, seed=1),
-                                dict(b=7, k=50, seed=4, dist="direct")])
+                                dict(b=7, k=50, seed=4, dist="direct"),
+                                dict(b=400, k=700, seed=5)])  # grouped appends (b > 256)
 def test_gpu_block_vs_oracle(ctx, kw):
-    x = wl.gen_c2(1500, 5, 3)
+    x = wl.gen_c2(3000 if kw["b"] > 256 else 1500, 5, 3)
     kw = dict(kw)
     b, seed, dist = kw.pop("b"), kw.pop("seed"), kw.pop("dist", None)
     k = kw.pop("k", 0)

@@ -111,7 +111,7 @@ def test_rejection_sweep_bitexact(ctx):
     x = wl.gen_c1(400, 5, 3)
     o = po.Oracle(x=x, kernel="gaussian", sigma=1.3)
     rng = np.random.default_rng(4)
-    for b in (1, 2, 17, 40, 120, 200, 256):
+    for b in (1, 2, 17, 40, 120, 200, 256, 300, 700):
         prop = rng.integers(0, 400, b)
         prop[b // 2:] = prop[: b - b // 2]  # duplicates
         h = o.submatrix(prop, prop)
@@ -338,13 +338,33 @@ def test_bench_column_throughput_rows(ctx):
 
 
 @pytest.mark.parametrize("b,d,kernel", [(256, 8, "gaussian"), (256, 40, "l1laplace")])
-def test_max_block_size(ctx, b, d, kernel):  # b = 256: the largest tile configuration
+def test_max_block_size(ctx, b, d, kernel):  # b = 256: the largest single-launch tile configuration
     x = wl.gen_c2(9000, d, 4)
     g, r, o = run_both(x, kernel, math.sqrt(d), k=600, b=b, ctx=ctx)
     assert_parity(g, r, o)
+
+
+# b > 256 (rpcholesky.hpp:342 accepts any b >= 1): rounds whose accepted set exceeds 256 are
+# appended in groups of 128 (block Cholesky against the sweep's L), the sweep holds H packed in
+# L2; pivots must still equal the reference's and F agree to 1e-10
+@pytest.mark.parametrize("b,d,kernel,replay", [(300, 8, "gaussian", False), (300, 8, "gaussian", True),
+                                               (600, 20, "gaussian", False),
+                                               (1024, 30, "l1laplace", False)])
+def test_block_size_beyond_256(ctx, b, d, kernel, replay):
+    x = wl.gen_c2(12000, d, 4)
+    g, r, o = run_both(x, kernel, math.sqrt(d), k=2 * b, b=b, ctx=ctx, replay=replay)
+    assert max(len(a) for a in g.accepted) > 128  # grouped appends really ran
+    assert_parity(g, r, o)
+
+
+def test_block_size_limits(ctx):
+    x = wl.gen_c2(3000, 4, 4)
+    with pytest.raises(ValueError, match="block size <= 1024"):
+        api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec("gaussian", 1.0)),
+                                   api.RunConfig.until_rank(10, 1025, 0), ctx)
     with pytest.raises(ValueError, match="block size <= 256"):
-        api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec(kernel, 1.0)),
-                                   api.RunConfig.until_rank(10, 257, 0), ctx)
+        api.accelerated_rpcholesky_lowmem(api.KernelOracle(x, api.KernelSpec("gaussian", 1.0)),
+                                          api.RunConfig.until_rank(10, 257, 0), ctx)
 
 
 @pytest.mark.parametrize("kernel,dist", [("matern32", None), ("matern32", "direct"),
