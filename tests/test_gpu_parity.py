@@ -407,3 +407,16 @@ def test_dimension_padding_boundaries(ctx, d, kernel, dist):
     rounds = 1 if (kernel == "gaussian" and d <= 3) else 3
     g, r, o = run_both(x, kernel, sigma, b=16, seed=d, rounds=rounds, ctx=ctx, dist=dist)
     assert_parity(g, r, o)
+
+
+# Any d on the standard path (the reference's KernelOracle takes any dimension): the point pack
+# stages fewer rows per CTA as d grows and takes a per-row kernel beyond the shared-memory
+# tile; the Gram / distance phases stream X in 16-coordinate chunks.
+@pytest.mark.parametrize("d,kernel,dist", [(500, "gaussian", None), (500, "l1laplace", None),
+                                           (3300, "gaussian", "direct"), (30000, "gaussian", None)])
+def test_large_dimension(ctx, d, kernel, dist):
+    n = 3000 if d < 30000 else 600
+    x = wl.gen_c3(n, d, 2)
+    sigma = math.sqrt(d) * (0.5 if kernel == "gaussian" else 10.0)
+    g, r, o = run_both(x, kernel, sigma, k=60, b=20, ctx=ctx, dist=dist)
+    assert_parity(g, r, o)

@@ -199,3 +199,16 @@ def test_gpu_krr_errors(ctx):
     fit = api.fit_krr(x, x[:, 0], spec, 1e-3, 5, cfg, 1e-8, 50, ctx)
     with pytest.raises(ValueError, match="dimension mismatch"):
         api.predict(fit.model, np.zeros((3, 3)))
+
+
+@pytest.mark.gpu
+def test_gpu_krr_dimension_limit():
+    """This build's KRR product kernel keeps a tile's points resident in shared memory:
+    d > 128 is rejected with the reference's invalid_argument class, not mis-computed."""
+    from paper_2410_03969_b200 import api
+    x = wl.gen_c3(300, 130, 1)
+    with pytest.raises(ValueError, match="d <= 128"):
+        api.fit_krr(x, np.ones(300), api.KernelSpec("gaussian", 3.0), 1e-3, 20,
+                    api.RunConfig.until_rank(20, 10, 0), 1e-8, 10)
+    with pytest.raises(ValueError, match="d <= 128"):
+        api.kernel_matvec(api.KernelOracle(x, api.KernelSpec("gaussian", 3.0)), np.ones(300))
