@@ -160,6 +160,14 @@ void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* p
                    RecordLayout lay, const int* pos, const int* m_dev, int m_max, int kcur,
                    double* bp, int64_t ldbp, cudaStream_t st, const double* lext = nullptr,
                    int m_full = 0, int g0 = 0, int kprop = -1);
+// linv (as launch_linv_dev, update layout) + B' = -L^{-1} F_S (forward substitution, into
+// bp rows perm_row(a) < m, columns < kcur) + the accepted X rows / norms / ids (as
+// launch_gather_accepted without F rows; n_rows operand rows, zero beyond m), one launch.
+void launch_round_prep(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
+                       int64_t ldl, int koff, double* linv_rm, const double* prop,
+                       RecordLayout lay, const int* pos, int kcur, double* bp, int64_t ldbp,
+                       int dpad, double* xs, double* sqnS, double* idS, double xscale,
+                       int n_rows, cudaStream_t st);
 // Gathers the accepted pivots' X rows, F rows (first kcur columns), norms and ids from the
 // proposal records into the update kernel's operand buffers (rows at perm_row(n), n < nb).
 // X rows are multiplied by xscale: the Gram kernel passes -2 (gram_xscale), so the DMMA

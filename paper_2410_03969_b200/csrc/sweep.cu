@@ -388,6 +388,167 @@ __global__ void __launch_bounds__(32 * kLinvWarps) linv_kernel(const double* __r
   for (int a = lane + 32 * NQ; a < nb; a += 32) linv_rm[(int64_t)perm_row(a) * ldl + col] = 0.0;
 }
 
+// ---- round prep: L^{-1}, B' and the accepted operands in one launch ----------------
+// Three independent roles over one grid, all reading the sweep's outputs (m on the device):
+//   CTAs [0, nA)        : L^{-1} columns (as linv_kernel: one warp per column),
+//   CTAs [nA, nA + nB)  : B' = -L^{-1} F_S by forward substitution L x = -F_S(:, k), one warp
+//                         per column k (no dependency on L^{-1}, so it runs beside it),
+//   CTAs [nA + nB, ...) : the accepted pivots' X rows (pre-scaled), norms and ids.
+// Replaces linv -> gather -> bprime (three dependent launches) on the accelerated path.
+template <int NQ>
+__device__ __forceinline__ void warp_lower_solve(const double* sL, int m, int t0, double (&x)[NQ]) {
+  const int lane = threadIdx.x & 31;
+  double rd[NQ], ln[NQ];
+  int ar[NQ];
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int a = lane + 32 * q;
+    ar[q] = a < m ? a : m - 1;
+    rd[q] = 1.0 / sL[(int64_t)ar[q] * m + ar[q]];
+    ln[q] = sL[(int64_t)t0 * m + ar[q]];
+  }
+  for (int t = t0; t < m; ++t) {
+    double lc[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) lc[q] = ln[q];
+    const int tn = t + 1 < m ? t + 1 : t;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) ln[q] = sL[(int64_t)tn * m + ar[q]];
+    const int ql = t >> 5, ll = t & 31;
+    double xt_own = x[0] * rd[0];
+#pragma unroll
+    for (int q = 1; q < NQ; ++q) xt_own = (q == ql) ? x[q] * rd[q] : xt_own;
+    const double xt = __shfl_sync(0xffffffffu, xt_own, ll);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int a = lane + 32 * q;
+      const double nx = fma(-lc[q], xt, x[q]);
+      x[q] = (a == t) ? xt : ((a > t) ? nx : x[q]);
+    }
+  }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(32 * kLinvWarps) round_prep_kernel(
+    const double* __restrict__ lacc_cm, int m_host, const int* m_dev, int nA, int nB, int nb,
+    int64_t ldl, int koff, int in_smem, double* __restrict__ linv_rm,
+    const double* __restrict__ prop, RecordLayout lay, const int* __restrict__ pos, int kcur,
+    double* __restrict__ bp, int64_t ldbp, int dpad, double* __restrict__ xs,
+    double* __restrict__ sqnS, double* __restrict__ idS, double xscale, int n_rows) {
+  extern __shared__ double smem_l[];
+  const int m = m_dev ? *m_dev : m_host;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bid = blockIdx.x;
+  if (bid >= nA + nB) {  // ---- operands of accepted pivot n (rows perm_row(n)) ----
+    const int n = bid - nA - nB;
+    const int dst = perm_row(n);
+    double* xr = xs + (int64_t)dst * dpad;
+    if (n < m) {
+      const double* rec = prop + (int64_t)pos[n] * lay.rec;
+      for (int i = tid; i < dpad; i += blockDim.x) xr[i] = xscale * rec[lay.xoff + i];
+      if (tid == 0) {
+        sqnS[n] = rec[1];
+        idS[n] = rec[0];
+      }
+    } else {
+      for (int i = tid; i < dpad; i += blockDim.x) xr[i] = 0.0;
+      if (tid == 0) {
+        sqnS[n] = 0.0;
+        idS[n] = -1.0;
+      }
+    }
+    return;
+  }
+  const bool inv = bid < nA;
+  const int c = inv ? bid * kLinvWarps + warp : 0;
+  const int k = inv ? 0 : (bid - nA) * kLinvWarps + warp;
+  if (inv && bid * kLinvWarps >= m) return;  // whole CTA beyond m
+  if (m <= 0) return;
+  const double* sL = lacc_cm;
+  if (in_smem) {
+    const int n2 = (m * m) >> 1;
+    const double2* src2 = reinterpret_cast<const double2*>(lacc_cm);
+    double2* dst2 = reinterpret_cast<double2*>(smem_l);
+    double2 buf[8];
+    for (int i0 = tid; i0 < n2; i0 += 8 * (int)blockDim.x) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * (int)blockDim.x;
+        if (i < n2) buf[u] = __ldg(src2 + i);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * (int)blockDim.x;
+        if (i < n2) dst2[i] = buf[u];
+      }
+    }
+    if (tid == 0 && ((m * m) & 1)) smem_l[m * m - 1] = lacc_cm[m * m - 1];
+    __syncthreads();
+    sL = smem_l;
+  }
+  double x[NQ];
+  if (inv) {
+    if (c >= m) return;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) x[q] = (lane + 32 * q == c) ? 1.0 : 0.0;
+    warp_lower_solve<NQ>(sL, m, c, x);
+    const int col = linv_slot(c, m, koff, 1);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int a = lane + 32 * q;
+      if (a < nb) linv_rm[(int64_t)perm_row(a) * ldl + col] = (a >= c && a < m) ? x[q] : 0.0;
+    }
+    for (int a = lane + 32 * NQ; a < nb; a += 32) linv_rm[(int64_t)perm_row(a) * ldl + col] = 0.0;
+    return;
+  }
+  if (k >= kcur) return;
+  // B'(:, k) = -L^{-1} F_S(:, k): forward substitution from the right-hand side -F_S(:, k)
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int a = lane + 32 * q;
+    x[q] = a < m ? -__ldg(prop + (int64_t)pos[a] * lay.rec + lay.foff + k) : 0.0;
+  }
+  warp_lower_solve<NQ>(sL, m, 0, x);
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    const int a = lane + 32 * q;
+    if (a < m) bp[(int64_t)perm_row(a) * ldbp + k] = x[q];
+  }
+  for (int a = m + lane; a < n_rows; a += 32) bp[(int64_t)perm_row(a) * ldbp + k] = 0.0;
+}
+
+template <int NQ>
+static void prep_launch(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
+                        int64_t ldl, int koff, double* linv_rm, const double* prop,
+                        RecordLayout lay, const int* pos, int kcur, double* bp, int64_t ldbp,
+                        int dpad, double* xs, double* sqnS, double* idS, double xscale,
+                        int n_rows, cudaStream_t st) {
+  ensure_smem_attr((const void*)round_prep_kernel<NQ>, 200 * 1024);
+  const size_t bytes = sizeof(double) * (size_t)m_max * m_max;
+  const int in_smem = bytes <= 200 * 1024;
+  const int nA = (m_max + kLinvWarps - 1) / kLinvWarps;
+  const int nB = (kcur + kLinvWarps - 1) / kLinvWarps;
+  round_prep_kernel<NQ><<<nA + nB + n_rows, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(
+      lacc_cm, m_host, m_dev, nA, nB, nb, ldl, koff, in_smem, linv_rm, prop, lay, pos, kcur, bp,
+      ldbp, dpad, xs, sqnS, idS, xscale, n_rows);
+}
+
+void launch_round_prep(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
+                       int64_t ldl, int koff, double* linv_rm, const double* prop,
+                       RecordLayout lay, const int* pos, int kcur, double* bp, int64_t ldbp,
+                       int dpad, double* xs, double* sqnS, double* idS, double xscale,
+                       int n_rows, cudaStream_t st) {
+  if (m_max <= 0) return;
+#define RPCB_PREP(NQ)                                                                         \
+  prep_launch<NQ>(lacc_cm, m_host, m_dev, m_max, nb, ldl, koff, linv_rm, prop, lay, pos, kcur, \
+                  bp, ldbp, dpad, xs, sqnS, idS, xscale, n_rows, st)
+  if (m_max <= 32) RPCB_PREP(1);
+  else if (m_max <= 64) RPCB_PREP(2);
+  else if (m_max <= 128) RPCB_PREP(4);
+  else RPCB_PREP(8);
+#undef RPCB_PREP
+}
+
 template <int NQ>
 static void linv_launch(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
                         int64_t ldl, int koff, int perm, double* linv_rm, cudaStream_t st) {
