@@ -439,20 +439,21 @@ __global__ void __launch_bounds__(32 * kLinvWarps) round_prep_kernel(
   const int m = m_dev ? *m_dev : m_host;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int bid = blockIdx.x;
-  if (bid >= nA + nB) {  // ---- operands of accepted pivot n (rows perm_row(n)) ----
-    const int n = bid - nA - nB;
+  if (bid >= nA + nB) {  // ---- operands of accepted pivot n (rows perm_row(n)), a warp each ----
+    const int n = (bid - nA - nB) * kLinvWarps + warp;
+    if (n >= n_rows) return;
     const int dst = perm_row(n);
     double* xr = xs + (int64_t)dst * dpad;
     if (n < m) {
       const double* rec = prop + (int64_t)pos[n] * lay.rec;
-      for (int i = tid; i < dpad; i += blockDim.x) xr[i] = xscale * rec[lay.xoff + i];
-      if (tid == 0) {
+      for (int i = lane; i < dpad; i += 32) xr[i] = xscale * rec[lay.xoff + i];
+      if (lane == 0) {
         sqnS[n] = rec[1];
         idS[n] = rec[0];
       }
     } else {
-      for (int i = tid; i < dpad; i += blockDim.x) xr[i] = 0.0;
-      if (tid == 0) {
+      for (int i = lane; i < dpad; i += 32) xr[i] = 0.0;
+      if (lane == 0) {
         sqnS[n] = 0.0;
         idS[n] = -1.0;
       }
@@ -528,7 +529,10 @@ static void prep_launch(const double* lacc_cm, int m_host, const int* m_dev, int
   const int in_smem = bytes <= 200 * 1024;
   const int nA = (m_max + kLinvWarps - 1) / kLinvWarps;
   const int nB = (kcur + kLinvWarps - 1) / kLinvWarps;
-  round_prep_kernel<NQ><<<nA + nB + n_rows, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(
+  const int nC = (n_rows + kLinvWarps - 1) / kLinvWarps;  // operand rows, a warp each
+  // (every CTA of the launch reserves the L copy's shared memory: few operand CTAs keep the
+  // whole grid in one wave)
+  round_prep_kernel<NQ><<<nA + nB + nC, 32 * kLinvWarps, in_smem ? bytes : 0, st>>>(
       lacc_cm, m_host, m_dev, nA, nB, nb, ldl, koff, in_smem, linv_rm, prop, lay, pos, kcur, bp,
       ldbp, dpad, xs, sqnS, idS, xscale, n_rows);
 }
