@@ -51,3 +51,19 @@ def test_runconfig_validation():
         api.RunConfig.until_rank(0, 4, 0)
     with pytest.raises(ValueError):
         api.RunConfig.fixed_rounds(3, 0, 0)
+
+
+def test_bench_gpus_flag_spawns_ranks_or_fails_loudly():
+    """bench.py --gpus N (no torchrun) starts one process per GPU; with fewer GPUs visible it
+    must fail with a message instead of silently running one rank."""
+    import subprocess
+    import sys
+    import torch
+    if torch.cuda.device_count() >= 2:
+        pytest.skip("multi-GPU host: the spawn path would really run")
+    env = dict(os.environ)
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1",
+                        "--warmup", "0"], capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode != 0
+    assert "--gpus 2" in r.stderr and "CUDA device" in r.stderr
