@@ -420,10 +420,11 @@ __global__ void __launch_bounds__(256, MINB)
       s_rowg2[gtid] = s2;
     }
     gsync();
-    if (gtid == 0) {
+    if (gtid < 32) {  // fixed-order tree over the row sums (as update_impl.cuh)
       double s2 = 0.0;
-      for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
-      p.tile_g2[tile] = s2;
+      for (int r = gtid; r < BM; r += 32) s2 = __dadd_rn(s2, s_rowg2[r]);
+      s2 = warp_sum_xor(s2);
+      if (gtid == 0) p.tile_g2[tile] = s2;
     }
   }
 }

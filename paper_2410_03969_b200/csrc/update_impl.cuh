@@ -653,12 +653,18 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     // (s_rowg2 is next written after the next tile's park barrier).  A barrier id of its own
     // (not gsync's): the early warps' arrivals can then never be counted toward a later
     // gsync, and the next tile's epilogue arrivals come after warp 0 passed that tile's park.
-    if (warp == 0) named_bar_sync(1 + G + grp, GT);
-    else named_bar_arrive(1 + G + grp, GT);
-    if (gtid == 0) {
+    // (the tile's ||G||^2 is a fixed-order tree over the row sums — each lane adds rows
+    // lane and lane + 32, then the xor butterfly, which every lane evaluates identically —
+    // instead of a 64-long serial chain that kept warp 0, and through the ring the group,
+    // waiting at every tile: 5.4k-cycle epilogues in the early rounds)
+    if (warp == 0) {
+      named_bar_sync(1 + G + grp, GT);
       double s2 = 0.0;
-      for (int r = 0; r < BM; ++r) s2 = __dadd_rn(s2, s_rowg2[r]);
-      p.tile_g2[tile] = p.g2_accum ? __dadd_rn(p.tile_g2[tile], s2) : s2;
+      for (int r = lane; r < BM; r += 32) s2 = __dadd_rn(s2, s_rowg2[r]);
+      s2 = warp_sum_xor(s2);
+      if (lane == 0) p.tile_g2[tile] = p.g2_accum ? __dadd_rn(p.tile_g2[tile], s2) : s2;
+    } else {
+      named_bar_arrive(1 + G + grp, GT);
     }
     mark(5);
     trc(k, 6);
