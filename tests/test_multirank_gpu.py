@@ -58,6 +58,12 @@ def _run(ctx, x, case, rpcf=None):
         if rpcf:
             r.write_rpcf(rpcf)
     r.free()
+    if case["algo"] == "accelerated" and not case["replay"]:
+        # the streamed-factor entry (rpc_accelerated_rpcholesky_into): each rank's rows land in
+        # a full-height host buffer while the rounds run
+        ri = api.accelerated_rpcholesky_into(ko, cfg, ctx=ctx)
+        out["factor_into"] = np.array(ri.factor)
+        ri.free()
     return out
 
 
@@ -133,6 +139,9 @@ def test_two_ranks_bitwise_equal_one_rank(two_rank_outputs, name):
         assert np.array_equal(two["resid"][r0:r0 + nr], one["resid"][r0:r0 + nr]), rank
         if "factor" in one:
             assert np.array_equal(two["factor"][r0:r0 + nr], one["factor"][r0:r0 + nr]), rank
+        if "factor_into" in one:
+            assert np.array_equal(one["factor_into"], one["factor"])
+            assert np.array_equal(two["factor_into"][r0:r0 + nr], one["factor"][r0:r0 + nr]), rank
     if name == "fast":
         with open(os.path.join(tmp, "two_fast.rpcf"), "rb") as a, \
                 open(os.path.join(tmp, "one_fast.rpcf"), "rb") as b:
