@@ -230,6 +230,16 @@ void launch_lowmem_append(const double* prop, RecordLayout lay, const int* pos, 
 // chol (k x k column-major, lower) from the row-major L.
 void launch_lowmem_chol(const double* Lrm, int64_t ldw, int k, double* chol, cudaStream_t st);
 
+// ---- symmetric kernel matvec (krr.hpp:143-162, one right-hand side), symv.cu ----------------
+// out = A v + add_coef * add_vec + add_const over the training points themselves, each
+// 1024 x 1024 block of the lower block triangle generated once and used for both A v and
+// A^T v; deterministic.  v: [n] (16-byte aligned, row stride ldv for the TMA map).
+int64_t symv_scratch_doubles(int64_t n);
+bool launch_symv(const double* X, int64_t dpad, int d, const double* sqn, const double* rec,
+                 int64_t prec, const double* v, int64_t ldv, int64_t n, int kind, int kfun,
+                 double escale, double* scratch, const double* add_vec, double add_coef,
+                 double add_const, double* out, cudaStream_t st);
+
 // ---- KRR preconditioner core (krr.hpp:30-70), krr_core.cu: row-major [kc][kc] ----------
 // kc = k rounded up to 64; entries beyond k hold the identity.  Lower triangle only.
 int64_t core_dim(int k);

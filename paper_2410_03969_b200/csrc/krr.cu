@@ -1,12 +1,14 @@
 // krr.cu — kernel ridge regression on the device (krr.hpp): the consumer of the
 // factor that accelerated_rpcholesky leaves in HBM.
 //
-//   kernel_matvec  krr.hpp:143-162   A V without forming A: the low-memory update kernel
-//                                    in product mode (lowmem_impl.cuh) regenerates each
-//                                    64 x 16 kernel tile in shared memory (Gram on DMMA +
-//                                    exp, or l1 distances on the FP64 cores) and multiplies
-//                                    it into V on the tensor cores.  N^2 kernel entries per
-//                                    product, no N^2 storage, HBM traffic O(N d).
+//   kernel_matvec  krr.hpp:143-162   A V without forming A.  One vector (every PCG step):
+//                                    the symmetric product (symv.cu) generates each
+//                                    1024 x 1024 block of the lower block triangle once and
+//                                    uses it for A v and A^T v — N^2/2 kernel entries.  Up to
+//                                    8 vectors (or RPC_KRR_GENERIC=1): the low-memory update
+//                                    kernel in product mode (lowmem_impl.cuh), N^2 entries.
+//                                    Kernel tiles are regenerated in registers (Gram on DMMA +
+//                                    exp, or l1 distances on the FP64 cores); no N^2 storage.
 //   Preconditioner krr.hpp:30-70     P = F F^T + mu I through Woodbury on the device-resident
 //                                    F: core = F^T F + mu I by a DMMA SYRK, its blocked
 //                                    Cholesky and the solves with it (krr_core.cu, no
@@ -188,6 +190,12 @@ __global__ void woodbury_z_kernel(const double* __restrict__ F, int64_t ldf, int
   }
 }
 
+// RPC_KRR_GENERIC=1 forces the generic (non-symmetric) product for A/B comparisons.
+bool use_symv() {
+  static const bool generic = std::getenv("RPC_KRR_GENERIC") != nullptr;
+  return !generic;
+}
+
 // X (host, any layout) -> packed device points [n][dpad] + norms; rejects non-finite.
 void upload_points(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx, int layout,
                    int64_t dpad, DBuf& X, DBuf& sqn) {
@@ -301,9 +309,18 @@ int rpc_kernel_matvec(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64
                                                rec.as<double>());
     // V (n x nrhs column-major) is W^T row-major with rows padded to ldv
     CK(cudaMemcpy2DAsync(W.p, ldv * 8, v, n * 8, n * 8, nrhs, cudaMemcpyHostToDevice, st));
-    kernel_product(ctx, X.as<double>(), sqn.as<double>(), n, dpad, d, rec.as<double>(), prec, n,
-                   W.as<double>(), ldv, (int)nrhs, kind, kfun, kscale, 1, o.as<double>(), nrhs,
-                   nullptr, 0.0, 0.0);
+    DBuf sym;
+    bool done = false;
+    if (nrhs == 1 && use_symv() && n >= 16384) {  // one vector: symmetric blocks, each once
+      sym = DBuf(ctx, sizeof(double) * symv_scratch_doubles(n));
+      done = launch_symv(X.as<double>(), dpad, (int)d, sqn.as<double>(), rec.as<double>(), prec,
+                         W.as<double>(), ldv, n, kind, kfun, kscale, sym.as<double>(), nullptr,
+                         0.0, 0.0, o.as<double>(), st);
+    }
+    if (!done)
+      kernel_product(ctx, X.as<double>(), sqn.as<double>(), n, dpad, d, rec.as<double>(), prec, n,
+                     W.as<double>(), ldv, (int)nrhs, kind, kfun, kscale, 1, o.as<double>(), nrhs,
+                     nullptr, 0.0, 0.0);
     // out: n x nrhs column-major <- o row-major [n][nrhs]
     if (nrhs == 1) {
       CK(cudaMemcpyAsync(out, o.p, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
@@ -446,11 +463,20 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
                                                    part.as<double>());
     finish_kernel<<<1, 1, 0, st>>>(part.as<double>(), nb, s_d, S_RZ);
     double* hst = static_cast<double*>(ctx->pinned(sizeof(double) * 8));
+    DBuf sym;
+    if (use_symv() && n >= 16384) sym = DBuf(ctx, sizeof(double) * symv_scratch_doubles(n));
     for (int64_t it = 0; it < max_iters; ++it) {
-      // ap = A p + mu p  (fused kernel regeneration + tensor-core product)
-      kernel_product(ctx, m->X.as<double>(), m->sqn.as<double>(), n, m->dpad, d,
-                     m->rec.as<double>(), m->prec, n, p.as<double>(), ldv, 1, kind, m->kfun, m->kscale,
-                     1, ap.as<double>(), 1, p.as<double>(), mu, 0.0);
+      // ap = A p + mu p  (fused kernel regeneration + tensor-core / FMA product; the
+      // symmetric form generates each off-diagonal block once for A p and A^T p)
+      const bool done =
+          sym.p && launch_symv(m->X.as<double>(), m->dpad, (int)d, m->sqn.as<double>(),
+                               m->rec.as<double>(), m->prec, p.as<double>(), ldv, n, kind, m->kfun,
+                               m->kscale, sym.as<double>(), p.as<double>(), mu, 0.0,
+                               ap.as<double>(), st);
+      if (!done)
+        kernel_product(ctx, m->X.as<double>(), m->sqn.as<double>(), n, m->dpad, d,
+                       m->rec.as<double>(), m->prec, n, p.as<double>(), ldv, 1, kind, m->kfun,
+                       m->kscale, 1, ap.as<double>(), 1, p.as<double>(), mu, 0.0);
       dot_partial_kernel<<<nb, kRedThreads, 0, st>>>(p.as<double>(), ap.as<double>(), n,
                                                      part.as<double>());
       finish_kernel<<<1, 1, 0, st>>>(part.as<double>(), nb, s_d, S_DENOM);

@@ -212,3 +212,23 @@ def test_gpu_krr_dimension_limit():
                     api.RunConfig.until_rank(20, 10, 0), 1e-8, 10)
     with pytest.raises(ValueError, match="d <= 128"):
         api.kernel_matvec(api.KernelOracle(x, api.KernelSpec("gaussian", 3.0)), np.ones(300))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kern,d,sigma", [("gaussian", 10, 3.0), ("l1laplace", 20, 6.0)])
+def test_gpu_symmetric_matvec(kern, d, sigma):
+    """N >= 16384 takes the symmetric product (symv.cu: each off-diagonal 1024 x 1024 block
+    generated once, used for A v and A^T v).  Checked against a dense product (row chunks,
+    numpy) and for bit-reproducibility run to run."""
+    from paper_2410_03969_b200 import api
+    n = 20000
+    x = wl.gen_c1(n, d, 5)
+    v = np.random.default_rng(3).standard_normal(n)
+    ko = api.KernelOracle(x, api.KernelSpec(kern, sigma))
+    y1 = api.kernel_matvec(ko, v)
+    y2 = api.kernel_matvec(ko, v)
+    assert np.array_equal(y1, y2)
+    want = np.zeros(n)
+    for r0 in range(0, n, 2000):
+        want[r0:r0 + 2000] = dense_kernel(x[r0:r0 + 2000], x, kern, sigma) @ v
+    assert rel(y1, want) <= 1e-12
