@@ -457,7 +457,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // queue them before the status read so they run while the host waits (grouped rounds
     // build them per group once m is known).
     if (!grouped) {
-      CK(cudaMemsetAsync(linv.p, 0, sizeof(double) * nbl * ldl, st));
+      // (no memset of the L^{-1} buffer: both kernels write every row of every column the
+      // consumers read, zeros included)
       if (lowmem) {
         launch_linv_dev(lacc.as<double>(), &d_sweep->m, b, (int)nbl, ldl, 0, linv.as<double>(), st, 0);
         ++launches;
@@ -501,7 +502,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       if (kcur + m > cap)
         raise(RPC_ENUMERIC, "accelerated_rpcholesky: factor capacity exceeded (duplicate pivot)");
       // (block / simple: kept blocks have m <= b, so cap = min(N, k + b) always suffices)
-      CK(cudaMemsetAsync(g2_all.p, 0, sizeof(double) * L.ncg, st));
+      // (g2_all needs no per-round reset: every round writes the same chunk slots, and the
+      // slots no shard writes stay zero from setup)
       if (lowmem) {
         // L_new = [[L, 0], [F_S, L_sel]]; L_new^{-1} rows [kcur, kcur+m) =
         // [-L_sel^{-1} (F_S L^{-1}) | L_sel^{-1}]   (rpcholesky.hpp:470-475)

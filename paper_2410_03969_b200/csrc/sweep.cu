@@ -463,8 +463,13 @@ __global__ void __launch_bounds__(32 * kLinvWarps) round_prep_kernel(
   const bool inv = bid < nA;
   const int c = inv ? bid * kLinvWarps + warp : 0;
   const int k = inv ? 0 : (bid - nA) * kLinvWarps + warp;
-  if (inv && bid * kLinvWarps >= m) return;  // whole CTA beyond m
   if (m <= 0) return;
+  if (inv && bid * kLinvWarps >= m) {
+    // columns [m, round16(m)) of the last 16-column chunk the update reads: zeros
+    if (c < ((m + 15) & ~15))
+      for (int a = lane; a < nb; a += 32) linv_rm[(int64_t)perm_row(a) * ldl + linv_slot(c, m, koff, 1)] = 0.0;
+    return;
+  }
   const double* sL = lacc_cm;
   if (in_smem) {
     const int n2 = (m * m) >> 1;
@@ -489,7 +494,11 @@ __global__ void __launch_bounds__(32 * kLinvWarps) round_prep_kernel(
   }
   double x[NQ];
   if (inv) {
-    if (c >= m) return;
+    if (c >= m) {
+      if (c < ((m + 15) & ~15))
+        for (int a = lane; a < nb; a += 32) linv_rm[(int64_t)perm_row(a) * ldl + linv_slot(c, m, koff, 1)] = 0.0;
+      return;
+    }
 #pragma unroll
     for (int q = 0; q < NQ; ++q) x[q] = (lane + 32 * q == c) ? 1.0 : 0.0;
     warp_lower_solve<NQ>(sL, m, c, x);
@@ -527,7 +536,7 @@ static void prep_launch(const double* lacc_cm, int m_host, const int* m_dev, int
   ensure_smem_attr((const void*)round_prep_kernel<NQ>, 200 * 1024);
   const size_t bytes = sizeof(double) * (size_t)m_max * m_max;
   const int in_smem = bytes <= 200 * 1024;
-  const int nA = (m_max + kLinvWarps - 1) / kLinvWarps;
+  const int nA = (((m_max + 15) & ~15) + kLinvWarps - 1) / kLinvWarps;  // through round16(m)
   const int nB = (kcur + kLinvWarps - 1) / kLinvWarps;
   const int nC = (n_rows + kLinvWarps - 1) / kLinvWarps;  // operand rows, a warp each
   // (every CTA of the launch reserves the L copy's shared memory: few operand CTAs keep the
