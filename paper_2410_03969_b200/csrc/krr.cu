@@ -190,10 +190,12 @@ __global__ void woodbury_z_kernel(const double* __restrict__ F, int64_t ldf, int
   }
 }
 
-// RPC_KRR_GENERIC=1 forces the generic (non-symmetric) product for A/B comparisons.
-bool use_symv() {
+// The symmetric product for one vector over n training points: from 16 super-blocks (enough
+// units to fill the GPU) up to a 4 GB partial buffer (n ~ 7e5; beyond that the generic
+// product, which needs no scratch).  RPC_KRR_GENERIC=1 forces the generic one (A/B runs).
+bool use_symv(int64_t n) {
   static const bool generic = std::getenv("RPC_KRR_GENERIC") != nullptr;
-  return !generic;
+  return !generic && n >= 16384 && symv_scratch_doubles(n) * 8 <= ((int64_t)4 << 30);
 }
 
 // X (host, any layout) -> packed device points [n][dpad] + norms; rejects non-finite.
@@ -311,7 +313,7 @@ int rpc_kernel_matvec(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64
     CK(cudaMemcpy2DAsync(W.p, ldv * 8, v, n * 8, n * 8, nrhs, cudaMemcpyHostToDevice, st));
     DBuf sym;
     bool done = false;
-    if (nrhs == 1 && use_symv() && n >= 16384) {  // one vector: symmetric blocks, each once
+    if (nrhs == 1 && use_symv(n)) {  // one vector: symmetric blocks, each generated once
       sym = DBuf(ctx, sizeof(double) * symv_scratch_doubles(n));
       done = launch_symv(X.as<double>(), dpad, (int)d, sqn.as<double>(), rec.as<double>(), prec,
                          W.as<double>(), ldv, n, kind, kfun, kscale, sym.as<double>(), nullptr,
@@ -464,7 +466,7 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
     finish_kernel<<<1, 1, 0, st>>>(part.as<double>(), nb, s_d, S_RZ);
     double* hst = static_cast<double*>(ctx->pinned(sizeof(double) * 8));
     DBuf sym;
-    if (use_symv() && n >= 16384) sym = DBuf(ctx, sizeof(double) * symv_scratch_doubles(n));
+    if (use_symv(n)) sym = DBuf(ctx, sizeof(double) * symv_scratch_doubles(n));
     for (int64_t it = 0; it < max_iters; ++it) {
       // ap = A p + mu p  (fused kernel regeneration + tensor-core / FMA product; the
       // symmetric form generates each off-diagonal block once for A p and A^T p)
