@@ -248,6 +248,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   std::vector<std::pair<int, int64_t>> upd_info;
   const bool dbg_phase = std::getenv("RPC_DEBUG_PHASES") != nullptr;
   const bool dbg_trace = std::getenv("RPC_DEBUG_TRACE") != nullptr;
+  const bool dbg_gaps = std::getenv("RPC_DEBUG_GAPS") != nullptr;
+  std::vector<Ev> gap_ev;
+  gap_ev.reserve(64);
   DBuf trace_buf(ctx, dbg_trace ? sizeof(unsigned long long) * 2 * 64 * 8 : 8);
   DBuf phase_clk(ctx, dbg_phase ? sizeof(unsigned long long) * 8 * 4096 : 8);
   std::vector<double> upd_flops;
@@ -471,6 +474,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                           idS.as<double>(), gram_xscale(kind), 256, st);
         ++launches;
       }
+    }
+    if (dbg_gaps) {  // RPC_DEBUG_GAPS: device idle between the round prep and the update
+      gap_ev.emplace_back();
+      CK(cudaEventRecord(gap_ev.back().e, st));
     }
     if (hbuf_dev) {
       // (published right after the sweep, above)
@@ -743,6 +750,16 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                    upd_flops[i / 2] / (ms * 1e-3) / 1e12);
   }
   tm.update_ms = update_ms;
+  if (dbg_gaps && !upd_ev.empty()) {
+    // pairs (prep done, update start): the host's per-round work showing up as device idle
+    double tot = 0.0;
+    for (size_t i = 0; i < gap_ev.size() && 2 * i < upd_ev.size(); ++i) {
+      CK(cudaEventElapsedTime(&ms, gap_ev[i].e, upd_ev[2 * i].e));
+      tot += ms;
+      std::fprintf(stderr, "[rpc] round %zu: prep end -> update start %.3f ms\n", i, ms);
+    }
+    std::fprintf(stderr, "[rpc] total prep->update gap %.3f ms\n", tot);
+  }
   tm.update_flops = flops;
   tm.update_bytes = bytes;
   tm.update_launches = upd_launches;
