@@ -9,6 +9,8 @@ timeout 900 python -m pytest tests -m gpu -x -q > $O/pytest_gpu.log 2>&1; echo "
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
 timeout 600 python bench.py > $O/bench.json 2> $O/bench.err; echo "bench rc=$?" >> $O/bench.err
 timeout 600 python bench.py --impl reference --steps 1 --warmup 3 > $O/bench_ref.json 2> $O/bench_ref.err
+# (ncu only right after the identical command exited 0 without it)
+timeout 600 python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $O/plain.log 2>&1 &&
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
-  --log-file $O/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu.log 2>&1
+  --log-file $O/launches.csv python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu.log 2>&1
 echo done
