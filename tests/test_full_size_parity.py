@@ -129,3 +129,26 @@ def test_c5_bounded_parity(replay):
     factor is 67 GB, beyond a host comparison; three rounds still run every kernel at full
     N and d with kcur up to 400."""
     check("C5", replay, rounds=3)
+
+
+def test_large_n_beyond_fused_prefix():
+    """N = 6e6 points: 1465 scan chunks, beyond the single-CTA fused prefix (1024 chunks), so the
+    tiled chunk-prefix kernel chains the chunk offsets; FixedRounds(2), b = 64, Gaussian."""
+    from paper_2410_03969_b200 import api
+    n, d, b = 6_000_000, 8, 64
+    x = wl.gen_c1(n, d, 7)
+    sigma = 2.0
+    o = po.Oracle(x=x, kernel="gaussian", sigma=sigma, n_threads=THREADS)
+    r = po.accelerated_rpcholesky(o, block_size=b, mode="fixed_rounds", rounds=2, seed=3,
+                                  copy_factor=False)
+    for replay in (False, True):
+        cfg = api.RunConfig.fixed_rounds(2, b, 3)
+        cfg.replay_scan = replay
+        g = api.accelerated_rpcholesky(api.KernelOracle(x, api.KernelSpec("gaussian", sigma)), cfg)
+        try:
+            assert np.array_equal(g.pivots, r.pivots)
+            f = g.factor_into(np.empty((n, g.rank), order="F"))
+            assert blocked_rel(f, r.factor) <= F_TOL
+            assert abs(g.relative_trace_error - po.relative_trace_error(o, r.factor)) <= TRACE_TOL
+        finally:
+            g.free()
