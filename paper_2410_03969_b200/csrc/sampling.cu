@@ -208,25 +208,35 @@ __device__ __forceinline__ void write_record(const SampleParams& p, int64_t lrow
   for (int k = threadIdx.x; k < p.kcur; k += blockDim.x) rec[p.lay.foff + k] = fr[k];
 }
 
+constexpr int kSampleStageMax = 4096;  // chunk ends staged in shared memory (N <= 16.7M)
 __global__ void __launch_bounds__(kScanThreads) sample_kernel(SampleParams p) {
   __shared__ double sh[kScanThreads + 1];
   __shared__ int s_chunk, s_mode, s_owner, s_best;
   __shared__ double s_off, s_target;
+  extern __shared__ double s_ends[];  // [nc] when staged
   const int j = blockIdx.x;
+  const int nc = p.n_chunks_global;
+  // the chunk ends go to shared memory in one parallel pass, so the draw's binary search
+  // costs shared-memory latency per probe instead of a dependent L2 round trip
+  const bool staged = nc <= kSampleStageMax;
+  if (staged) {
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) s_ends[c] = p.chunk_end[c];
+    __syncthreads();
+  }
+  const double* ends = staged ? s_ends : p.chunk_end;
   if (threadIdx.x == 0) {
     const double r = u01(splitmix64_draw(p.seed, p.draw0 + (uint64_t)j));
-    const int nc = p.n_chunks_global;
-    const double total = p.chunk_end[nc - 1];
+    const double total = ends[nc - 1];
     const double target = __dmul_rn(r, total);
     int lo = 0, hi = nc;  // upper_bound over chunk ends
     while (lo < hi) {
       const int mid = (lo + hi) >> 1;
-      if (target < p.chunk_end[mid]) hi = mid; else lo = mid + 1;
+      if (target < ends[mid]) hi = mid; else lo = mid + 1;
     }
     int mode = 0;
     if (lo == nc) {  // clamp to N-1, then walk back over the zero plateau
       int c = nc - 1;
-      while (c > 0 && p.chunk_end[c] == p.chunk_end[c - 1]) --c;
+      while (c > 0 && ends[c] == ends[c - 1]) --c;
       lo = c;
       mode = 1;
     }
@@ -235,7 +245,7 @@ __global__ void __launch_bounds__(kScanThreads) sample_kernel(SampleParams p) {
     s_chunk = lo;
     s_mode = mode;
     s_target = target;
-    s_off = lo ? p.chunk_end[lo - 1] : 0.0;
+    s_off = lo ? ends[lo - 1] : 0.0;
     s_owner = o;
     s_best = mode ? -1 : INT_MAX;
     p.owner[j] = o;
@@ -275,7 +285,9 @@ __global__ void __launch_bounds__(kScanThreads) sample_kernel(SampleParams p) {
 }
 
 void launch_sample(const SampleParams& p, cudaStream_t st) {
-  sample_kernel<<<p.b, kScanThreads, 0, st>>>(p);
+  const int nc = p.n_chunks_global;
+  const size_t smem = nc <= kSampleStageMax ? sizeof(double) * (size_t)nc : 0;
+  sample_kernel<<<p.b, kScanThreads, smem, st>>>(p);
 }
 
 // ---- replay mode -----------------------------------------------------------
