@@ -174,6 +174,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   DBuf linv(ctx, sizeof(double) * nbl * ldl), pos(ctx, sizeof(int) * b),
       acc_ids(ctx, sizeof(int64_t) * b), hp(ctx, sizeof(double) * ((size_t)b * (b + 1) / 2 + 1));
   DBuf status(ctx, sizeof(ScanStatus) + sizeof(SweepOut));
+  // split-K H block scratch
+  DBuf hb_part(ctx, sizeof(double) * hblock_scratch_doubles(b)),
+      hb_tick(ctx, sizeof(unsigned) * hblock_tickets(b));
+  CK(cudaMemsetAsync(hb_tick.p, 0, hb_tick.bytes, st));
   // accepted-pivot operands of the fused update (rows permuted, see common.cuh perm_row)
   DBuf xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * ldf),
       sqnS(ctx, sizeof(double) * 256), idS(ctx, sizeof(double) * 256);
@@ -405,7 +409,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       launch_gather_records(prop.as<double>(), lay.rec, 2 + dpad + kcur, kept_idx.as<int>(), mk,
                             propk.as<double>(), st);
       launch_hblock(propk.as<double>(), lay, mk, (int)dpad, (int)d, (int)kcur, kind, kfun, kspec.sigma,
-                    Hbuf.as<double>(), st);
+                    Hbuf.as<double>(), st, hb_part.as<double>(), hb_tick.as<unsigned>());
       launches += 2;
       for (int attempt = 0;; ++attempt) {
         launch_sweep(Hbuf.as<double>(), mk, cfg.seed, 0, propk.as<double>(), lay, pos.as<int>(),
@@ -441,7 +445,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     } else {
     // -- K3: H block; K4: rejection sweep (replicated on every shard)
     launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kfun, kspec.sigma,
-                  Hbuf.as<double>(), st);
+                  Hbuf.as<double>(), st, hb_part.as<double>(), hb_tick.as<unsigned>());
     dbg(st, "hblock");
     // the sweep's tail also publishes the round status into mapped host memory
     launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,

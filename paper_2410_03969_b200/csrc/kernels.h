@@ -82,8 +82,21 @@ void launch_replay_scan(const double* u, int64_t n, double* cumsum, ScanStatus* 
 void launch_replay_sample(const SampleParams& p, const double* cumsum, cudaStream_t st);
 
 // ---- K3/K4: H block, rejection sweep, L^{-1} ------------------------------
+// part (hblock_scratch_doubles) / tickets (zeroed once, hblock_tickets entries, self-resetting):
+// split-K scratch; nullptr = one CTA per tile over the whole k range.
 void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d, int kcur,
-                   int kind, int kfun, double sigma, double* H, cudaStream_t st);
+                   int kind, int kfun, double sigma, double* H, cudaStream_t st,
+                   double* part = nullptr, unsigned* tickets = nullptr);
+int hblock_splits(int b, int kcur);
+// any block of at most b proposals: splits * nb^2 <= max(nb^2, 2 * 296) (hblock_splits)
+inline size_t hblock_scratch_doubles(int b) {
+  const size_t nb = (size_t)(b + 15) / 16;
+  return (nb * nb > 592 ? nb * nb : 592) * 256;
+}
+inline size_t hblock_tickets(int b) {
+  const int nb = (b + 15) / 16;
+  return (size_t)nb * nb;
+}
 struct SweepOut {
   int32_t m;
   int32_t pad;

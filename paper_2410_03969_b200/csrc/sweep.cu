@@ -12,25 +12,34 @@
 // proposal, counters draw0 + i), root = sqrt(h_ii), l_j = h_ji / root,
 // h_pq -= l_p * l_q with two roundings.  Only the lower triangle of H is ever
 // read by the reference sweep, so it is held packed in shared memory.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kentry.cuh"
 #include "kernels.h"
 
 namespace rpcb {
 
-// One 16 x 16 tile of H per CTA (lower-triangle tiles only: the sweep reads q <= p).  The
-// F(S', :) products are summed sequentially over k (no FMA), so H is bitwise the oracle's;
-// the 128-wide k slabs are double-buffered through registers so the L2 latency of slab
+// One 16 x 16 tile of H per CTA (lower-triangle tiles only: the sweep reads q <= p), its
+// k range split over gridDim.z CTAs so the dependent add chains are short: CTA z sums
+// k in its slab sequentially (no FMA) into part[z][tile][256]; the last CTA of a tile to
+// finish (ticket counter, self-resetting) adds the slab partials in slab order and writes
+// H = A(S', S') - total.  The order is fixed, so H is the same on every shard and run.
+// The 128-wide k slabs are double-buffered through registers so the L2 latency of slab
 // s + 1 hides behind the dependent add chain of slab s.
 __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ prop,
                                                      RecordLayout lay, int b, int d, int kcur,
                                                      int kind, int kfun, double sigma,
-                                                     double* __restrict__ H) {
+                                                     double* __restrict__ H, int kslab,
+                                                     double* __restrict__ part,
+                                                     unsigned* __restrict__ tickets) {
   if (blockIdx.x > blockIdx.y) return;
   __shared__ double sp[16][129];
   __shared__ double sq[16][129];
+  __shared__ int s_last;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
   const int p = blockIdx.y * 16 + ty, q = blockIdx.x * 16 + tx;
+  const int ks0 = blockIdx.z * kslab, ks1 = min(kcur, ks0 + kslab);
   // this thread's share of a slab: rows rr0 + 2 e, column kk
   const int kk = tid & 127, rr0 = tid >> 7;
   const double* rp[8];
@@ -47,7 +56,7 @@ __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ 
   }
   double np[8], nq[8];
   auto fetch = [&](int k0) {
-    const bool kin = k0 + kk < kcur;
+    const bool kin = k0 + kk < ks1;
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       np[e] = (vp[e] && kin) ? __ldg(rp[e] + k0) : 0.0;
@@ -55,19 +64,34 @@ __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ 
     }
   };
   double acc = 0.0;
-  if (kcur > 0) fetch(0);
-  for (int k0 = 0; k0 < kcur; k0 += 128) {
+  if (ks0 < ks1) fetch(ks0);
+  for (int k0 = ks0; k0 < ks1; k0 += 128) {
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
       sp[rr0 + 2 * e][kk] = np[e];
       sq[rr0 + 2 * e][kk] = nq[e];
     }
     __syncthreads();
-    if (k0 + 128 < kcur) fetch(k0 + 128);
-    const int kend = min(128, kcur - k0);
+    if (k0 + 128 < ks1) fetch(k0 + 128);
+    const int kend = min(128, ks1 - k0);
 #pragma unroll 8
     for (int k = 0; k < kend; ++k) acc = __dadd_rn(acc, __dmul_rn(sp[ty][k], sq[tx][k]));
     __syncthreads();
+  }
+  const int nz = gridDim.z;
+  if (nz > 1) {
+    const int tile = blockIdx.y * gridDim.x + blockIdx.x;
+    part[((int64_t)blockIdx.z * gridDim.x * gridDim.y + tile) * 256 + tid] = acc;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(&tickets[tile], 1u) == (unsigned)(nz - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    acc = 0.0;
+    for (int z = 0; z < nz; ++z)
+      acc = __dadd_rn(acc, __ldcg(part + ((int64_t)z * gridDim.x * gridDim.y + tile) * 256 + tid));
+    if (tid == 0) tickets[tile] = 0u;
   }
   if (p < b && q < b && q <= p) {
     const double a = kernel_entry(prop + (int64_t)p * lay.rec, prop + (int64_t)q * lay.rec, lay,
@@ -76,12 +100,22 @@ __global__ void __launch_bounds__(256) hblock_kernel(const double* __restrict__ 
   }
 }
 
+int hblock_splits(int b, int kcur) {
+  const int nb = (b + 15) / 16, tiles = nb * (nb + 1) / 2;
+  const int by_k = (kcur + 127) / 128;
+  const int by_grid = std::max(1, 296 / tiles);  // ~2 CTAs per SM
+  return std::max(1, std::min(by_k, by_grid));
+}
+
 void launch_hblock(const double* prop, RecordLayout lay, int b, int dpad, int d, int kcur,
-                   int kind, int kfun, double sigma, double* H, cudaStream_t st) {
+                   int kind, int kfun, double sigma, double* H, cudaStream_t st, double* part,
+                   unsigned* tickets) {
   (void)dpad;
   const int nb = (b + 15) / 16;
-  hblock_kernel<<<dim3(nb, nb), dim3(16, 16), 0, st>>>(prop, lay, b, d, kcur, kind, kfun, sigma,
-                                                        H);
+  const int nz = part && tickets ? hblock_splits(b, kcur) : 1;
+  const int kslab = nz > 1 ? (((kcur + nz - 1) / nz + 127) / 128) * 128 : std::max(kcur, 1);
+  hblock_kernel<<<dim3(nb, nb, nz), dim3(16, 16), 0, st>>>(prop, lay, b, d, kcur, kind, kfun,
+                                                            sigma, H, kslab, part, tickets);
 }
 
 #ifdef RPC_SWEEP_PROBE  // debug aid (tools/sweep_probe.cu): per-block phase clocks
