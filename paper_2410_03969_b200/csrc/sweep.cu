@@ -233,7 +233,9 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
 #pragma unroll
         for (int q = 0; q < kSweepBlock; ++q) {
           if (q <= ii) continue;
-          const double lq = __shfl_sync(0xffffffffu, lp, q);
+          // lane q's l value from the in-block store above (one broadcast LDS.64 instead of
+          // two 32-bit shuffles; read only where lane q was live)
+          const double lq = lblk[nacc * kSweepBlock + q];
           if (live && i0 + q <= p) row[q] = __dsub_rn(row[q], __dmul_rn(lp, lq));
         }
         if (lane == 0) {
