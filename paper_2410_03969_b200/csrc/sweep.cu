@@ -230,13 +230,21 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
         STEP_CLK(i, 3)
         if (live && p >= i) lblk[nacc * kSweepBlock + (p - i0)] = lp;
         __syncwarp();
+        // lanes q's l values from the in-block store above (broadcast LDS.128 pairs instead of
+        // 32-bit shuffles; read only where lane q was live), all loads issued before the
+        // updates so they overlap instead of queueing behind one temporary register
+        {
+          const double2* lb2 = reinterpret_cast<const double2*>(lblk + nacc * kSweepBlock);
+          double2 lqp[kSweepBlock / 2];
 #pragma unroll
-        for (int q = 0; q < kSweepBlock; ++q) {
-          if (q <= ii) continue;
-          // lane q's l value from the in-block store above (one broadcast LDS.64 instead of
-          // two 32-bit shuffles; read only where lane q was live)
-          const double lq = lblk[nacc * kSweepBlock + q];
-          if (live && i0 + q <= p) row[q] = __dsub_rn(row[q], __dmul_rn(lp, lq));
+          for (int h = 0; h < kSweepBlock / 2; ++h)
+            if (2 * h + 1 > ii) lqp[h] = lb2[h];
+#pragma unroll
+          for (int q = 0; q < kSweepBlock; ++q) {
+            if (q <= ii) continue;
+            const double lq = (q & 1) ? lqp[q >> 1].y : lqp[q >> 1].x;
+            if (live && i0 + q <= p) row[q] = __dsub_rn(row[q], __dmul_rn(lp, lq));
+          }
         }
         if (lane == 0) {
           s_acc[nacc] = i;
