@@ -13,6 +13,8 @@
 // the shards exchange only: chunk totals (+ previous round ||G||^2 partials),
 // and the b proposal records (id, ||x||^2, x, F row).  The sweep and L^{-1}
 // are computed redundantly and bit-identically on every shard.
+#include <atomic>
+
 #include "runtime.h"
 
 namespace rpcb_rt {
@@ -24,6 +26,37 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
   const int64_t lr = piv[i] - row0;
   if (lr < 0 || lr >= n_loc) return;
   for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[j * k + i] = F[lr * ldf + j];
+}
+
+// Launch tags of the fused sweep + prep (its progress word and the host sequence word):
+// unique per launch within the process.
+static unsigned next_epoch() {
+  static std::atomic<unsigned> e{0x5eed0001u};
+  unsigned v = e.fetch_add(1u);
+  return v ? v : e.fetch_add(1u);
+}
+
+// Host wait for the fused launch's status publish: spin on the sequence word the sweep
+// writes last into mapped pinned memory (no event-completion round trip).  Every few
+// thousand polls the launch's event is queried: an event that completed (or failed) without
+// the word means a fault, reported instead of spinning forever.
+static void wait_published(const int32_t* seq, unsigned epoch, cudaEvent_t ev) {
+  const volatile int32_t* w = seq;
+  for (unsigned it = 1;; ++it) {
+    if ((unsigned)*w == epoch) break;
+    if ((it & 4095u) == 0) {
+      const cudaError_t e = cudaEventQuery(ev);
+      if (e == cudaErrorNotReady) continue;
+      if ((unsigned)*w == epoch) break;
+      CK(e);
+      CK(cudaGetLastError());
+      throw RpcError{RPC_ECUDA, "round status was not published by the sweep"};
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
 }
 
 // The factorization proper.  `src` points to this process's shard rows (device
@@ -194,6 +227,23 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   if (grouped) lsub = DBuf(ctx, sizeof(double) * kGroup * kGroup);
   DBuf prefix_counter(ctx, sizeof(unsigned));
   CK(cudaMemsetAsync(prefix_counter.p, 0, sizeof(unsigned), st));
+  // fast-scan thread bases (sampler) and the update-fused scan's chunk bookkeeping
+  DBuf tb_all(ctx, sizeof(double) * (size_t)L.ncg * kScanThreads);
+  const bool fuse_scan_ok = P == 1 && ctx->world == 1 && !lowmem && !replay && L.ncg <= 4096 &&
+                            std::getenv("RPC_NO_FUSED_SCAN") == nullptr;
+  DBuf scan_tsum;
+  if (fuse_scan_ok) {
+    const int64_t ntiles64 = (res->shards[0].n_loc + 63) / 64;
+    scan_tsum = DBuf(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, 4 * ntiles64));
+  }
+  // true while the last update's 16-row run sums (tsum) describe the current u: the next
+  // scan then chains them (launch_chunk_chain, 1/16 of u's bytes) instead of a totals pass
+  // over u, and the sampler chains the chunk offsets
+  bool scan_fresh = false;
+  // fused sweep + round prep (accelerated, b <= 128, one group): progress word + acceptance map
+  DBuf sweep_prog(ctx, sizeof(unsigned long long)), sweep_aidx(ctx, sizeof(int) * b);
+  CK(cudaMemsetAsync(sweep_prog.p, 0, sizeof(unsigned long long), st));
+  const bool fused_prep_ok = std::getenv("RPC_NO_FUSED_PREP") == nullptr;
   DBuf kept_idx, propk;  // block / simple: kept proposals (first draw of each distinct id)
   if (algo != kAlgoAccelerated) {
     kept_idx = DBuf(ctx, sizeof(int) * b);
@@ -255,6 +305,17 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   const bool dbg_gaps = std::getenv("RPC_DEBUG_GAPS") != nullptr;
   std::vector<Ev> gap_ev;
   gap_ev.reserve(64);
+  // RPC_DEBUG_CHAIN: an event after every per-round stage; the elapsed time between
+  // consecutive marks is charged to the later label (device timeline incl. launch gaps)
+  const bool dbg_chain = std::getenv("RPC_DEBUG_CHAIN") != nullptr;
+  std::vector<std::pair<const char*, Ev>> chain_ev;
+  chain_ev.reserve(dbg_chain ? 1024 : 0);
+  double host_pre_us = 0.0, host_launch_us = 0.0;  // RPC_DEBUG_CHAIN: wake -> launch, launch call
+  auto cmark = [&](const char* what) {
+    if (!dbg_chain) return;
+    chain_ev.emplace_back(what, Ev());
+    CK(cudaEventRecord(chain_ev.back().second.e, st));
+  };
   DBuf trace_buf(ctx, dbg_trace ? sizeof(unsigned long long) * 2 * 64 * 8 : 8);
   DBuf phase_clk(ctx, dbg_phase ? sizeof(unsigned long long) * 8 * 4096 : 8);
   std::vector<double> upd_flops;
@@ -291,6 +352,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   for (int64_t round = 0;; ++round) {
     if (cfg.mode == RPC_FIXED_ROUNDS ? round >= cfg.rounds : kcur >= cfg.target_rank) break;
     NvtxRange nv_round("rpc:round");
+    cmark("round start");
     // SplitMix64 draw counters: accelerated uses b proposal + b accept draws per round
     // (rpcholesky.hpp:362-364, 179), block b proposals (293-296), simple one (226)
     const uint64_t draw0 = (algo == kAlgoAccelerated ? 2ull : 1ull) * (uint64_t)b * (uint64_t)round;
@@ -305,14 +367,24 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       fp.status = d_scan;
       fp.g2_all = pending_g2 ? g2_all.as<double>() : nullptr;
     }
+    // (skipped when the previous update already chained its scan: chunk ends, thread bases
+    // and the round status are current)
+    if (scan_fresh) {
+      Shard& s = res->shards[0];
+      launch_chunk_chain(scan_tsum.as<double>(), s.tile_g2.as<double>(), s.n_loc, s.nchunks,
+                         tb_all.as<double>(), totals_all.as<double>(), g2_all.as<double>(), st);
+      ++launches;
+    }
     for (Shard& s : res->shards) {
+      if (scan_fresh) break;
       // (+ the previous update's per-tile ||G||^2 partials -> per-chunk, fixed order)
       launch_chunk_totals(s.u.as<double>(), s.n_loc, s.nchunks, totals_all.as<double>() + s.chunk0, st,
                           pending_g2 && s.n_loc ? s.tile_g2.as<double>() : nullptr,
-                          (int)((s.n_loc + 63) / 64), g2_all.as<double>() + s.chunk0, fp);
+                          (int)((s.n_loc + 63) / 64), g2_all.as<double>() + s.chunk0, fp,
+                          tb_all.as<double>() + (size_t)s.chunk0 * kScanThreads);
       ++launches;
     }
-    if (!fuse_prefix) {
+    if (!fuse_prefix && !scan_fresh) {
       allgather(ctx, totals_all.as<double>(), L.cpr);
       if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
       launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr,
@@ -320,6 +392,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       ++launches;
     }
     dbg(st, "scan");
+    cmark("chunk totals");
     if (replay) {
       const double* ug = res->shards[0].u.as<double>();
       if (P > 1) {
@@ -360,6 +433,13 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.lay = lay;
       sp.records = prop.as<double>();  // the owner of draw j writes slot j
       sp.owner = owner.as<int>();
+      sp.tb = tb_all.as<double>() + (size_t)s.chunk0 * kScanThreads;
+      if (scan_fresh && !replay) {  // (one shard) offsets + status from the update's chunk totals
+        sp.totals = totals_all.as<double>();
+        sp.chunk_g2 = g2_all.as<double>();
+        sp.chunk_end_out = chunk_end.as<double>();
+        sp.status = d_scan;
+      }
       // every shard runs the sampler, including shards without rows (it returns early for
       // draws it does not own)
       if (replay) launch_replay_sample(sp, cumsum.as<double>(), st);
@@ -367,6 +447,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       dbg(st, "sample");
       ++launches;
     }
+    cmark("sample");
     allreduce_owner(ctx, prop.p, (size_t)b * lay.rec);
     if (lowmem && kcur > 0) {
       // F(S', :) = A(S', S) L^{-T}  (= W_prop^T of rpcholesky.hpp:441-444)
@@ -377,6 +458,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       launches += 2;
       dbg(st, "lowmem fprop");
     }
+    auto h_wake = clk::now();  // (RPC_DEBUG_CHAIN) the host learned the round's status
     if (algo != kAlgoAccelerated) {
       // ---- block_rpcholesky (rpcholesky.hpp:268-333) / simple_rpcholesky (206-246):
       // every distinct proposal is kept (sorted), its block factored by an all-accepting
@@ -447,11 +529,28 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     launch_hblock(prop.as<double>(), lay, b, (int)dpad, (int)d, (int)kcur, kind, kfun, kspec.sigma,
                   Hbuf.as<double>(), st, hb_part.as<double>(), hb_tick.as<unsigned>());
     dbg(st, "hblock");
+    cmark("hblock");
     // the sweep's tail also publishes the round status into mapped host memory
-    launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
-                 pos.as<int>(), acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(), d_sweep,
-                 hp.as<double>(), st, 0, hbuf_dev ? d_scan : nullptr, hbuf_dev);
+    // (fused: the round prep runs in the same launch behind the sweep, and the host spins on
+    // the status's sequence word instead of an event)
+    bool fused = false;
+    const unsigned epoch = next_epoch();
+    if (fused_prep_ok && hbuf_dev && !grouped && !lowmem && b <= 128) {
+      const int g = launch_sweep_prep(
+          Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
+          pos.as<int>(), acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(), d_sweep,
+          d_scan, hbuf_dev, sweep_prog.as<unsigned long long>(), sweep_aidx.as<int>(), epoch,
+          (int)nbl, ldl, linv.as<double>(), (int)kcur, fs.as<double>(), ldf, (int)dpad,
+          xs.as<double>(), sqnS.as<double>(), idS.as<double>(), gram_xscale(kind), 256, st);
+      if (g < 0 && g != -3) CK(cudaGetLastError());
+      fused = g > 0;
+    }
+    if (!fused)
+      launch_sweep(Hbuf.as<double>(), b, cfg.seed, draw0 + (uint64_t)b, prop.as<double>(), lay,
+                   pos.as<int>(), acc_ids.as<int64_t>(), lcol.as<double>(), lacc.as<double>(),
+                   d_sweep, hp.as<double>(), st, 0, hbuf_dev ? d_scan : nullptr, hbuf_dev);
     dbg(st, "sweep");
+    cmark("sweep");
     launches += 2;
     if (hbuf_dev) {
       // status words went straight into mapped host memory (sweep tail): no copy-engine
@@ -463,7 +562,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     // L^{-1} and the accepted-pivot operands only need the sweep's device-side outputs:
     // queue them before the status read so they run while the host waits (grouped rounds
     // build them per group once m is known).
-    if (!grouped) {
+    if (!grouped && !fused) {
       // (no memset of the L^{-1} buffer: both kernels write every row of every column the
       // consumers read, zeros included)
       if (lowmem) {
@@ -479,6 +578,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         ++launches;
       }
     }
+    cmark("round prep");
     if (dbg_gaps) {  // RPC_DEBUG_GAPS: device idle between the round prep and the update
       gap_ev.emplace_back();
       CK(cudaEventRecord(gap_ev.back().e, st));
@@ -492,8 +592,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                            sizeof(double), b, cudaMemcpyDeviceToHost, st));
       CK(cudaMemcpyAsync(h_acc_ids, acc_ids.p, sizeof(int64_t) * b, cudaMemcpyDeviceToHost, st));
     }
-    if (hbuf_dev) CK(cudaEventSynchronize(ev_pub.e));
+    if (fused) wait_published(&h_sweep->pad, epoch, ev_pub.e);
+    else if (hbuf_dev) CK(cudaEventSynchronize(ev_pub.e));
     else CK(cudaStreamSynchronize(st));
+    h_wake = clk::now();
     }  // accelerated
     CK(cudaGetLastError());
     if (pending_g2) {
@@ -617,6 +719,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.kfun = kernel_fun(kspec, &up.escale);
         up.tile_g2 = s.tile_g2.as<double>();
         up.g2_accum = g0 > 0;  // later groups add their ||G||^2 to the round's tile partials
+        const bool fscan = fuse_scan_ok && !grouped && algo == kAlgoAccelerated &&
+                           update_regp2(mg) && update_tile_rows(mg) == 64;
+        if (fscan) up.tsum = scan_tsum.as<double>();
+        scan_fresh = fscan;
         if (dbg_trace) {
           CK(cudaMemsetAsync(trace_buf.p, 0, trace_buf.bytes, st));
           up.trace = trace_buf.as<unsigned long long>();
@@ -628,9 +734,14 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         upd_ev.emplace_back();
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
+        if (dbg_chain) host_pre_us += 1e3 * ms_since(h_wake);
+        cmark("host gap");
+        const auto h_l0 = clk::now();
         const int bm = launch_update(up, st);
+        if (dbg_chain) host_launch_us += 1e3 * ms_since(h_l0);
         CK(cudaEventRecord(upd_ev.back().e, st));
         dbg(st, "update");
+        cmark("update");
         if (dbg_phase) {
           std::vector<unsigned long long> h(phase_clk.bytes / 8);
           CK(cudaMemcpyAsync(h.data(), phase_clk.p, phase_clk.bytes, cudaMemcpyDeviceToHost, st));
@@ -763,6 +874,23 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       std::fprintf(stderr, "[rpc] round %zu: prep end -> update start %.3f ms\n", i, ms);
     }
     std::fprintf(stderr, "[rpc] total prep->update gap %.3f ms\n", tot);
+  }
+  if (dbg_chain && chain_ev.size() > 1) {
+    std::vector<std::pair<std::string, std::pair<double, int>>> agg;
+    for (size_t i = 1; i < chain_ev.size(); ++i) {
+      CK(cudaEventElapsedTime(&ms, chain_ev[i - 1].second.e, chain_ev[i].second.e));
+      std::string lab = chain_ev[i].first;
+      auto it = std::find_if(agg.begin(), agg.end(), [&](auto& a) { return a.first == lab; });
+      if (it == agg.end()) agg.push_back({lab, {ms, 1}});
+      else it->second.first += ms, it->second.second += 1;
+    }
+    for (auto& a : agg)
+      std::fprintf(stderr, "[rpc] chain %-14s %4d x  avg %8.1f us  total %8.3f ms\n",
+                   a.first.c_str(), a.second.second, 1e3 * a.second.first / a.second.second,
+                   a.second.first);
+    std::fprintf(stderr, "[rpc] host: wake -> update launch %.1f us, launch call %.1f us (per update)\n",
+                 host_pre_us / std::max<int64_t>(1, upd_launches),
+                 host_launch_us / std::max<int64_t>(1, upd_launches));
   }
   tm.update_flops = flops;
   tm.update_bytes = bytes;
@@ -1483,7 +1611,11 @@ int rpc_sample_discrete(rpc_ctx* ctx, const double* u, int64_t n, int64_t b, uin
       if (hs.exhausted) raise(RPC_EINVAL, "sample_discrete: total weight must be > 0");
       launch_replay_sample(sp, cs.as<double>(), st);
     } else {
-      launch_chunk_totals(du.as<double>(), n, L.nc, totals.as<double>(), st);
+      // thread bases for the sampler (RPC_NO_TB_SAMPLER: the rescanning sampler instead)
+      DBuf tbd(ctx, sizeof(double) * (size_t)L.ncg * kScanThreads);
+      launch_chunk_totals(du.as<double>(), n, L.nc, totals.as<double>(), st, nullptr, 0, nullptr,
+                          FusedPrefix(), tbd.as<double>());
+      if (!std::getenv("RPC_NO_TB_SAMPLER")) sp.tb = tbd.as<double>();
       CK(cudaMemsetAsync(totals.as<double>() + L.nc, 0, sizeof(double) * (L.ncg - L.nc), st));
       launch_chunk_prefix(totals.as<double>(), nullptr, L.ncg, cend.as<double>(),
                           status.as<ScanStatus>(), st);

@@ -47,7 +47,8 @@ struct FusedPrefix {
 // chunk_g2[c] in fixed order (the update kernels' tiles are 64 rows: 64 tiles per chunk).
 void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
                          cudaStream_t st, const double* tile_g2 = nullptr, int n_tiles = 0,
-                         double* chunk_g2 = nullptr, FusedPrefix fp = FusedPrefix());
+                         double* chunk_g2 = nullptr, FusedPrefix fp = FusedPrefix(),
+                         double* tb = nullptr);
 void launch_chunk_prefix(const double* totals_all, const double* g2_all, int n_chunks,
                          double* chunk_end, ScanStatus* status, cudaStream_t st);
 // One CTA per draw: draw j uses SplitMix64 counter draw0 + j.
@@ -72,6 +73,16 @@ struct SampleParams {
   RecordLayout lay;
   double* records;          // this shard's slot: [b][rec]
   int* owner;               // [b]
+  // thread bases of the fast scan, tb[lc][t] = B_(t+1) of local chunk lc (written by the
+  // chunk-totals pass or by the fused update); null: the sampler rescans the drawn chunk
+  const double* tb = nullptr;
+  // with tb: per-chunk totals / ||G||^2 partials of the previous update (fused scan); the
+  // sampler then chains the chunk offsets itself (chunk_prefix_kernel's order), writes them
+  // to chunk_end and the round status (total, g2_prev, exhausted) to *status (draw 0's CTA)
+  const double* totals = nullptr;
+  const double* chunk_g2 = nullptr;
+  double* chunk_end_out = nullptr;
+  ScanStatus* status = nullptr;
 };
 void launch_sample(const SampleParams& p, cudaStream_t st);
 // Replay mode: strictly sequential cumulative_sums (rng.hpp:67-75) over the global
@@ -155,6 +166,10 @@ struct UpdateParams {
   int g2_accum;                                 // add to tile_g2 instead of storing (grouped rounds)
   // columns-only mode (standalone K5: A(:, S) -> cols_out col-major [m][ld_out])
   int columns_only; double* cols_out; int64_t ld_out;
+  // Scan partials (single warp column, 64-row tiles, tsum != null): the epilogue also writes
+  // each 16-row run's sequential sum of the new u (tsum[row / 16] = chunk_scan_core's
+  // per-thread sum), so the next round's scan reads 1/16 of u (launch_chunk_chain).
+  double* tsum;
   // RPC_DEBUG_TIMING: per-CTA cycle counters per phase ([grid][8] u64), or null
   unsigned long long* phase_clk;
   // RPC_DEBUG_TRACE: CTA 0 per-group phase clocks [G][64 tiles][8] (debug only)
@@ -176,6 +191,19 @@ void launch_bprime(const double* linv_rm, int64_t ldl, int koff, const double* p
 // linv (as launch_linv_dev, update layout) + B' = -L^{-1} F_S (forward substitution, into
 // bp rows perm_row(a) < m, columns < kcur) + the accepted X rows / norms / ids (as
 // launch_gather_accepted without F rows; n_rows operand rows, zero beyond m), one launch.
+// Sweep + round prep in one cooperative launch (b <= 128): CTA 0 sweeps (as launch_sweep
+// with the mapped-memory publish, plus a sequence word SweepOut::pad = epoch written last),
+// the other CTAs form L^{-1}, B' and the accepted operands (as launch_round_prep with
+// m_dev) behind it from its per-block progress word.  prog: one u64 (any initial value);
+// aidx: [b] ints.  epoch must differ between launches sharing prog.  Returns the grid size,
+// or < 0 when the launch is not possible (caller falls back to the two launches).
+int launch_sweep_prep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
+                      RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol,
+                      double* lacc_cm, SweepOut* out, const ScanStatus* pub_scan,
+                      char* pub_host, unsigned long long* prog, int* aidx, unsigned epoch,
+                      int nb, int64_t ldl, double* linv_rm, int kcur, double* bp, int64_t ldbp,
+                      int dpad, double* xs, double* sqnS, double* idS, double xscale,
+                      int n_rows, cudaStream_t st);
 void launch_round_prep(const double* lacc_cm, int m_host, const int* m_dev, int m_max, int nb,
                        int64_t ldl, int koff, double* linv_rm, const double* prop,
                        RecordLayout lay, const int* pos, int kcur, double* bp, int64_t ldbp,
@@ -190,6 +218,11 @@ void launch_gather_accepted(const double* prop, RecordLayout lay, const int* pos
                             double* sqnS, double* idS, cudaStream_t st,
                             const int* m_dev = nullptr, double xscale = 1.0);
 inline double gram_xscale(int kind) { return kind == kGaussGram ? -2.0 : 1.0; }
+// From the update's 16-row run sums (UpdateParams::tsum) and tile ||G||^2 partials: per
+// local chunk the thread bases tb[c][t] = B_(t+1), totals[c] and chunk_g2[c] (tile order),
+// with chunk_totals_kernel's serial association (bitwise the same values).
+void launch_chunk_chain(const double* tsum, const double* tile_g2, int64_t n_loc, int n_chunks,
+                        double* tb, double* totals, double* chunk_g2, cudaStream_t st);
 // per-chunk sum of per-tile partials (tile = rows_per_tile rows)
 void launch_tile_to_chunk(const double* tile_g2, int n_tiles, int tiles_per_chunk,
                           int n_chunks_local, double* chunk_g2, cudaStream_t st);

@@ -81,13 +81,15 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
                                                                     const double* __restrict__ tile_g2,
                                                                     int n_tiles,
                                                                     double* __restrict__ chunk_g2,
-                                                                    FusedPrefix fp) {
+                                                                    FusedPrefix fp,
+                                                                    double* __restrict__ tb) {
   __shared__ double sh[kScanThreads + 1];
   const int c = blockIdx.x;
   const int64_t r0 = (int64_t)c * kChunk;
   const int n_valid = (int)lmin(kChunk, n_loc - r0);
   double s[16];
   const double base = chunk_scan_core(u + r0, n_valid, s, sh);
+  if (tb) tb[(int64_t)c * kScanThreads + threadIdx.x] = sh[threadIdx.x + 1];  // B_(t+1)
   const int last = n_valid - 1;
   if (threadIdx.x == (last >> 4)) {
     double v = 0.0;
@@ -149,10 +151,62 @@ __global__ void __launch_bounds__(kScanThreads) chunk_totals_kernel(const double
 
 void launch_chunk_totals(const double* u, int64_t n_loc, int n_chunks, double* totals,
                          cudaStream_t st, const double* tile_g2, int n_tiles, double* chunk_g2,
-                         FusedPrefix fp) {
+                         FusedPrefix fp, double* tb) {
   if (n_chunks > 0)
     chunk_totals_kernel<<<n_chunks, kScanThreads, 0, st>>>(u, n_loc, totals, tile_g2, n_tiles,
-                                                           chunk_g2, fp);
+                                                           chunk_g2, fp, tb);
+}
+
+// One warp per chunk: lane l holds runs 8l .. 8l + 7 and tiles 2l, 2l + 1; the serial chains
+// B_(t+1) = B_t + s_t and g = g + tile_g2 pass from lane to lane in order.
+__global__ void __launch_bounds__(32) chunk_chain_kernel(const double* __restrict__ tsum,
+                                                         const double* __restrict__ tile_g2,
+                                                         int64_t n_loc, double* __restrict__ tb,
+                                                         double* __restrict__ totals,
+                                                         double* __restrict__ chunk_g2) {
+  constexpr int kTiles = kChunk / 64;
+  const int c = blockIdx.x, lane = threadIdx.x;
+  const int64_t r0 = (int64_t)c * kChunk;
+  const int nrun = (int)((lmin(kChunk, n_loc - r0) + 15) / 16);   // runs holding rows
+  const int ntl = (int)((lmin(kChunk, n_loc - r0) + 63) / 64);    // tiles holding rows
+  double v[8], gt[2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int t = 8 * lane + i;
+    v[i] = t < nrun ? __ldg(tsum + (int64_t)c * kScanThreads + t) : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const int tl = 2 * lane + i;
+    gt[i] = tl < ntl ? __ldg(tile_g2 + (int64_t)c * kTiles + tl) : 0.0;
+  }
+  double bsum = 0.0, gsum = 0.0;
+  for (int L = 0; L < 32; ++L) {
+    if (lane == L) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        bsum = __dadd_rn(bsum, v[i]);
+        v[i] = bsum;
+      }
+      if (2 * L < ntl) gsum = __dadd_rn(gsum, gt[0]);
+      if (2 * L + 1 < ntl) gsum = __dadd_rn(gsum, gt[1]);
+    }
+    bsum = __shfl_sync(0xffffffffu, bsum, L);
+    gsum = __shfl_sync(0xffffffffu, gsum, L);
+  }
+  double2* o2 = reinterpret_cast<double2*>(tb + (int64_t)c * kScanThreads + 8 * lane);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) o2[i] = make_double2(v[2 * i], v[2 * i + 1]);
+  if (lane == 0) {
+    totals[c] = bsum;
+    chunk_g2[c] = gsum;
+  }
+}
+
+void launch_chunk_chain(const double* tsum, const double* tile_g2, int64_t n_loc, int n_chunks,
+                        double* tb, double* totals, double* chunk_g2, cudaStream_t st) {
+  if (n_chunks > 0)
+    chunk_chain_kernel<<<n_chunks, 32, 0, st>>>(tsum, tile_g2, n_loc, tb, totals, chunk_g2);
 }
 
 // Serial chunk-offset chain (fixed order => p-invariant).  The totals are staged in
@@ -284,10 +338,129 @@ __global__ void __launch_bounds__(kScanThreads) sample_kernel(SampleParams p) {
   write_record(p, r0 + best, p.records + (int64_t)j * p.lay.rec);
 }
 
+// Same draws from the stored thread bases (p.tb): thread t of the drawn chunk knows where
+// its 16-row run starts (B_t) and ends (B_(t+1)), so the run holding the first cumsum > target
+// is found without rescanning the chunk (no 256-long base chain per draw); only that thread
+// re-adds its 16 rows.  Identical result: the fast cumsum is monotone, cum_i =
+// off + (B_t + s_e), and a run contains the first index above the target iff its end is
+// above it and its start is not (plateau mode: iff its end exceeds its start).
+__global__ void __launch_bounds__(kScanThreads) sample_tb_kernel(SampleParams p) {
+  __shared__ int s_chunk, s_mode, s_owner, s_best;
+  __shared__ double s_off, s_target;
+  extern __shared__ double s_ends[];  // [nc] when staged (+ [nc] g2 partials, CTA 0, fused)
+  const int j = blockIdx.x;
+  const int nc = p.n_chunks_global;
+  const bool staged = nc <= kSampleStageMax;
+  if (p.totals) {
+    // fused scan: the chunk offsets from the previous update's chunk totals, chained in
+    // chunk_prefix_kernel's order by every CTA (thread 0, out of shared memory); draw 0's CTA
+    // also chains the ||G||^2 partials and publishes the offsets and the round status
+    double* s_g2 = s_ends + nc;
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) {
+      s_ends[c] = __ldg(p.totals + c);
+      if (j == 0) s_g2[c] = __ldg(p.chunk_g2 + c);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double off = 0.0;
+      for (int c = 0; c < nc; ++c) {
+        off = __dadd_rn(off, s_ends[c]);
+        s_ends[c] = off;
+      }
+    } else if (j == 0 && threadIdx.x == 32) {
+      double g2 = 0.0;
+      for (int c = 0; c < nc; ++c) g2 = __dadd_rn(g2, s_g2[c]);
+      s_g2[0] = g2;
+    }
+    __syncthreads();
+    if (j == 0) {
+      for (int c = threadIdx.x; c < nc; c += blockDim.x) p.chunk_end_out[c] = s_ends[c];
+      if (threadIdx.x == 0) {
+        p.status->total = s_ends[nc - 1];
+        p.status->g2_prev = s_g2[0];
+        p.status->exhausted = !(s_ends[nc - 1] > 0.0);
+      }
+    }
+  } else if (staged) {
+    for (int c = threadIdx.x; c < nc; c += blockDim.x) s_ends[c] = p.chunk_end[c];
+    __syncthreads();
+  }
+  const double* ends = staged ? s_ends : p.chunk_end;
+  if (threadIdx.x == 0) {
+    const double r = u01(splitmix64_draw(p.seed, p.draw0 + (uint64_t)j));
+    const double total = ends[nc - 1];
+    const double target = __dmul_rn(r, total);
+    int lo = 0, hi = nc;  // upper_bound over chunk ends
+    while (lo < hi) {
+      const int mid = (lo + hi) >> 1;
+      if (target < ends[mid]) hi = mid; else lo = mid + 1;
+    }
+    int mode = 0;
+    if (lo == nc) {  // clamp to N-1, then walk back over the zero plateau
+      int c = nc - 1;
+      while (c > 0 && ends[c] == ends[c - 1]) --c;
+      lo = c;
+      mode = 1;
+    }
+    int o = 0;
+    while (o + 1 < p.n_shards && p.shard_chunk0[o + 1] <= lo) ++o;
+    s_chunk = lo;
+    s_mode = mode;
+    s_target = target;
+    s_off = lo ? ends[lo - 1] : 0.0;
+    s_owner = o;
+    s_best = -1;
+    p.owner[j] = o;
+  }
+  __syncthreads();
+  if (s_owner != p.shard) return;
+  const int lc = s_chunk - p.chunk0;
+  const int64_t r0 = (int64_t)lc * kChunk;
+  const int n_valid = (int)lmin(kChunk, p.n_loc - r0);
+  const int t = threadIdx.x, e0 = 16 * t;
+  const double* tbc = p.tb + (int64_t)lc * kScanThreads;
+  const double bend = __ldg(tbc + t), bstart = t ? __ldg(tbc + t - 1) : 0.0;
+  const double off = s_off, target = s_target;
+  const double cend = __dadd_rn(off, bend), cstart = __dadd_rn(off, bstart);
+  if (s_mode == 0) {
+    if (e0 < n_valid && cend > target && !(t > 0 && cstart > target)) {
+      double acc = 0.0;
+      int best = -1;
+      for (int e = 0; e < 16 && e0 + e < n_valid; ++e) {
+        acc = __dadd_rn(acc, __ldg(p.u + r0 + e0 + e));
+        if (__dadd_rn(off, __dadd_rn(bstart, acc)) > target) {
+          best = e0 + e;
+          break;
+        }
+      }
+      s_best = best;  // one run qualifies
+    }
+  } else if (e0 < n_valid && cend > cstart) {
+    atomicMax(&s_best, t);  // the last run with an increase
+  }
+  __syncthreads();
+  if (s_mode != 0 && t == s_best) {
+    double acc = 0.0, prev = cstart;
+    int best = -1;
+    for (int e = 0; e < 16 && e0 + e < n_valid; ++e) {
+      acc = __dadd_rn(acc, __ldg(p.u + r0 + e0 + e));
+      const double cum = __dadd_rn(off, __dadd_rn(bstart, acc));
+      if (cum > prev) best = e0 + e;
+      prev = cum;
+    }
+    s_best = best;
+  }
+  __syncthreads();
+  int best = s_best;
+  if (best < 0) best = 0;  // unreachable when total > 0
+  write_record(p, r0 + best, p.records + (int64_t)j * p.lay.rec);
+}
+
 void launch_sample(const SampleParams& p, cudaStream_t st) {
   const int nc = p.n_chunks_global;
   const size_t smem = nc <= kSampleStageMax ? sizeof(double) * (size_t)nc : 0;
-  sample_kernel<<<p.b, kScanThreads, smem, st>>>(p);
+  if (p.tb) sample_tb_kernel<<<p.b, kScanThreads, p.totals ? 2 * smem : smem, st>>>(p);
+  else sample_kernel<<<p.b, kScanThreads, smem, st>>>(p);
 }
 
 // ---- replay mode -----------------------------------------------------------

@@ -156,12 +156,32 @@ __device__ __forceinline__ int64_t tri(int p) { return (int64_t)p * (p + 1) / 2;
 //   3. all threads apply the block's accepted rank-1 updates to the trailing
 //      triangle, in acceptance order per entry.
 // Three CTA barriers per 16 steps instead of two per step.
-__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
+// Progress publication for the fused sweep + round-prep launch (sweep_prep_kernel): after
+// every 16-step block the sweep CTA releases (epoch << 32) | accepted-count, with the block's
+// L columns (lcol), positions (pos) and acceptance indices (aidx) written before; the final
+// count carries bit 31.  The prep workers acquire it and run their substitutions behind the
+// sweep.
+struct SweepProgress {
+  unsigned long long* prog;
+  int* aidx;  // [b] acceptance index of proposal j, -1 if rejected
+  unsigned epoch;
+};
+
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void sweep_body(
     const double* __restrict__ H, int b, uint64_t seed, uint64_t draw0,
     const double* __restrict__ prop, RecordLayout lay, int* __restrict__ pos,
     int64_t* __restrict__ acc_ids, double* __restrict__ lcol, double* __restrict__ lacc_cm,
     SweepOut* out, double* hp_global, int accept_all, const ScanStatus* pub_scan,
-    char* pub_host) {
+    char* pub_host, const SweepProgress* prg) {
   extern __shared__ double sm[];
   __shared__ int s_m, s_nacc, s_acc[kSweepBlock];
   __shared__ double s_root[kSweepBlock];
@@ -182,6 +202,7 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     // LLT success condition (Eigen fails on the first pivot <= 0)
     rdraw[i] = accept_all ? 0.0 : u01(splitmix64_draw(seed, draw0 + (uint64_t)i));
     udiag[i] = H[(int64_t)i * b + i];
+    if (prg) prg->aidx[i] = -1;
   }
   if (tid == 0) s_m = 0;
   __syncthreads();
@@ -296,11 +317,24 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
           hp[base + q] = h;
         }
       }
-      if (tid < nacc) s_pos[m0 + tid] = s_acc[tid];
+      if (tid < nacc) {
+        s_pos[m0 + tid] = s_acc[tid];
+        if (prg) {
+          pos[m0 + tid] = s_acc[tid];
+          prg->aidx[s_acc[tid]] = m0 + tid;
+        }
+      }
       if (tid == 0) s_m = m0 + nacc;
     }
     __syncthreads();
     SWEEP_CLK(i0 / kSweepBlock, 3)
+    // (warp 1 publishes: warp 0 goes straight on to the next block's decisions; the barrier
+    // above ordered every thread's lcol / pos / aidx writes before this fence)
+    if (prg && tid == 32 && (nacc > 0 || i1 == b)) {
+      __threadfence();
+      st_release_u64(prg->prog, ((unsigned long long)prg->epoch << 32) | (unsigned)s_m |
+                                    (i1 == b ? 0x80000000u : 0u));
+    }
   }
   const int m = s_m;
   for (int a = tid; a < m; a += kSweepThreads) {
@@ -320,16 +354,31 @@ __global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
     int64_t* haid = reinterpret_cast<int64_t*>(hpid + b);
     if (tid == 0) {
       *hs = *pub_scan;
-      SweepOut o;
-      o.m = m;
-      o.pad = 0;
-      *hw = o;
+      hw->m = m;
     }
     for (int j = tid; j < b; j += kSweepThreads) {
       hpid[j] = prop[(int64_t)j * lay.rec];
       haid[j] = j < m ? (int64_t)prop[(int64_t)s_pos[j] * lay.rec] : 0;
     }
+    if (prg) {
+      // sequence word last: the host spins on it instead of waiting for the launch to end
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        *reinterpret_cast<volatile int32_t*>(&hw->pad) = (int32_t)prg->epoch;
+      }
+    }
   }
+}
+
+__global__ void __launch_bounds__(kSweepThreads) sweep_kernel(
+    const double* __restrict__ H, int b, uint64_t seed, uint64_t draw0,
+    const double* __restrict__ prop, RecordLayout lay, int* __restrict__ pos,
+    int64_t* __restrict__ acc_ids, double* __restrict__ lcol, double* __restrict__ lacc_cm,
+    SweepOut* out, double* hp_global, int accept_all, const ScanStatus* pub_scan,
+    char* pub_host) {
+  sweep_body(H, b, seed, draw0, prop, lay, pos, acc_ids, lcol, lacc_cm, out, hp_global,
+             accept_all, pub_scan, pub_host, nullptr);
 }
 
 void launch_sweep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
@@ -604,6 +653,226 @@ void launch_round_prep(const double* lacc_cm, int m_host, const int* m_dev, int 
   else if (m_max <= 128) RPCB_PREP(4);
   else RPCB_PREP(8);
 #undef RPCB_PREP
+}
+
+// ---- fused sweep + round prep --------------------------------------------------------
+// CTA 0 runs the sweep (sweep_body, publishing its progress after every 16-step block);
+// every other warp of the grid runs one item of the round prep behind it:
+//   items [0, kcur)             B'(:, k) = -L^{-1} F_S(:, k)   (forward substitution),
+//   items [kcur, kcur + nc16)   L^{-1}(:, c), c = item - kcur   (c < round16(b)),
+// then the accepted operand rows once the final count is out.  The substitution runs over
+// proposal rows j (lane j & 31, slot j >> 5) instead of acceptance indices: accepted column c
+// (position p_c) updates x_j for j > p_c with exactly the operations of warp_lower_solve
+// (x_t = x_(p_c) * (1 / L_cc), x_j = fma(-L(j, c), x_t, x_j)), so B' and L^{-1} are the
+// round_prep_kernel's bit for bit; rejected rows carry values nobody reads.  Columns arrive
+// 16 at a time, so a warp's chain trails the sweep by one block and the prep work leaves
+// the round's critical path (it ran after the sweep: ~25 us per C4 round).
+struct PrepArgs {
+  const double* lcol;
+  int b;
+  const double* prop;
+  RecordLayout lay;
+  int kcur;
+  double* bp;
+  int64_t ldbp;
+  double* linv_rm;
+  int64_t ldl;
+  int nb;
+  int dpad;
+  double* xs;
+  double* sqnS;
+  double* idS;
+  double xscale;
+  int n_rows;
+  const int* pos;
+  const int* aidx;
+  const unsigned long long* prog;
+  unsigned epoch;
+};
+
+// lane 0 polls the progress word until at least `need` columns are out or the sweep is done;
+// returns the count, `done` set with the final one
+__device__ __forceinline__ int prep_wait(const PrepArgs& a, int need, bool& done) {
+  unsigned long long v = 0;
+  if ((threadIdx.x & 31) == 0) {
+    for (;;) {
+      v = ld_acquire_u64(a.prog);
+      if ((unsigned)(v >> 32) == a.epoch &&
+          ((int)(v & 0x7fffffffu) >= need || (v & 0x80000000ull)))
+        break;
+      __nanosleep(64);
+    }
+  }
+  __syncwarp();
+  v = __shfl_sync(0xffffffffu, v, 0);
+  done = (v & 0x80000000ull) != 0;
+  return (int)(v & 0x7fffffffu);
+}
+
+template <int NQ>
+__device__ __forceinline__ void prep_solve(const PrepArgs& a, int item) {
+  const int lane = threadIdx.x & 31;
+  const bool inv = item >= a.kcur;
+  const int c = inv ? item - a.kcur : 0, k = inv ? 0 : item;
+  bool done = false;
+  int avail = prep_wait(a, inv ? c + 1 : 1, done);
+  double x[NQ];
+  int t = 0;
+  if (inv) {
+    if (avail <= c) {  // c >= m: zero column inside the last 16-column chunk the update reads
+      if (c < ((avail + 15) & ~15))
+        for (int r = lane; r < a.nb; r += 32) a.linv_rm[(int64_t)perm_row(r) * a.ldl + kslot16(c)] = 0.0;
+      return;
+    }
+    const int pc = __ldcg(a.pos + c);
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) x[q] = (lane + 32 * q == pc) ? 1.0 : 0.0;
+    t = c;
+  } else {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = lane + 32 * q;
+      x[q] = j < a.b ? -__ldg(a.prop + (int64_t)j * a.lay.rec + a.lay.foff + k) : 0.0;
+    }
+  }
+  constexpr int kB = 8;  // columns whose loads are issued together
+  for (;;) {
+    if (t >= avail) {
+      if (done) break;
+      avail = prep_wait(a, t + 1, done);
+      if (t >= avail) break;
+    }
+    while (t < avail) {
+      const int nbt = min(kB, avail - t);
+      int pp[kB];
+      double dd[kB], lc[kB][NQ];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) pp[u] = u < nbt ? __ldcg(a.pos + t + u) : 0;
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const double* col = a.lcol + (int64_t)(t + u) * a.b;
+        dd[u] = u < nbt ? __ldcg(col + pp[u]) : 1.0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int j = lane + 32 * q;
+          lc[u][q] = (u < nbt && j < a.b) ? __ldcg(col + j) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        if (u >= nbt) break;
+        const double rd = 1.0 / dd[u];
+        const int p = pp[u], ql = p >> 5;
+        double own = x[0];
+#pragma unroll
+        for (int q = 1; q < NQ; ++q) own = (q == ql) ? x[q] : own;
+        const double xt = __shfl_sync(0xffffffffu, own * rd, p & 31);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+          const int j = lane + 32 * q;
+          const double nx = fma(-lc[u][q], xt, x[q]);
+          x[q] = (j == p) ? xt : ((j > p) ? nx : x[q]);
+        }
+      }
+      t += nbt;
+    }
+  }
+  const int m = avail;
+  if (inv) {
+    const int col = kslot16(c);
+    for (int r = lane; r < a.nb; r += 32)
+      if (r < c || r >= m) a.linv_rm[(int64_t)perm_row(r) * a.ldl + col] = 0.0;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = lane + 32 * q;
+      const int r = j < a.b ? __ldcg(a.aidx + j) : -1;
+      if (r >= c) a.linv_rm[(int64_t)perm_row(r) * a.ldl + col] = x[q];
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      const int j = lane + 32 * q;
+      const int r = j < a.b ? __ldcg(a.aidx + j) : -1;
+      if (r >= 0) a.bp[(int64_t)perm_row(r) * a.ldbp + k] = x[q];
+    }
+    for (int r = m + lane; r < a.n_rows; r += 32) a.bp[(int64_t)perm_row(r) * a.ldbp + k] = 0.0;
+  }
+}
+
+__device__ __forceinline__ void prep_operand(const PrepArgs& a, int n) {
+  const int lane = threadIdx.x & 31;
+  bool done = false;
+  const int m = prep_wait(a, 1 << 30, done);  // the final count
+  const int dst = perm_row(n);
+  double* xr = a.xs + (int64_t)dst * a.dpad;
+  if (n < m) {
+    const double* rec = a.prop + (int64_t)__ldcg(a.pos + n) * a.lay.rec;
+    for (int i = lane; i < a.dpad; i += 32) xr[i] = a.xscale * rec[a.lay.xoff + i];
+    if (lane == 0) {
+      a.sqnS[n] = rec[1];
+      a.idS[n] = rec[0];
+    }
+  } else {
+    for (int i = lane; i < a.dpad; i += 32) xr[i] = 0.0;
+    if (lane == 0) {
+      a.sqnS[n] = 0.0;
+      a.idS[n] = -1.0;
+    }
+  }
+}
+
+template <int NQ>
+__global__ void __launch_bounds__(kSweepThreads) sweep_prep_kernel(
+    const double* __restrict__ H, int b, uint64_t seed, uint64_t draw0,
+    const double* __restrict__ prop, RecordLayout lay, int* __restrict__ pos,
+    int64_t* __restrict__ acc_ids, double* __restrict__ lcol, double* __restrict__ lacc_cm,
+    SweepOut* out, const ScanStatus* pub_scan, char* pub_host, SweepProgress prg, PrepArgs pa) {
+  if (blockIdx.x == 0) {
+    sweep_body(H, b, seed, draw0, prop, lay, pos, acc_ids, lcol, lacc_cm, out, nullptr, 0,
+               pub_scan, pub_host, &prg);
+    return;
+  }
+  const int nw = (gridDim.x - 1) * (kSweepThreads / 32);
+  const int gw = (blockIdx.x - 1) * (kSweepThreads / 32) + (threadIdx.x >> 5);
+  const int nitems = pa.kcur + ((b + 15) & ~15);
+  for (int it = gw; it < nitems; it += nw) prep_solve<NQ>(pa, it);
+  for (int n = nw - 1 - gw; n < pa.n_rows; n += nw) prep_operand(pa, n);
+}
+
+int launch_sweep_prep(const double* H, int b, uint64_t seed, uint64_t draw0, const double* prop,
+                      RecordLayout lay, int* pos, int64_t* acc_ids, double* lcol,
+                      double* lacc_cm, SweepOut* out, const ScanStatus* pub_scan,
+                      char* pub_host, unsigned long long* prog, int* aidx, unsigned epoch,
+                      int nb, int64_t ldl, double* linv_rm, int kcur, double* bp, int64_t ldbp,
+                      int dpad, double* xs, double* sqnS, double* idS, double xscale,
+                      int n_rows, cudaStream_t st) {
+  if (b < 1 || b > 128) return -1;
+  const size_t packed = (size_t)b * (b + 1) / 2;
+  const size_t smem = sizeof(double) * (2 * (size_t)b + kSweepBlock * kSweepBlock +
+                                        kSweepBlock * (size_t)b + packed);
+  SweepProgress prg{prog, aidx, epoch};
+  PrepArgs pa{lcol, b,      prop, lay,  kcur, bp,     ldbp, linv_rm, ldl,  nb,
+              dpad, xs,     sqnS, idS,  xscale, n_rows, pos,  aidx,    prog, epoch};
+  auto go = [&](auto kfn) -> int {
+    if (ensure_smem_attr((const void*)kfn, (int)smem) != cudaSuccess) return -2;
+    const int occ = cached_occupancy((const void*)kfn, kSweepThreads, smem, 1);
+    const int items = kcur + ((b + 15) & ~15);
+    const int want = 1 + std::max(1, (std::max(items, n_rows) + kSweepThreads / 32 - 1) /
+                                         (kSweepThreads / 32));
+    const int grid = std::min(want, occ * num_sms());
+    if (grid < 2) return -3;
+    void* args[] = {(void*)&H,   (void*)&b,       (void*)&seed,  (void*)&draw0,   (void*)&prop,
+                    (void*)&lay, (void*)&pos,     (void*)&acc_ids, (void*)&lcol, (void*)&lacc_cm,
+                    (void*)&out, (void*)&pub_scan, (void*)&pub_host, (void*)&prg,  (void*)&pa};
+    // cooperative: every CTA co-resident, so the prep warps can wait on the sweep CTA
+    return cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(kSweepThreads), args,
+                                       smem, st) == cudaSuccess
+               ? grid
+               : -4;
+  };
+  if (b <= 32) return go(sweep_prep_kernel<1>);
+  if (b <= 64) return go(sweep_prep_kernel<2>);
+  return go(sweep_prep_kernel<4>);
 }
 
 template <int NQ>

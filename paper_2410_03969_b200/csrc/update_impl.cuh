@@ -1,4 +1,7 @@
 #pragma once
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 // update_impl.cuh — K5+K6: the fused round update, one CTA per BM-row tile of the shard.
 //
 // For the accepted pivots S (m columns) of a round it computes, without ever
@@ -600,6 +603,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
     }  // !REGP2
     // ---- epilogue ------------------------------------------------------------------
     double rs[2] = {0.0, 0.0};
+    double unew[2] = {0.0, 0.0};  // new u of this lane's rows (t == 0 lanes; 0 past n_loc)
 #pragma unroll
     for (int fr = 0; fr < 2; ++fr) {
       const int64_t grow = tile_row0 + arow[fr];
@@ -623,7 +627,8 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
           double s2 = rs[fr];
           if (rin) {
             const double un = __dsub_rn(p.u[grow], s2);
-            p.u[grow] = un < 0.0 ? 0.0 : un;
+            unew[fr] = un < 0.0 ? 0.0 : un;
+            p.u[grow] = unew[fr];
           } else {
             s2 = 0.0;
           }
@@ -632,6 +637,19 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       } else if (t == 0) {
         s_rown[wc * BM + arow[fr]] = rs[fr];
       }
+    }
+    if (WC == 1 && !COLS && p.tsum) {
+      // sequential sum of the warp's 16 rows in row order (row 8 fr + r sits in quad g with
+      // perm8(g) == r): the per-thread sum of chunk_scan_core, zero past n_loc
+      double ssum = 0.0;
+#pragma unroll
+      for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int gq = (r & 1) ? 4 + (r >> 1) : (r >> 1);  // perm8(gq) == r
+          ssum = __dadd_rn(ssum, __shfl_sync(0xffffffffu, unew[fr], 4 * gq));
+        }
+      if (lane == 0) p.tsum[(tile_row0 >> 4) + wr] = ssum;
     }
     if (WC > 1) {
       gsync();
@@ -663,6 +681,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       for (int r = lane; r < BM; r += 32) s2 = __dadd_rn(s2, s_rowg2[r]);
       s2 = warp_sum_xor(s2);
       if (lane == 0) p.tile_g2[tile] = p.g2_accum ? __dadd_rn(p.tile_g2[tile], s2) : s2;
+
     } else {
       named_bar_arrive(1 + G + grp, GT);
     }
@@ -707,7 +726,10 @@ template <int WC, int NFW, bool GRAM, int MINB, int G, bool COLS = false>
 int launch_t(const UpdateParams& p, cudaStream_t st) {
   using C = UCfg<WC, NFW, G>;
   const void* kfn = (const void*)update_kernel<WC, NFW, GRAM, MINB, G, COLS>;
+  static const bool dbg_launch = std::getenv("RPC_DEBUG_LAUNCH") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
   if (ensure_smem_attr(kfn, C::SMEM) != cudaSuccess) return -2;
+  const auto t1 = std::chrono::steady_clock::now();
   CUtensorMap mX, mXS, mF, mFS, mG, mL;
   bool ok = make_map(&mX, p.X, p.dpad, p.n_loc, p.dpad, C::BM) &&
             make_map(&mXS, p.xs, p.dpad, C::NB, p.dpad, C::NB) &&
@@ -716,14 +738,22 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
             make_map(&mG, p.F, p.kcur + p.m, p.n_loc, p.ldf, C::BM) &&
             make_map(&mL, p.linv, p.ldl, C::NB, p.ldl, C::NB);
   if (!ok) return -3;
+  const auto t2 = std::chrono::steady_clock::now();
   // persistent: one CTA per SM, tiles strided by the grid (p.tile_g2 is per tile)
   const int64_t ntiles = (p.n_loc + C::BM - 1) / C::BM;
   // persistent grid sized by occupancy: small m (early rounds, kernel-column bench) fits two
   // CTAs per SM, which hides the latency of the short per-tile chains
   const int occ = cached_occupancy(kfn, C::NT, C::SMEM, MINB);
   const unsigned grid = (unsigned)std::min<int64_t>((ntiles + G - 1) / G, (int64_t)occ * num_sms());
+  const auto t3 = std::chrono::steady_clock::now();
   if (grid)
     update_kernel<WC, NFW, GRAM, MINB, G, COLS><<<grid, C::NT, C::SMEM, st>>>(p, mX, mXS, mF, mFS, mG, mL);
+  if (dbg_launch) {
+    const auto t4 = std::chrono::steady_clock::now();
+    auto us = [](auto a, auto b) { return std::chrono::duration<double, std::micro>(b - a).count(); };
+    std::fprintf(stderr, "[launch] attr %.2f maps %.2f occ %.2f launch %.2f us\n", us(t0, t1),
+                 us(t1, t2), us(t2, t3), us(t3, t4));
+  }
   return C::BM;
 }
 

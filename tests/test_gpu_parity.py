@@ -420,3 +420,71 @@ def test_large_dimension(ctx, d, kernel, dist):
     sigma = math.sqrt(d) * (0.5 if kernel == "gaussian" else 10.0)
     g, r, o = run_both(x, kernel, sigma, k=60, b=20, ctx=ctx, dist=dist)
     assert_parity(g, r, o)
+
+
+# ------------------------------------------- fused sweep + round prep (one launch)
+@pytest.mark.parametrize("n,d,b,k", [(20000, 10, 40, 200), (30000, 30, 120, 600), (8000, 3, 24, 96),
+                                     (12000, 20, 128, 500), (6000, 5, 1, 20), (9000, 8, 17, 70)])
+def test_fused_sweep_prep_bitwise_equals_two_launches(ctx, monkeypatch, n, d, b, k):
+    """The fused launch (CTA 0 sweeps, the other warps form L^-1, B' and the operands behind
+    its per-block progress word) must reproduce the two-launch path bit for bit: same
+    pivots, and F, u, chol identical to the last bit (same operations per entry)."""
+    x = wl.gen_c1(n, d, 3)
+    spec = api.KernelSpec("gaussian", math.sqrt(d))
+    cfg = api.RunConfig.until_rank(k, b, 11)
+    monkeypatch.delenv("RPC_NO_FUSED_PREP", raising=False)
+    a = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    monkeypatch.setenv("RPC_NO_FUSED_PREP", "1")
+    r = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    assert np.array_equal(a.pivots, r.pivots)
+    assert np.array_equal(a.factor, r.factor)
+    assert np.array_equal(a.residual_diag, r.residual_diag)
+    assert np.array_equal(a.chol_factor, r.chol_factor)
+    assert a.relative_trace_error == r.relative_trace_error
+
+
+def test_sample_from_thread_bases_equals_rescan(ctx, monkeypatch):
+    """The sampler that reads the stored thread bases must pick exactly the rows the
+    rescanning sampler picks (same fast cumsum), including zero plateaus, runs of zeros
+    spanning whole 16-row runs and chunks, partial last chunks and the clamp case."""
+    rng = np.random.default_rng(5)
+    cases = []
+    for n in (1, 17, 4096, 4097, 12289, 100000, 262144 + 7):
+        u = rng.random(n) ** 4
+        u[rng.random(n) < 0.3] = 0.0
+        cases.append(u)
+    u = rng.random(50000)
+    u[:20000] = 0.0
+    u[30000:] = 0.0          # trailing zero chunks: plateau walk back over whole chunks
+    cases.append(u)
+    u = np.zeros(9000)
+    u[4095] = 1e-300         # a single tiny weight
+    u[8191] = 2.0
+    cases.append(u)
+    for u in cases:
+        if not np.any(u > 0):
+            continue
+        monkeypatch.delenv("RPC_NO_TB_SAMPLER", raising=False)
+        a = api.sample_discrete(u, 300, 17, 5, replay=False, ctx=ctx)
+        monkeypatch.setenv("RPC_NO_TB_SAMPLER", "1")
+        b = api.sample_discrete(u, 300, 17, 5, replay=False, ctx=ctx)
+        assert np.array_equal(a, b)
+        assert np.all(u[a] > 0.0)
+
+
+@pytest.mark.parametrize("n,d,b,k", [(20000, 10, 40, 200), (70000, 30, 120, 600),
+                                     (4097, 3, 24, 96), (200000, 20, 128, 500)])
+def test_update_fused_scan_bitwise_equals_totals_pass(ctx, monkeypatch, n, d, b, k):
+    """Scan chained inside the update's epilogue (thread bases, chunk totals, chunk offsets,
+    status) against the separate totals pass: identical pivots and factor bit for bit."""
+    x = wl.gen_c1(n, d, 4)
+    spec = api.KernelSpec("gaussian", math.sqrt(d))
+    cfg = api.RunConfig.until_rank(k, b, 13)
+    monkeypatch.delenv("RPC_NO_FUSED_SCAN", raising=False)
+    a = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    monkeypatch.setenv("RPC_NO_FUSED_SCAN", "1")
+    r = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    assert np.array_equal(a.pivots, r.pivots)
+    assert np.array_equal(a.factor, r.factor)
+    assert np.array_equal(a.residual_diag, r.residual_diag)
+    assert a.relative_trace_error == r.relative_trace_error
