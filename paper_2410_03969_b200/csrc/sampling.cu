@@ -644,35 +644,43 @@ __global__ void __launch_bounds__(256) pack_points_kernel(const double* __restri
                                                           int rows, double* __restrict__ X,
                                                           double* __restrict__ sqn,
                                                           int* nonfinite) {
-  extern __shared__ double tile[];  // [rows][dpad]
+  extern __shared__ double tile[];  // [rows][dpad + 1] (odd stride: per-row reads of one
+                                    // column by 32 lanes hit distinct banks)
   const int64_t r0 = (int64_t)blockIdx.x * rows;
   const int nr = (int)lmin(rows, n_loc - r0);
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int dp = (int)dpad, ts = dp + 1;
   bool bad = false;
-  const int64_t tot = (int64_t)nr * dpad;
+  // (no 64-bit index divisions: a warp per row for row-major sources, whose rows are
+  // contiguous, a warp per column for column-major ones)
   if (src_row_major) {
-    for (int64_t i = tid; i < tot; i += blockDim.x) {
-      const int64_t r = i / dpad, c = i % dpad;
-      double v = 0.0;
-      if (c < d) v = src[(r0 + r) * ld_src + c];
-      bad |= !isfinite(v);
-      tile[i] = v;
+    for (int r = warp; r < nr; r += nw) {
+      const double* sr = src + (r0 + r) * ld_src;
+      for (int c = lane; c < dp; c += 32) {
+        const double v = c < d ? __ldg(sr + c) : 0.0;
+        bad |= !isfinite(v);
+        tile[r * ts + c] = v;
+      }
     }
   } else {
-    for (int64_t i = tid; i < tot; i += blockDim.x) {
-      const int64_t c = i / nr, r = i % nr;
-      double v = 0.0;
-      if (c < d) v = src[c * ld_src + r0 + r];
-      bad |= !isfinite(v);
-      tile[r * dpad + c] = v;
+    for (int c = warp; c < dp; c += nw) {
+      const double* sc = src + (int64_t)c * ld_src + r0;
+      for (int r = lane; r < nr; r += 32) {
+        const double v = c < d ? __ldg(sc + r) : 0.0;
+        bad |= !isfinite(v);
+        tile[r * ts + c] = v;
+      }
     }
   }
   __syncthreads();
-  for (int64_t i = tid; i < tot; i += blockDim.x) X[r0 * dpad + i] = tile[i];
+  for (int r = warp; r < nr; r += nw) {
+    double* xr = X + (r0 + r) * dpad;
+    for (int c = lane; c < dp; c += 32) xr[c] = tile[r * ts + c];
+  }
   if (tid < nr) {
     double s = 0.0;
     for (int c = 0; c < d; ++c) {
-      const double v = tile[tid * dpad + c];
+      const double v = tile[tid * ts + c];
       s = __dadd_rn(s, __dmul_rn(v, v));
     }
     sqn[r0 + tid] = s;
@@ -708,13 +716,13 @@ void launch_pack_points(const double* src, int64_t n_loc, int d, int64_t ld_src,
                         int src_row_major, int64_t dpad, double* X, double* sqn,
                         int* nonfinite, cudaStream_t st) {
   if (n_loc <= 0) return;
-  const int rows = (int)lmin(kPackRows, kPackSmem / (int64_t)(sizeof(double) * dpad));
+  const int rows = (int)lmin(kPackRows, kPackSmem / (int64_t)(sizeof(double) * (dpad + 1)));
   if (rows < 1) {
     pack_row_kernel<<<(unsigned)n_loc, 256, 0, st>>>(src, d, ld_src, src_row_major, dpad, X, sqn,
                                                      nonfinite);
     return;
   }
-  const size_t smem = sizeof(double) * rows * (size_t)dpad;
+  const size_t smem = sizeof(double) * rows * (size_t)(dpad + 1);
   ensure_smem_attr((const void*)pack_points_kernel, kPackSmem);
   pack_points_kernel<<<(unsigned)((n_loc + rows - 1) / rows), 256, smem, st>>>(
       src, n_loc, d, ld_src, src_row_major, dpad, rows, X, sqn, nonfinite);
