@@ -10,6 +10,10 @@ reduce, ||G||^2 allgather) is not measurable on one GPU; it is charged at a stat
 per collective (--coll-us, default 15 us: small NCCL collectives over NVLink/NVSwitch).
 
   python tools/scaling_projection.py [--coll-us 15] > profiles/r02_scaling_projection.json
+
+The conservative columns take the chain from the P-shard run itself (fact - update there):
+the sharded scan path (per-shard totals, allgather, prefix) with every shard's small launches
+serialised on the one GPU, so it over-states what P GPUs would pay.
 """
 import argparse
 import json
@@ -58,11 +62,17 @@ def main():
         per_gpu_update = upd / P
         colls = 0 if P == 1 else 3 * rounds  # chunk totals (+ g2) allgathers, record reduce
         proj = per_gpu_update + base["chain_ms"] + colls * args.coll_us * 1e-3
+        # conservative: the chain as the P-shard run measures it (the sharded scan path, every
+        # shard's small launches serialised on the one GPU, device-local exchange)
+        chain_p = fact - upd
+        proj_c = per_gpu_update + chain_p + colls * args.coll_us * 1e-3
         out["rows"].append({
             "P": P, "virtual_run_factorize_ms": fact, "update_ms_all_shards": upd,
             "per_gpu_update_ms": per_gpu_update, "replicated_chain_ms": base["chain_ms"],
             "collectives": colls, "projected_ms": proj,
             "projected_speedup": base["factorize_ms"] / proj,
+            "chain_ms_sharded_run": chain_p, "projected_ms_conservative": proj_c,
+            "projected_speedup_conservative": base["factorize_ms"] / proj_c,
             "pivots_equal_to_P1": bool(np.array_equal(piv, base["pivots"]))})
     out["rounds"] = rounds
     print(json.dumps(out, indent=1))
