@@ -229,13 +229,14 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   CK(cudaMemsetAsync(prefix_counter.p, 0, sizeof(unsigned), st));
   // fast-scan thread bases (sampler) and the update-fused scan's chunk bookkeeping
   DBuf tb_all(ctx, sizeof(double) * (size_t)L.ncg * kScanThreads);
-  const bool fuse_scan_ok = P == 1 && ctx->world == 1 && !lowmem && !replay && L.ncg <= 4096 &&
+  const bool fuse_scan_ok = !lowmem && !replay && L.ncg <= 4096 &&
                             std::getenv("RPC_NO_FUSED_SCAN") == nullptr;
-  DBuf scan_tsum;
-  if (fuse_scan_ok) {
-    const int64_t ntiles64 = (res->shards[0].n_loc + 63) / 64;
-    scan_tsum = DBuf(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, 4 * ntiles64));
-  }
+  std::vector<DBuf> scan_tsum(res->shards.size());  // per shard: 16-row run sums of u
+  if (fuse_scan_ok)
+    for (size_t si = 0; si < res->shards.size(); ++si) {
+      const int64_t ntiles64 = (res->shards[si].n_loc + 63) / 64;
+      scan_tsum[si] = DBuf(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, 4 * ntiles64));
+    }
   // true while the last update's 16-row run sums (tsum) describe the current u: the next
   // scan then chains them (launch_chunk_chain, 1/16 of u's bytes) instead of a totals pass
   // over u, and the sampler chains the chunk offsets
@@ -369,11 +370,17 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     }
     // (skipped when the previous update already chained its scan: chunk ends, thread bases
     // and the round status are current)
+    // one shard: the sampler chains the chunk offsets from the chained totals itself
+    const bool sampler_prefix = scan_fresh && P == 1 && ctx->world == 1;
     if (scan_fresh) {
-      Shard& s = res->shards[0];
-      launch_chunk_chain(scan_tsum.as<double>(), s.tile_g2.as<double>(), s.n_loc, s.nchunks,
-                         tb_all.as<double>(), totals_all.as<double>(), g2_all.as<double>(), st);
-      ++launches;
+      for (size_t si = 0; si < res->shards.size(); ++si) {
+        Shard& s = res->shards[si];
+        launch_chunk_chain(scan_tsum[si].as<double>(), s.tile_g2.as<double>(), s.n_loc,
+                           s.nchunks, tb_all.as<double>() + (size_t)s.chunk0 * kScanThreads,
+                           totals_all.as<double>() + s.chunk0, g2_all.as<double>() + s.chunk0,
+                           st);
+        ++launches;
+      }
     }
     for (Shard& s : res->shards) {
       if (scan_fresh) break;
@@ -384,7 +391,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
                           tb_all.as<double>() + (size_t)s.chunk0 * kScanThreads);
       ++launches;
     }
-    if (!fuse_prefix && !scan_fresh) {
+    if (scan_fresh ? !sampler_prefix : !fuse_prefix) {
       allgather(ctx, totals_all.as<double>(), L.cpr);
       if (pending_g2) allgather(ctx, g2_all.as<double>(), L.cpr);
       launch_chunk_prefix(totals_all.as<double>(), pending_g2 ? g2_all.as<double>() : nullptr,
@@ -434,7 +441,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       sp.records = prop.as<double>();  // the owner of draw j writes slot j
       sp.owner = owner.as<int>();
       sp.tb = tb_all.as<double>() + (size_t)s.chunk0 * kScanThreads;
-      if (scan_fresh && !replay) {  // (one shard) offsets + status from the update's chunk totals
+      if (sampler_prefix) {  // (one shard) offsets + status from the update's chunk totals
         sp.totals = totals_all.as<double>();
         sp.chunk_g2 = g2_all.as<double>();
         sp.chunk_end_out = chunk_end.as<double>();
@@ -721,7 +728,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         up.g2_accum = g0 > 0;  // later groups add their ||G||^2 to the round's tile partials
         const bool fscan = fuse_scan_ok && !grouped && algo == kAlgoAccelerated &&
                            update_regp2(mg) && update_tile_rows(mg) == 64;
-        if (fscan) up.tsum = scan_tsum.as<double>();
+        if (fscan) up.tsum = scan_tsum[&s - res->shards.data()].as<double>();
         scan_fresh = fscan;
         if (dbg_trace) {
           CK(cudaMemsetAsync(trace_buf.p, 0, trace_buf.bytes, st));

@@ -472,19 +472,24 @@ def test_sample_from_thread_bases_equals_rescan(ctx, monkeypatch):
         assert np.all(u[a] > 0.0)
 
 
-@pytest.mark.parametrize("n,d,b,k", [(20000, 10, 40, 200), (70000, 30, 120, 600),
-                                     (4097, 3, 24, 96), (200000, 20, 128, 500)])
-def test_update_fused_scan_bitwise_equals_totals_pass(ctx, monkeypatch, n, d, b, k):
-    """Scan chained inside the update's epilogue (thread bases, chunk totals, chunk offsets,
-    status) against the separate totals pass: identical pivots and factor bit for bit."""
+@pytest.mark.parametrize("n,d,b,k,shards", [(20000, 10, 40, 200, 1), (70000, 30, 120, 600, 1),
+                                            (4097, 3, 24, 96, 1), (200000, 20, 128, 500, 1),
+                                            (70000, 30, 120, 600, 3), (20000, 10, 40, 200, 2)])
+def test_update_fused_scan_bitwise_equals_totals_pass(ctx, monkeypatch, n, d, b, k, shards):
+    """Scan from the update's 16-row run sums (chunk chaining launch, thread-base sampler,
+    offsets chained by the sampler on one shard or by the prefix pass across shards) against
+    the totals pass over u: identical pivots and factor bit for bit."""
     x = wl.gen_c1(n, d, 4)
     spec = api.KernelSpec("gaussian", math.sqrt(d))
     cfg = api.RunConfig.until_rank(k, b, 13)
+    c = ctx if shards == 1 else api.Context(0, virtual_shards=shards)
     monkeypatch.delenv("RPC_NO_FUSED_SCAN", raising=False)
-    a = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    a = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, c)
     monkeypatch.setenv("RPC_NO_FUSED_SCAN", "1")
-    r = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    r = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, c)
     assert np.array_equal(a.pivots, r.pivots)
     assert np.array_equal(a.factor, r.factor)
     assert np.array_equal(a.residual_diag, r.residual_diag)
     assert a.relative_trace_error == r.relative_trace_error
+    if shards > 1:
+        c.close()
