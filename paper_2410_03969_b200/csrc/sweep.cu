@@ -309,12 +309,34 @@ __device__ __forceinline__ void sweep_body(
       }
       SWEEP_CLK(i0 / kSweepBlock, 2)
       // ---- 3. trailing update, acceptance order per entry ----
-      for (int p = i1 + warp; p < b; p += nwarps) {
-        const int64_t base = tri(p);
-        for (int q = i1 + lane; q <= p; q += 32) {
-          double h = hp[base + q];
-          for (int k = 0; k < nacc; ++k) h = __dsub_rn(h, __dmul_rn(lpan[k * b + p], lpan[k * b + q]));
-          hp[base + q] = h;
+      // Each lane carries four independent entries — rows p0, p0 + nwarps, columns q, q + 32 —
+      // so four dependent subtract chains are in flight instead of one (the chain of a single
+      // entry, not the FP64 throughput, bounded this phase: b = 120 probe 37.7k -> 31.6k
+      // cycles; eight entries per lane or four columns of one row measured slower); each entry
+      // still receives h - l_k(p) l_k(q) for the block's accepted steps k in order.
+      for (int p0 = i1 + warp; p0 < b; p0 += 2 * nwarps) {
+        const int p1 = p0 + nwarps;
+        const bool v1 = p1 < b;
+        const int pr1 = v1 ? p1 : p0;
+        const int64_t b0 = tri(p0), b1 = tri(pr1);
+        for (int q = i1 + lane; q <= pr1; q += 64) {
+          const int q2 = q + 32, qb = q2 < b ? q2 : q;
+          const bool e00 = q <= p0, e01 = q2 <= p0, e10 = v1 && q <= p1, e11 = v1 && q2 <= p1;
+          double h00 = e00 ? hp[b0 + q] : 0.0, h01 = e01 ? hp[b0 + q2] : 0.0;
+          double h10 = e10 ? hp[b1 + q] : 0.0, h11 = e11 ? hp[b1 + q2] : 0.0;
+#pragma unroll 4
+          for (int k = 0; k < nacc; ++k) {
+            const double* lk = lpan + k * b;
+            const double l0 = lk[p0], l1 = lk[pr1], la = lk[q], lb = lk[qb];
+            h00 = __dsub_rn(h00, __dmul_rn(l0, la));
+            h01 = __dsub_rn(h01, __dmul_rn(l0, lb));
+            h10 = __dsub_rn(h10, __dmul_rn(l1, la));
+            h11 = __dsub_rn(h11, __dmul_rn(l1, lb));
+          }
+          if (e00) hp[b0 + q] = h00;
+          if (e01) hp[b0 + q2] = h01;
+          if (e10) hp[b1 + q] = h10;
+          if (e11) hp[b1 + q2] = h11;
         }
       }
       if (tid < nacc) {
