@@ -237,6 +237,29 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       const int64_t ntiles64 = (res->shards[si].n_loc + 63) / 64;
       scan_tsum[si] = DBuf(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, 4 * ntiles64));
     }
+  // Residual GEMM on the tensor cores (i8gemm.cu): F's int8 digit planes are kept beside F
+  // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 480) and
+  // m <= 128 compute F B'^T there; the update kernel then adds it.  Opt-in (RPC_I8=1) until
+  // it beats the FP64 DMMA path end to end (RPC_NO_I8 forces it off).
+  const bool i8_ok = !lowmem && algo == kAlgoAccelerated && !grouped &&
+                     std::getenv("RPC_I8") != nullptr && std::getenv("RPC_NO_I8") == nullptr;
+  const int64_t i8_min_k = std::getenv("RPC_I8_MIN_K") ? std::atoll(std::getenv("RPC_I8_MIN_K")) : 480;
+  const int64_t i8_kcap = round_up(std::max<int64_t>(cap, 1), 64);
+  std::vector<DBuf> i8_planes(res->shards.size());
+  std::vector<int64_t> i8_rows(res->shards.size(), 0);
+  DBuf i8_bplanes, i8_cscale, i8_c;
+  if (i8_ok) {
+    int64_t maxrows = 0;
+    for (size_t si = 0; si < res->shards.size(); ++si) {
+      i8_rows[si] = round_up(std::max<int64_t>(res->shards[si].n_loc, 1), 128);
+      maxrows = std::max(maxrows, i8_rows[si]);
+      i8_planes[si] = DBuf(ctx, (size_t)kI8Slices * i8_rows[si] * i8_kcap);
+    }
+    i8_bplanes = DBuf(ctx, (size_t)kI8Slices * kI8MaxCols * i8_kcap);
+    i8_cscale = DBuf(ctx, sizeof(double) * kI8MaxCols);
+    i8_c = DBuf(ctx, sizeof(double) * (size_t)maxrows * kI8MaxCols);
+  }
+  int64_t i8_launches = 0;
   // true while the last update's 16-row run sums (tsum) describe the current u: the next
   // scan then chains them (launch_chunk_chain, 1/16 of u's bytes) instead of a totals pass
   // over u, and the sampler chains the chunk offsets
@@ -729,6 +752,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         const bool fscan = fuse_scan_ok && !grouped && algo == kAlgoAccelerated &&
                            update_regp2(mg) && update_tile_rows(mg) == 64;
         if (fscan) up.tsum = scan_tsum[&s - res->shards.data()].as<double>();
+
         scan_fresh = fscan;
         if (dbg_trace) {
           CK(cudaMemsetAsync(trace_buf.p, 0, trace_buf.bytes, st));
@@ -741,6 +765,19 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         upd_ev.emplace_back();
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
+        // (the tensor-core residual GEMM is timed as part of the round's update)
+        if (i8_ok && kg >= i8_min_k && mg <= kI8MaxCols) {
+          const size_t si = &s - res->shards.data();
+          if (launch_i8_residual(reinterpret_cast<const int8_t*>(i8_planes[si].p), i8_rows[si],
+                                 i8_kcap, s.n_loc, fs.as<double>(), ldf, mg, (int)kg,
+                                 reinterpret_cast<int8_t*>(i8_bplanes.p), i8_cscale.as<double>(),
+                                 i8_c.as<double>(), kI8MaxCols, st) == 0) {
+            up.cext = i8_c.as<double>();
+            up.ldce = kI8MaxCols;
+            ++i8_launches;
+            launches += 2;
+          }
+        }
         if (dbg_chain) host_pre_us += 1e3 * ms_since(h_wake);
         cmark("host gap");
         const auto h_l0 = clk::now();
@@ -779,6 +816,15 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         bytes += 8.0 * (N * kg + N * mg + N * d + 2.0 * N);
       }
       }  // groups
+      // this round's columns into F's digit planes (coalesced: a warp per row segment; byte
+      // stores from the update epilogue's fragment layout measured 3-4x slower per round)
+      if (i8_ok)
+        for (size_t si = 0; si < res->shards.size(); ++si) {
+          Shard& s = res->shards[si];
+          launch_slice_cols(s.F.as<double>(), ldf, s.n_loc, (int)kcur, m,
+                            reinterpret_cast<int8_t*>(i8_planes[si].p), i8_rows[si], i8_kcap, st);
+          ++launches;
+        }
       pending_g2 = true;
       if (sink.p) {
         const auto hs0 = clk::now();

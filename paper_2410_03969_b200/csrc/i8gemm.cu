@@ -1,0 +1,333 @@
+// i8gemm.cu — the round's residual GEMM C = F(:, :kcur) B'^T on the 5th-generation tensor
+// cores through int8 slices (Ozaki scheme I), for rounds where it beats the FP64 DMMA
+// phase of the fused update (which then adds C instead of running its own GEMM).
+//
+// Representation.  |F_ij| <= 1 (unit-diagonal kernels: ||F_i||^2 = 1 - u_i <= 1), so F is
+// held as kSlices signed base-2^7 digits of F * 2^6 at a fixed scale:
+//   F_ij = sum_t f_t 2^(-6 - 7 t) + e,  |f_t| <= 64,  |e| <= 2^-49,
+// kept beside F as int8 planes [kSlices][kcap / 64][rows][64] (each round appends its new
+// columns: launch_slice_cols).  B' (m x kcur, per round) is scaled per row by 2^-e_c (max |B'_c,:| <
+// 2^e_c) and sliced the same way.  Then
+//   C_ic = 2^(e_c - 12) sum_{d < kSlices} 2^(-7 d) A_d(i, c),  A_d = sum_{t + u = d} f_t b_u^T,
+// each A_d an exact int32 sum (|f_t b_u| <= 2^12, k <= 2^15 / (d + 1) terms) accumulated by
+// tcgen05.mma.kind::i8 in tensor memory; the dropped digit products (t + u >= kSlices) and the
+// representation error bound the result at ~6e-14 of sum_j |F_ij| |B'_cj| (tools/ozaki_probe.cu:
+// 6.2e-14 measured at the C4 round-9 shape; the FP64 DMMA GEMM it replaces is ~1e-16 of that).
+//
+// Kernel: one CTA per 128 F rows x 64 output columns; kSlices accumulators x 64 TMEM columns
+// (448 of 512).  Warp 0 issues the TMA loads (kSlices + kSlices planes per 64-byte K block,
+// 64-byte swizzle, two stages), warp 1 the MMAs (one thread; tcgen05.commit frees a stage),
+// warps 2-5 the epilogue (tcgen05.ld 32x32b, FP64 Horner over the diagonals, column scale).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace rpcb {
+
+constexpr int kSlices = kI8Slices;
+constexpr int kI8BM = 128, kI8BN = 64, kI8KB = 64, kI8Nst = 2;
+constexpr int kI8Apl = kI8BM * kI8KB, kI8Bpl = kI8BN * kI8KB;
+constexpr int kI8Stage = kSlices * (kI8Apl + kI8Bpl);
+
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(smem_u32(smem_dst)),
+      "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+  uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)1 << 16;           // leading byte offset (unused: swizzled K-major)
+  d |= (uint64_t)(512 >> 4) << 32;  // stride byte offset: 8 rows x 64 B
+  d |= (uint64_t)1 << 46;           // descriptor version (sm_100)
+  d |= (uint64_t)4 << 61;           // SWIZZLE_64B
+  return d;
+}
+
+__global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                       const __grid_constant__ CUtensorMap tmB,
+                                                       int a_nblk, int b_plane_rows,
+                                                       int64_t n_rows, int m, int nkb,
+                                                       const double* __restrict__ cscale,
+                                                       double* __restrict__ C, int64_t ldc) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[kI8Nst], empty[kI8Nst], done;
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // (column halves of one row tile are adjacent in launch order, so the second CTA's A
+  // planes come from L2 instead of HBM)
+  const int64_t row0 = (int64_t)blockIdx.y * kI8BM;
+  const int col0 = blockIdx.x * kI8BN;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kI8Nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    mbar_fence_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tbase = tmem_base_s;
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kI8Nst;
+        if (kb >= kI8Nst) mbar_wait(&empty[s], ((kb / kI8Nst) - 1) & 1);
+        mbar_arrive_expect_tx(&full[s], kI8Stage);
+        unsigned char* st = sm + s * kI8Stage;
+        for (int t = 0; t < kSlices; ++t)
+          tma_load_3d(st + t * kI8Apl, &tmA, 0, (int)row0, t * a_nblk + kb, &full[s]);
+        for (int u = 0; u < kSlices; ++u)
+          tma_load_2d(st + kSlices * kI8Apl + u * kI8Bpl, &tmB, kb * kI8KB, u * b_plane_rows + col0,
+                      &full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = 64
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
+                             ((uint32_t)(kI8BN >> 3) << 17) | ((uint32_t)(kI8BM >> 4) << 24);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kI8Nst;
+        mbar_wait(&full[s], (kb / kI8Nst) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const uint32_t ba = smem_u32(sm + s * kI8Stage), bb = ba + kSlices * kI8Apl;
+#pragma unroll
+        for (int t = 0; t < kSlices; ++t)
+#pragma unroll
+          for (int u = 0; u < kSlices - t; ++u)
+#pragma unroll
+            for (int ks = 0; ks < kI8KB / 32; ++ks) {
+              const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
+              const uint64_t db = umma_desc_sw64(bb + u * kI8Bpl + ks * 32);
+              // the first product of each diagonal (t = 0) at the first K step overwrites
+              const uint32_t accum = (kb | ks | t) != 0;
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                      tbase + (uint32_t)((t + u) * kI8BN)),
+                  "l"(da), "l"(db), "r"(idesc), "r"(accum));
+            }
+        asm volatile(
+            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&empty[s])));
+      }
+      asm volatile(
+          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+              smem_u32(&done)));
+    }
+  } else {
+    mbar_wait(&done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const int q = warp & 3;  // the TMEM lane quadrant this warp may read
+    const int64_t r = row0 + q * 32 + lane;
+#pragma unroll 1
+    for (int cc = 0; cc < kI8BN / 16; ++cc) {
+      double acc[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll
+      for (int d = kSlices - 1; d >= 0; --d) {
+        uint32_t v[16];
+        const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * kI8BN + cc * 16);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+            "%10, %11, %12, %13, %14, %15}, [%16];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+            : "r"(ta));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[j] = fma(acc[j], 0.0078125, (double)(int)v[j]);
+      }
+      if (r < n_rows) {
+        double* cr = C + r * ldc + col0 + cc * 16;
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          const int c = col0 + cc * 16 + j;
+          if (c + 1 < m)
+            *reinterpret_cast<double2*>(cr + j) =
+                make_double2(acc[j] * cscale[c], acc[j + 1] * cscale[c + 1]);
+          else if (c < m)
+            cr[j] = acc[j] * cscale[c];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
+// kSlices digits of v * 2^6 (|v| <= 1) in base 2^7, each rounded to nearest (magic-number rint)
+__device__ __forceinline__ void slice_value(double v, int8_t* out, int64_t pstride) {
+  constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52
+  double r = v * 64.0;
+#pragma unroll
+  for (int t = 0; t < kSlices; ++t) {
+    const double rr = r + kM;
+    out[t * pstride] = (int8_t)__double2loint(rr);
+    r = (r - (rr - kM)) * 128.0;
+  }
+}
+
+// F's digit planes are column-block-major, [kI8Slices][kcap / 64][plane_rows][64] bytes: the
+// GEMM's A tile (128 rows x 64 K bytes) is one contiguous 8 KB box, and a round's new columns
+// land in whole 64-byte row segments.  Columns [c0, c0 + nc): a half-warp per (row, block), a
+// lane per 4-column group, one 32-bit store per plane; the group holding c0 keeps its bytes
+// below c0 (earlier rounds' digits).
+__global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ F, int64_t ldf,
+                                                         int64_t n, int c0, int nc,
+                                                         int8_t* __restrict__ planes,
+                                                         int64_t pstride, int64_t bstride) {
+  const int b0 = c0 >> 6, nb = ((c0 + nc + 63) >> 6) - b0;
+  const int64_t item = blockIdx.x * 16 + (threadIdx.x >> 4);  // (row, block) pair
+  if (item >= n * nb) return;
+  const int64_t r = item / nb;
+  const int blk = b0 + (int)(item - r * nb);
+  const int g = blk * 16 + (int)(threadIdx.x & 15);  // 4-column group
+  if (4 * g + 3 < c0 || 4 * g >= c0 + nc) return;
+  const double* fr = F + r * ldf;
+  int8_t* base = planes + (int64_t)blk * bstride + r * 64 + 4 * (g & 15);
+  uint32_t w[kSlices];
+#pragma unroll
+  for (int t = 0; t < kSlices; ++t)
+    w[t] = 4 * g < c0 ? *reinterpret_cast<const uint32_t*>(base + t * pstride) : 0u;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int c = 4 * g + e;
+    if (c < c0 || c >= c0 + nc) continue;
+    constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52
+    double rr = __ldg(fr + c) * 64.0;
+#pragma unroll
+    for (int t = 0; t < kSlices; ++t) {
+      const double q = rr + kM;
+      const uint32_t byte = (uint32_t)__double2loint(q) & 0xffu;
+      w[t] = (w[t] & ~(0xffu << (8 * e))) | (byte << (8 * e));
+      rr = (rr - (q - kM)) * 128.0;
+    }
+  }
+#pragma unroll
+  for (int t = 0; t < kSlices; ++t) *reinterpret_cast<uint32_t*>(base + t * pstride) = w[t];
+}
+
+// B' rows (logical a < m at bp[perm_row(a)], columns < kcur): per-row scale 2^-e (max < 2^e),
+// planes [t][a][k] zero for k >= kcur and for rows m <= a < rows_pad; cscale[a] = 2^(e - 12)
+__global__ void __launch_bounds__(256) slice_bprime_kernel(const double* __restrict__ bp,
+                                                           int64_t ldbp, int m, int kcur,
+                                                           int kpad, int8_t* __restrict__ planes,
+                                                           int64_t pstride,
+                                                           double* __restrict__ cscale) {
+  const int a = blockIdx.x;
+  __shared__ double s_max[8];
+  const double* row = bp + (int64_t)perm_row(a) * ldbp;
+  double mx = 0.0;
+  if (a < m)
+    for (int k = threadIdx.x; k < kcur; k += blockDim.x) mx = fmax(mx, fabs(__ldg(row + k)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) s_max[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  mx = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) mx = fmax(mx, s_max[w]);
+  int e = 0;
+  if (mx > 0.0) frexp(mx, &e);  // mx = f 2^e, f in [0.5, 1)
+  const double sc = ldexp(1.0, -e);
+  if (threadIdx.x == 0) cscale[a] = a < m ? ldexp(1.0, e - 12) : 0.0;
+  for (int k = threadIdx.x; k < kpad; k += blockDim.x) {
+    const double v = (a < m && k < kcur) ? __ldg(row + k) * sc : 0.0;
+    slice_value(v, planes + (int64_t)a * kpad + k, pstride);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 i8_encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  });
+  return fn;
+}
+
+// F's planes as a 3D tensor {64 bytes, plane_rows, kI8Slices * nblk}: box {64, 128, 1}
+static bool i8_map_a(CUtensorMap* mp, const void* base, int64_t plane_rows, int64_t nblk_all) {
+  auto fn = i8_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {64, (cuuint64_t)plane_rows, (cuuint64_t)nblk_all};
+  cuuint64_t strides[2] = {64, (cuuint64_t)(plane_rows * 64)};
+  cuuint32_t box[3] = {64, (cuuint32_t)kI8BM, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  return fn(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool i8_map(CUtensorMap* mp, const void* base, int64_t inner, int64_t rows, int64_t pitch,
+                   int box_rows) {
+  auto fn = i8_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch};
+  cuuint32_t box[2] = {(cuuint32_t)kI8KB, (cuuint32_t)box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_slice_cols(const double* F, int64_t ldf, int64_t n, int c0, int nc, int8_t* planes,
+                       int64_t plane_rows, int64_t kcap, cudaStream_t st) {
+  if (n <= 0 || nc <= 0) return;
+  const int nb = ((c0 + nc + 63) >> 6) - (c0 >> 6);
+  const int64_t items = n * nb;
+  slice_cols_kernel<<<(unsigned)((items + 15) / 16), 256, 0, st>>>(
+      F, ldf, n, c0, nc, planes, plane_rows * kcap, plane_rows * 64);
+}
+
+int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, int64_t n_rows,
+                       const double* bp, int64_t ldbp, int m, int kcur, int8_t* bplanes,
+                       double* cscale, double* C, int64_t ldc, cudaStream_t st) {
+  if (m < 1 || m > kI8MaxCols || kcur < 1 || n_rows <= 0) return -1;
+  const int kpad = (kcur + kI8KB - 1) / kI8KB * kI8KB;
+  if (kpad > kcap) return -1;
+  const int mpad = (m + kI8BN - 1) / kI8BN * kI8BN;  // B plane rows (zeros beyond m)
+  slice_bprime_kernel<<<mpad, 256, 0, st>>>(bp, ldbp, m, kcur, kpad, bplanes,
+                                            (int64_t)mpad * kpad, cscale);
+  CUtensorMap mA, mB;
+  if (!i8_map_a(&mA, fplanes, plane_rows, (int64_t)kSlices * (kcap / 64)) ||
+      !i8_map(&mB, bplanes, kpad, (int64_t)kSlices * mpad, kpad, kI8BN))
+    return -3;
+  const size_t smem = (size_t)kI8Nst * kI8Stage + 1024;
+  if (ensure_smem_attr((const void*)i8gemm_kernel, (int)smem) != cudaSuccess) return -2;
+  const dim3 grid((unsigned)(mpad / kI8BN), (unsigned)((n_rows + kI8BM - 1) / kI8BM));
+  i8gemm_kernel<<<grid, 192, smem, st>>>(mA, mB, (int)(kcap / 64), mpad, n_rows, m, kpad / kI8KB,
+                                         cscale, C, ldc);
+  return 0;
+}
+
+}  // namespace rpcb

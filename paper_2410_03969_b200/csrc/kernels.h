@@ -147,6 +147,40 @@ void launch_linv(const double* lacc_cm, int m, int nb, int64_t ldl, int koff, do
 void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb, int64_t ldl,
                      int koff, double* linv_rm, cudaStream_t st, int perm = 1);
 
+// ---- residual GEMM on int8 slices (i8gemm.cu) ----------------------------------------
+constexpr int kI8Slices = 7;     // base-2^7 digits per operand (Ozaki scheme I)
+constexpr int kI8MaxCols = 128;  // output columns (accepted pivots) per launch
+// The digits of v (|v| <= 1): V = rint(v 2^48) split into balanced base-2^7 digits, most
+// significant first, v = sum_t d_t 2^(-6 - 7 t) + e, |d_t| <= 64, |e| <= 2^-49 (one rounding;
+// integer ops only after the first FMA).
+__host__ __device__ inline void i8_digits(double v, int (&d)[kI8Slices]) {
+  const double t = v * 281474976710656.0 + 6755399441055744.0;  // v 2^48 + 1.5 2^52
+  long long V;
+#ifdef __CUDA_ARCH__
+  V = __double_as_longlong(t) - 0x4338000000000000LL;
+#else
+  long long bits;
+  __builtin_memcpy(&bits, &t, 8);
+  V = bits - 0x4338000000000000LL;
+#endif
+#pragma unroll
+  for (int j = kI8Slices - 1; j > 0; --j) {
+    const long long dj = ((V + 64) & 127) - 64;
+    d[j] = (int)dj;
+    V = (V - dj) >> 7;
+  }
+  d[0] = (int)V;
+}
+// F(:, c0:c0+nc) -> digit planes [kI8Slices][kcap / 64][plane_rows][64] (int8, kcap % 64 == 0)
+void launch_slice_cols(const double* F, int64_t ldf, int64_t n, int c0, int nc, int8_t* planes,
+                       int64_t plane_rows, int64_t kcap, cudaStream_t st);
+// C(:, :m) = F(:, :kcur) B'^T from F's planes and B' (rows perm_row(a) of bp, as the update's
+// B operand), sliced here into bplanes ([kI8Slices][128][kcap] int8) with per-row scales
+// (cscale[128]).  C row-major [n_rows][ldc].  Returns 0, or < 0 when not applicable.
+int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, int64_t n_rows,
+                       const double* bp, int64_t ldbp, int m, int kcur, int8_t* bplanes,
+                       double* cscale, double* C, int64_t ldc, cudaStream_t st);
+
 // ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
 struct UpdateParams {
   const double* X; int64_t dpad; int dchunks;   // X shard [n_loc][dpad]
@@ -170,6 +204,9 @@ struct UpdateParams {
   // each 16-row run's sequential sum of the new u (tsum[row / 16] = chunk_scan_core's
   // per-thread sum), so the next round's scan reads 1/16 of u (launch_chunk_chain).
   double* tsum;
+  // Residual GEMM precomputed on the tensor cores (launch_i8_residual; m <= 128): the kernel
+  // skips its own F B'^T phase and adds cext[row][col] (row-major, ld ldce) instead.
+  const double* cext; int64_t ldce;
   // RPC_DEBUG_TIMING: per-CTA cycle counters per phase ([grid][8] u64), or null
   unsigned long long* phase_clk;
   // RPC_DEBUG_TRACE: CTA 0 per-group phase clocks [G][64 tiles][8] (debug only)

@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
 
   const int m = p.m, kcur = p.kcur;
   const int nX = p.dchunks;
-  const int nFk = COLS ? 0 : (kcur + 15) >> 4;
+  const int nFk = (COLS || (REGP2 && p.cext)) ? 0 : (kcur + 15) >> 4;
   // Phase-2 A tiles start at F column kcur - koff: TMA box starts must be 16-byte
   // aligned in the inner dimension, so for odd kcur one extra leading column is
   // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
@@ -552,6 +552,25 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       if (nFk > 0) {
         const int ks = (kcur - 16 * (nFk - 1) + 3) / 4;
         consume([&](uint32_t so) { mma_stage(so, 0, ks); });
+      }
+      if (p.cext) {  // F B'^T from the tensor-core residual launch (i8gemm.cu)
+#pragma unroll
+        for (int fr = 0; fr < 2; ++fr) {
+          const int64_t grow = tile_row0 + arow[fr];
+          if (grow >= p.n_loc) continue;
+          const double* cr = p.cext + grow * p.ldce;
+#pragma unroll
+          for (int q = 0; q < NFW; ++q) {
+            const int col = 8 * q + 2 * t;
+            if (col + 1 < m) {
+              const double2 cv = __ldg(reinterpret_cast<const double2*>(cr + col));
+              acc[fr][q][0] += cv.x;
+              acc[fr][q][1] += cv.y;
+            } else if (col < m) {
+              acc[fr][q][0] += __ldg(cr + col);
+            }
+          }
+        }
       }
       mark(3);
       trc(k, 5);
