@@ -223,6 +223,12 @@ typedef struct {
   double host_setup_ms;    /* ... allocation, upload, packing, validation */
   double host_loop_ms;     /* ... the round loop */
   double host_final_ms;    /* ... finalisation (chol gather, bookkeeping) */
+  /* rounds whose residual GEMM F B'^T ran on the tensor cores (int8 digit planes, i8gemm.cu;
+   * included in update_ms / update_flops above): */
+  double tc_ms;            /* device time of those launches (digit planes of B' + GEMM) */
+  double tc_int8_ops;      /* int8 tensor-core operations issued (2 per MAC, padded shapes) */
+  double tc_fp64_flops;    /* the FP64 flops of the GEMMs they replaced (2 N m kcur) */
+  double tc_slice_ms;      /* device time appending F's columns to its digit planes */
 } rpc_timing;
 int rpc_result_timing(const rpc_result* r, rpc_timing* t);
 void rpc_result_free(rpc_result* r);

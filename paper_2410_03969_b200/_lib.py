@@ -83,6 +83,10 @@ class TimingC(C.Structure):
         ("host_setup_ms", C.c_double),
         ("host_loop_ms", C.c_double),
         ("host_final_ms", C.c_double),
+        ("tc_ms", C.c_double),
+        ("tc_int8_ops", C.c_double),
+        ("tc_fp64_flops", C.c_double),
+        ("tc_slice_ms", C.c_double),
     ]
 
 

@@ -28,6 +28,13 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
   for (int64_t j = threadIdx.x; j <= i; j += blockDim.x) out_rm[j * k + i] = F[lr * ldf + j];
 }
 
+// First factor width at which a round's residual GEMM goes to the tensor cores (i8gemm.cu):
+// below it the FP64 DMMA phase of the update is as fast (C4 crossover ~400 columns).
+static int64_t i8_min_k_env() {
+  const char* e = std::getenv("RPC_I8_MIN_K");
+  return e ? std::atoll(e) : 480;
+}
+
 // Launch tags of the fused sweep + prep (its progress word and the host sequence word):
 // unique per launch within the process.
 static unsigned next_epoch() {
@@ -239,11 +246,21 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     }
   // Residual GEMM on the tensor cores (i8gemm.cu): F's int8 digit planes are kept beside F
   // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 480) and
-  // m <= 128 compute F B'^T there; the update kernel then adds it.  Opt-in (RPC_I8=1) until
-  // it beats the FP64 DMMA path end to end (RPC_NO_I8 forces it off).
-  const bool i8_ok = !lowmem && algo == kAlgoAccelerated && !grouped &&
-                     std::getenv("RPC_I8") != nullptr && std::getenv("RPC_NO_I8") == nullptr;
-  const int64_t i8_min_k = std::getenv("RPC_I8_MIN_K") ? std::atoll(std::getenv("RPC_I8_MIN_K")) : 480;
+  // m <= 128 compute F B'^T there; the update kernel then adds it.  Used when the planes fit
+  // next to F (7 bytes per factor entry); RPC_NO_I8 forces the FP64 DMMA path.
+  bool i8_ok = !lowmem && algo == kAlgoAccelerated && !grouped && cap > i8_min_k_env() &&
+               std::getenv("RPC_NO_I8") == nullptr;
+  if (i8_ok) {
+    size_t fr = 0, tot = 0;
+    int64_t rows = 0;
+    for (const Shard& sh : res->shards) rows += round_up(std::max<int64_t>(sh.n_loc, 1), 128);
+    const double need = (double)kI8Slices * rows * round_up(cap, 64) + 8.0 * rows * kI8MaxCols;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || need > 0.8 * (double)fr) {
+      cudaGetLastError();
+      i8_ok = false;
+    }
+  }
+  const int64_t i8_min_k = i8_min_k_env();
   const int64_t i8_kcap = round_up(std::max<int64_t>(cap, 1), 64);
   std::vector<DBuf> i8_planes(res->shards.size());
   std::vector<int64_t> i8_rows(res->shards.size(), 0);
@@ -260,6 +277,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     i8_c = DBuf(ctx, sizeof(double) * (size_t)maxrows * kI8MaxCols);
   }
   int64_t i8_launches = 0;
+  double tc_ops = 0.0, tc_fl = 0.0;
+  std::vector<Ev> tc_ev, sl_ev;  // (start, end) pairs: tensor-core residual, plane appends
   // true while the last update's 16-row run sums (tsum) describe the current u: the next
   // scan then chains them (launch_chunk_chain, 1/16 of u's bytes) instead of a totals pass
   // over u, and the sampler chains the chunk offsets
@@ -768,6 +787,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         // (the tensor-core residual GEMM is timed as part of the round's update)
         if (i8_ok && kg >= i8_min_k && mg <= kI8MaxCols) {
           const size_t si = &s - res->shards.data();
+          tc_ev.emplace_back();
+          tc_ev.emplace_back();
+          CK(cudaEventRecord(tc_ev[tc_ev.size() - 2].e, st));
           if (launch_i8_residual(reinterpret_cast<const int8_t*>(i8_planes[si].p), i8_rows[si],
                                  i8_kcap, s.n_loc, fs.as<double>(), ldf, mg, (int)kg,
                                  reinterpret_cast<int8_t*>(i8_bplanes.p), i8_cscale.as<double>(),
@@ -776,7 +798,11 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
             up.ldce = kI8MaxCols;
             ++i8_launches;
             launches += 2;
+            const double rows = (double)round_up(s.n_loc, 128), cols = (double)round_up(mg, 64);
+            tc_ops += 2.0 * (kI8Slices * (kI8Slices + 1) / 2) * rows * cols * (double)round_up(kg, 64);
+            tc_fl += 2.0 * (double)s.n_loc * mg * (double)kg;
           }
+          CK(cudaEventRecord(tc_ev.back().e, st));
         }
         if (dbg_chain) host_pre_us += 1e3 * ms_since(h_wake);
         cmark("host gap");
@@ -818,13 +844,18 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       }  // groups
       // this round's columns into F's digit planes (coalesced: a warp per row segment; byte
       // stores from the update epilogue's fragment layout measured 3-4x slower per round)
-      if (i8_ok)
+      if (i8_ok) {
+        sl_ev.emplace_back();
+        sl_ev.emplace_back();
+        CK(cudaEventRecord(sl_ev[sl_ev.size() - 2].e, st));
         for (size_t si = 0; si < res->shards.size(); ++si) {
           Shard& s = res->shards[si];
           launch_slice_cols(s.F.as<double>(), ldf, s.n_loc, (int)kcur, m,
                             reinterpret_cast<int8_t*>(i8_planes[si].p), i8_rows[si], i8_kcap, st);
           ++launches;
         }
+        CK(cudaEventRecord(sl_ev.back().e, st));
+      }
       pending_g2 = true;
       if (sink.p) {
         const auto hs0 = clk::now();
@@ -944,6 +975,21 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     std::fprintf(stderr, "[rpc] host: wake -> update launch %.1f us, launch call %.1f us (per update)\n",
                  host_pre_us / std::max<int64_t>(1, upd_launches),
                  host_launch_us / std::max<int64_t>(1, upd_launches));
+  }
+  {
+    double tcm = 0.0, slm = 0.0;
+    for (size_t i = 0; i + 1 < tc_ev.size(); i += 2) {
+      CK(cudaEventElapsedTime(&ms, tc_ev[i].e, tc_ev[i + 1].e));
+      tcm += ms;
+    }
+    for (size_t i = 0; i + 1 < sl_ev.size(); i += 2) {
+      CK(cudaEventElapsedTime(&ms, sl_ev[i].e, sl_ev[i + 1].e));
+      slm += ms;
+    }
+    tm.tc_ms = tcm;
+    tm.tc_int8_ops = tc_ops;
+    tm.tc_fp64_flops = tc_fl;
+    tm.tc_slice_ms = slm;
   }
   tm.update_flops = flops;
   tm.update_bytes = bytes;

@@ -14,14 +14,16 @@
 // representation error bound the result at ~6e-14 of sum_j |F_ij| |B'_cj| (tools/ozaki_probe.cu:
 // 6.2e-14 measured at the C4 round-9 shape; the FP64 DMMA GEMM it replaces is ~1e-16 of that).
 //
-// Kernel: one CTA per 128 F rows x 64 output columns; kSlices accumulators x 64 TMEM columns
-// (448 of 512).  Warp 0 issues the TMA loads (kSlices + kSlices planes per 64-byte K block,
-// 64-byte swizzle, two stages), warp 1 the MMAs (one thread; tcgen05.commit frees a stage),
-// warps 2-5 the epilogue (tcgen05.ld 32x32b, FP64 Horner over the diagonals, column scale).
+// Kernel: persistent, tiles of 128 F rows x 64 output columns; kSlices accumulators x 64 TMEM
+// columns (448 of 512).  Warp 0 issues the TMA loads (kSlices + kSlices planes per 64-byte K
+// block, 64-byte swizzle, two stages), warp 1 the MMAs (one thread; tcgen05.commit frees a
+// stage), warps 2-5 the epilogue (tcgen05.ld 32x32b, FP64 sum over the diagonals, column
+// scale), which releases each diagonal to the next tile's MMAs as soon as it has read it.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -43,6 +45,7 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const void* tmap, in
       : "memory");
 }
 
+// K-major operand tile of 64-byte rows with the 64-byte swizzle (two MMA K steps per row)
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   uint64_t d = (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)1 << 16;           // leading byte offset (unused: swizzled K-major)
@@ -52,27 +55,30 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
   return d;
 }
 
+// Persistent: a CTA per SM walks the (row tile, column half) tiles.  The epilogue drains the
+// diagonals in order d = 0 .. 6 (C = sum_d 2^(-7 d) A_d accumulated in FP64 registers, 64
+// columns a thread) and releases each diagonal's TMEM columns as soon as it has read them; the
+// next tile's first K block issues its products diagonal by diagonal, each diagonal's first
+// product (which overwrites) after that release, so the drain overlaps the next tile's MMAs.
 __global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ CUtensorMap tmA,
                                                        const __grid_constant__ CUtensorMap tmB,
                                                        int a_nblk, int b_plane_rows,
-                                                       int64_t n_rows, int m, int nkb,
+                                                       int64_t n_rows, int m, int nkb, int ncolt,
+                                                       int64_t ntiles,
                                                        const double* __restrict__ cscale,
                                                        double* __restrict__ C, int64_t ldc) {
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
-  __shared__ uint64_t full[kI8Nst], empty[kI8Nst], done;
+  __shared__ uint64_t full[kI8Nst], empty[kI8Nst], done, drained[kSlices];
   __shared__ uint32_t tmem_base_s;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // (column halves of one row tile are adjacent in launch order, so the second CTA's A
-  // planes come from L2 instead of HBM)
-  const int64_t row0 = (int64_t)blockIdx.y * kI8BM;
-  const int col0 = blockIdx.x * kI8BN;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kI8Nst; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
     mbar_init(&done, 1);
+    for (int d = 0; d < kSlices; ++d) mbar_init(&drained[d], 4);
     mbar_fence_init();
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -88,16 +94,21 @@ __global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ 
   const uint32_t tbase = tmem_base_s;
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kI8Nst;
-        if (kb >= kI8Nst) mbar_wait(&empty[s], ((kb / kI8Nst) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], kI8Stage);
-        unsigned char* st = sm + s * kI8Stage;
-        for (int t = 0; t < kSlices; ++t)
-          tma_load_3d(st + t * kI8Apl, &tmA, 0, (int)row0, t * a_nblk + kb, &full[s]);
-        for (int u = 0; u < kSlices; ++u)
-          tma_load_2d(st + kSlices * kI8Apl + u * kI8Bpl, &tmB, kb * kI8KB, u * b_plane_rows + col0,
-                      &full[s]);
+      int it = 0;  // stage use counter across tiles
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row0 = (tile / ncolt) * kI8BM;
+        const int col0 = (int)(tile % ncolt) * kI8BN;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kI8Nst;
+          if (it >= kI8Nst) mbar_wait(&empty[s], ((it / kI8Nst) - 1) & 1);
+          mbar_arrive_expect_tx(&full[s], kI8Stage);
+          unsigned char* st = sm + s * kI8Stage;
+          for (int t = 0; t < kSlices; ++t)
+            tma_load_3d(st + t * kI8Apl, &tmA, 0, (int)row0, t * a_nblk + kb, &full[s]);
+          for (int u = 0; u < kSlices; ++u)
+            tma_load_2d(st + kSlices * kI8Apl + u * kI8Bpl, &tmB, kb * kI8KB,
+                        u * b_plane_rows + col0, &full[s]);
+        }
       }
     }
   } else if (warp == 1) {
@@ -105,65 +116,84 @@ __global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ 
       // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = 64
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                              ((uint32_t)(kI8BN >> 3) << 17) | ((uint32_t)(kI8BM >> 4) << 24);
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kI8Nst;
-        mbar_wait(&full[s], (kb / kI8Nst) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const uint32_t ba = smem_u32(sm + s * kI8Stage), bb = ba + kSlices * kI8Apl;
+      int it = 0, ti = 0;
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = it % kI8Nst;
+          mbar_wait(&full[s], (it / kI8Nst) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+          const uint32_t ba = smem_u32(sm + s * kI8Stage), bb = ba + kSlices * kI8Apl;
+          // products diagonal by diagonal; in the first K block a diagonal's first product
+          // overwrites it, once the previous tile's epilogue has drained it
 #pragma unroll
-        for (int t = 0; t < kSlices; ++t)
-#pragma unroll
-          for (int u = 0; u < kSlices - t; ++u)
-#pragma unroll
-            for (int ks = 0; ks < kI8KB / 32; ++ks) {
-              const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
-              const uint64_t db = umma_desc_sw64(bb + u * kI8Bpl + ks * 32);
-              // the first product of each diagonal (t = 0) at the first K step overwrites
-              const uint32_t accum = (kb | ks | t) != 0;
-              asm volatile(
-                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-                      tbase + (uint32_t)((t + u) * kI8BN)),
-                  "l"(da), "l"(db), "r"(idesc), "r"(accum));
+          for (int d = 0; d < kSlices; ++d) {
+            if (kb == 0 && ti > 0) {
+              mbar_wait(&drained[d], (ti - 1) & 1);
+              asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             }
+#pragma unroll
+            for (int t = 0; t <= d; ++t)
+#pragma unroll
+              for (int ks = 0; ks < kI8KB / 32; ++ks) {
+                const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
+                const uint64_t db = umma_desc_sw64(bb + (d - t) * kI8Bpl + ks * 32);
+                const uint32_t accum = (kb | ks | t) != 0;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                        tbase + (uint32_t)(d * kI8BN)),
+                    "l"(da), "l"(db), "r"(idesc), "r"(accum));
+              }
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                  smem_u32(&empty[s])));
+        }
         asm volatile(
             "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                smem_u32(&empty[s])));
+                smem_u32(&done)));
       }
-      asm volatile(
-          "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-              smem_u32(&done)));
     }
   } else {
-    mbar_wait(&done, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const int q = warp & 3;  // the TMEM lane quadrant this warp may read
-    const int64_t r = row0 + q * 32 + lane;
-#pragma unroll 1
-    for (int cc = 0; cc < kI8BN / 16; ++cc) {
-      double acc[16];
+    int ti = 0;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++ti) {
+      const int64_t r = (tile / ncolt) * kI8BM + q * 32 + lane;
+      const int col0 = (int)(tile % ncolt) * kI8BN;
+      mbar_wait(&done, ti & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      double acc[kI8BN];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+      for (int j = 0; j < kI8BN; ++j) acc[j] = 0.0;
+      double wd = 1.0;  // 2^(-7 d)
 #pragma unroll
-      for (int d = kSlices - 1; d >= 0; --d) {
-        uint32_t v[16];
-        const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * kI8BN + cc * 16);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
-            "%10, %11, %12, %13, %14, %15}, [%16];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-              "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-              "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-            : "r"(ta));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+      for (int d = 0; d < kSlices; ++d) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[j] = fma(acc[j], 0.0078125, (double)(int)v[j]);
+        for (int cc = 0; cc < kI8BN / 16; ++cc) {
+          uint32_t v[16];
+          const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * kI8BN + cc * 16);
+          asm volatile(
+              "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+              "%10, %11, %12, %13, %14, %15}, [%16];\n"
+              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+              : "r"(ta));
+          asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[cc * 16 + j] = fma((double)(int)v[j], wd, acc[cc * 16 + j]);
+        }
+        // this warp's reads of diagonal d are complete: release its TMEM columns
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&drained[d]);
+        wd *= 0.0078125;
       }
       if (r < n_rows) {
-        double* cr = C + r * ldc + col0 + cc * 16;
+        double* cr = C + r * ldc + col0;
 #pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          const int c = col0 + cc * 16 + j;
+        for (int j = 0; j < kI8BN; j += 2) {
+          const int c = col0 + j;
           if (c + 1 < m)
             *reinterpret_cast<double2*>(cr + j) =
                 make_double2(acc[j] * cscale[c], acc[j + 1] * cscale[c + 1]);
@@ -192,43 +222,68 @@ __device__ __forceinline__ void slice_value(double v, int8_t* out, int64_t pstri
 }
 
 // F's digit planes are column-block-major, [kI8Slices][kcap / 64][plane_rows][64] bytes: the
-// GEMM's A tile (128 rows x 64 K bytes) is one contiguous 8 KB box, and a round's new columns
-// land in whole 64-byte row segments.  Columns [c0, c0 + nc): a half-warp per (row, block), a
-// lane per 4-column group, one 32-bit store per plane; the group holding c0 keeps its bytes
-// below c0 (earlier rounds' digits).
+// GEMM's A tile (128 rows x 64 K bytes) is one contiguous box, and a round's new columns land
+// in whole 64-byte row segments.  Columns [c0, c0 + nc): a thread per (row, 8-column group):
+// two 32-byte loads of F, 56 digits, one 64-bit store per plane; the group holding c0 keeps
+// its bytes below c0 (earlier rounds' digits).
 __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ F, int64_t ldf,
                                                          int64_t n, int c0, int nc,
                                                          int8_t* __restrict__ planes,
                                                          int64_t pstride, int64_t bstride) {
-  const int b0 = c0 >> 6, nb = ((c0 + nc + 63) >> 6) - b0;
-  const int64_t item = blockIdx.x * 16 + (threadIdx.x >> 4);  // (row, block) pair
-  if (item >= n * nb) return;
-  const int64_t r = item / nb;
-  const int blk = b0 + (int)(item - r * nb);
-  const int g = blk * 16 + (int)(threadIdx.x & 15);  // 4-column group
-  if (4 * g + 3 < c0 || 4 * g >= c0 + nc) return;
-  const double* fr = F + r * ldf;
-  int8_t* base = planes + (int64_t)blk * bstride + r * 64 + 4 * (g & 15);
-  uint32_t w[kSlices];
+  const int g0 = c0 >> 3, ng = ((c0 + nc + 7) >> 3) - g0;
+  const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (item >= n * ng) return;
+  const int64_t r = item / ng;
+  const int g = g0 + (int)(item - r * ng);  // 8-column group
+  const int blk = g >> 3;
+  const double* fr = F + r * ldf + 8 * g;
+  int8_t* base = planes + (int64_t)blk * bstride + r * 64 + 8 * (g & 7);
+  uint64_t w[kSlices];
+  const bool head = 8 * g < c0;
 #pragma unroll
   for (int t = 0; t < kSlices; ++t)
-    w[t] = 4 * g < c0 ? *reinterpret_cast<const uint32_t*>(base + t * pstride) : 0u;
+    w[t] = head ? *reinterpret_cast<const uint64_t*>(base + t * pstride) : 0ull;
+  double v[8];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int c = 4 * g + e;
+  for (int e = 0; e < 8; ++e) {
+    const int c = 8 * g + e;
+    v[e] = (c >= c0 && c < c0 + nc) ? __ldg(fr + e) : 0.0;
+  }
+  // digits of F: V = rint(F 2^48) (|V| <= 2^48), d_0 = V >> 42 (signed, |d_0| <= 64) and six
+  // unsigned 7-bit chunks below it (0 .. 127): F = sum_t d_t 2^(-6 - 7 t) within 2^-49.  Integer
+  // ops only after one FMA (the balanced FP64 digit chain cost ~3x more here).
+  uint32_t wl[kSlices], wh[kSlices];
+#pragma unroll
+  for (int t = 0; t < kSlices; ++t) {
+    wl[t] = (uint32_t)w[t];
+    wh[t] = (uint32_t)(w[t] >> 32);
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int c = 8 * g + e;
     if (c < c0 || c >= c0 + nc) continue;
-    constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52
-    double rr = __ldg(fr + c) * 64.0;
+    const double q = fma(v[e], 281474976710656.0, 6755399441055744.0);  // v 2^48 + 1.5 2^52
+    const long long V = __double_as_longlong(q) - 0x4338000000000000LL;
+    const uint32_t lo = (uint32_t)V, hi = (uint32_t)((unsigned long long)V >> 32);
+    uint32_t dg[kSlices];
+    dg[6] = lo & 127u;
+    dg[5] = (lo >> 7) & 127u;
+    dg[4] = (lo >> 14) & 127u;
+    dg[3] = (lo >> 21) & 127u;
+    dg[2] = __funnelshift_r(lo, hi, 28) & 127u;
+    dg[1] = (hi >> 3) & 127u;
+    dg[0] = (uint32_t)((int)hi >> 10) & 0xffu;  // V >> 42, two's complement byte
+    const int sh = 8 * (e & 3);
 #pragma unroll
     for (int t = 0; t < kSlices; ++t) {
-      const double q = rr + kM;
-      const uint32_t byte = (uint32_t)__double2loint(q) & 0xffu;
-      w[t] = (w[t] & ~(0xffu << (8 * e))) | (byte << (8 * e));
-      rr = (rr - (q - kM)) * 128.0;
+      if (e < 4) wl[t] = (wl[t] & ~(0xffu << sh)) | (dg[t] << sh);
+      else wh[t] = (wh[t] & ~(0xffu << sh)) | (dg[t] << sh);
     }
   }
 #pragma unroll
-  for (int t = 0; t < kSlices; ++t) *reinterpret_cast<uint32_t*>(base + t * pstride) = w[t];
+  for (int t = 0; t < kSlices; ++t) w[t] = ((uint64_t)wh[t] << 32) | wl[t];
+#pragma unroll
+  for (int t = 0; t < kSlices; ++t) *reinterpret_cast<uint64_t*>(base + t * pstride) = w[t];
 }
 
 // B' rows (logical a < m at bp[perm_row(a)], columns < kcur): per-row scale 2^-e (max < 2^e),
@@ -280,7 +335,7 @@ static bool i8_map_a(CUtensorMap* mp, const void* base, int64_t plane_rows, int6
   if (!fn) return false;
   cuuint64_t dims[3] = {64, (cuuint64_t)plane_rows, (cuuint64_t)nblk_all};
   cuuint64_t strides[2] = {64, (cuuint64_t)(plane_rows * 64)};
-  cuuint32_t box[3] = {64, (cuuint32_t)kI8BM, 1};
+  cuuint32_t box[3] = {(cuuint32_t)kI8KB, (cuuint32_t)kI8BM, 1};
   cuuint32_t es[3] = {1, 1, 1};
   return fn(mp, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
@@ -303,9 +358,9 @@ static bool i8_map(CUtensorMap* mp, const void* base, int64_t inner, int64_t row
 void launch_slice_cols(const double* F, int64_t ldf, int64_t n, int c0, int nc, int8_t* planes,
                        int64_t plane_rows, int64_t kcap, cudaStream_t st) {
   if (n <= 0 || nc <= 0) return;
-  const int nb = ((c0 + nc + 63) >> 6) - (c0 >> 6);
-  const int64_t items = n * nb;
-  slice_cols_kernel<<<(unsigned)((items + 15) / 16), 256, 0, st>>>(
+  const int ng = ((c0 + nc + 7) >> 3) - (c0 >> 3);
+  const int64_t items = n * ng;
+  slice_cols_kernel<<<(unsigned)((items + 255) / 256), 256, 0, st>>>(
       F, ldf, n, c0, nc, planes, plane_rows * kcap, plane_rows * 64);
 }
 
@@ -323,9 +378,11 @@ int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, 
       !i8_map(&mB, bplanes, kpad, (int64_t)kSlices * mpad, kpad, kI8BN))
     return -3;
   const size_t smem = (size_t)kI8Nst * kI8Stage + 1024;
+  const int a_nblk = (int)(kcap / 64), nkb = kpad / kI8KB, ncolt = mpad / kI8BN;
+  const int64_t ntiles = (n_rows + kI8BM - 1) / kI8BM * ncolt;
   if (ensure_smem_attr((const void*)i8gemm_kernel, (int)smem) != cudaSuccess) return -2;
-  const dim3 grid((unsigned)(mpad / kI8BN), (unsigned)((n_rows + kI8BM - 1) / kI8BM));
-  i8gemm_kernel<<<grid, 192, smem, st>>>(mA, mB, (int)(kcap / 64), mpad, n_rows, m, kpad / kI8KB,
+  const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
+  i8gemm_kernel<<<grid, 192, smem, st>>>(mA, mB, a_nblk, mpad, n_rows, m, nkb, ncolt, ntiles,
                                          cscale, C, ldc);
   return 0;
 }

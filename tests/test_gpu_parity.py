@@ -493,3 +493,28 @@ def test_update_fused_scan_bitwise_equals_totals_pass(ctx, monkeypatch, n, d, b,
     assert a.relative_trace_error == r.relative_trace_error
     if shards > 1:
         c.close()
+
+
+@pytest.mark.parametrize("n,d,b,k,kernel", [(60000, 30, 120, 800, "gaussian"),
+                                            (40000, 10, 64, 700, "gaussian"),
+                                            (50000, 20, 100, 650, "laplace")])
+def test_tensor_core_residual_matches_dmma_and_oracle(ctx, monkeypatch, n, d, b, k, kernel):
+    """Rounds past RPC_I8_MIN_K compute F B'^T from int8 digit planes on tcgen05 (i8gemm.cu):
+    same pivots as the FP64 DMMA path and the oracle, factor within the parity bar."""
+    x = wl.gen_c1(n, d, 6)
+    sigma = math.sqrt(d)
+    spec = api.KernelSpec(kernel, sigma)
+    cfg = api.RunConfig.until_rank(k, b, 21)
+    monkeypatch.setenv("RPC_I8_MIN_K", "256")
+    monkeypatch.delenv("RPC_NO_I8", raising=False)
+    a = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    monkeypatch.setenv("RPC_NO_I8", "1")
+    r = api.accelerated_rpcholesky(api.KernelOracle(x, spec), cfg, ctx)
+    assert np.array_equal(a.pivots, r.pivots)
+    rel = np.linalg.norm(a.factor - r.factor) / np.linalg.norm(r.factor)
+    assert rel <= 1e-10, rel
+    assert abs(a.relative_trace_error - r.relative_trace_error) <= 1e-12
+    o = po.Oracle(x=x, kernel=kernel, sigma=sigma, n_threads=8)
+    ref = po.accelerated_rpcholesky(o, block_size=b, seed=21, target_rank=k)
+    assert np.array_equal(a.pivots, ref.pivots)
+    assert np.linalg.norm(a.factor - ref.factor) / np.linalg.norm(ref.factor) <= F_TOL

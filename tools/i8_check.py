@@ -20,9 +20,9 @@ cfg = api.RunConfig.until_rank(w.k, w.b, w.seed)
 res = {}
 for mode in ("dmma", "i8"):
     if mode == "dmma":
-        os.environ.pop("RPC_I8", None)
+        os.environ["RPC_NO_I8"] = "1"
     else:
-        os.environ["RPC_I8"] = "1"
+        os.environ.pop("RPC_NO_I8", None)
     ts = []
     for rep in range(3):
         r = api.accelerated_rpcholesky_device(xd.data_ptr(), w.n, w.d, w.d, L.RPC_ROW_MAJOR, spec,
