@@ -119,6 +119,15 @@ __device__ __forceinline__ double kfun_eval(double dd, int f, double s, const do
   return exp_tab(dd * s, tab);
 }
 
+// f(integral_constant<J>) for J = 0 .. N-1 (compile-time indices into register arrays).
+template <int N, int J = 0, class F>
+__device__ __forceinline__ void static_for_asc(F&& f) {
+  if constexpr (J < N) {
+    f(std::integral_constant<int, J>{});
+    static_for_asc<N, J + 1>(f);
+  }
+}
+
 // f(integral_constant<J>) for J = N-1 down to 0 (compile-time indices into register arrays).
 template <int J, class F>
 __device__ __forceinline__ void static_for_desc(F&& f) {
@@ -171,7 +180,10 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
   // loaded and multiplied by the zero column 0 of the shifted L^{-1} (koff = 1).
   const int koff = kcur & 1;
   const int nL = (COLS || p.columns_only) ? 0 : REGP2 ? (m + 15) >> 4 : (m + koff + 15) >> 4;
-  const int T = nX + nFk + nL;               // chunks per tile
+  // REGP2 with a tensor-core residual (p.cext): C's 16-column chunks stream through the ring's
+  // A slots in place of the F chunks (TMA, tmG re-pointed at C), so the add is prefetched
+  const int nCk = (REGP2 && p.cext) ? (m + 15) >> 4 : 0;
+  const int T = nX + nFk + nL + nCk;         // chunks per tile
   const int ntiles = (int)((p.n_loc + BM - 1) / BM);
   const int vb = (int)blockIdx.x * G + grp, vgrid = (int)gridDim.x * G;  // virtual block per group
   const int my_tiles = vb < ntiles ? (ntiles - 1 - vb) / vgrid + 1 : 0;
@@ -220,8 +232,11 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
       unsigned char* Bs = As + C::A_BYTES;
       const int r0 = (int)((vb + (int64_t)k * vgrid) * BM);
       const bool l_only = REGP2 && c >= nX && c < nX + nL;  // phase 2: the L^{-1} chunk only
-      mbar_arrive_expect_tx(&full[s], l_only ? C::B_BYTES : C::STAGE);
-      if (c < nX) {
+      const bool c_only = REGP2 && nCk > 0 && c >= nX + nL;   // tensor-core residual chunk
+      mbar_arrive_expect_tx(&full[s], l_only ? C::B_BYTES : c_only ? C::A_BYTES : C::STAGE);
+      if (c_only) {
+        tma_load_2d(As, &tmG, 16 * (c - nX - nL), r0, &full[s]);
+      } else if (c < nX) {
         tma_load_2d(As, &tmX, 16 * c, r0, &full[s]);
         tma_load_2d(Bs, &tmXS, 16 * c, 0, &full[s]);
       } else if (l_only) {  // chunks J = nL-1 .. 0 (descending, see REGP2)
@@ -553,25 +568,25 @@ __global__ void __launch_bounds__(UCfg<WC, NFW, G>::NT, MINB)
         const int ks = (kcur - 16 * (nFk - 1) + 3) / 4;
         consume([&](uint32_t so) { mma_stage(so, 0, ks); });
       }
-      if (p.cext) {  // F B'^T from the tensor-core residual launch (i8gemm.cu)
+      // F B'^T from the tensor-core residual launch (i8gemm.cu): chunk J of C holds columns
+      // 16 J .. 16 J + 15, i.e. this lane's fragments 2 J and 2 J + 1
+      static_for_asc<(NFW + 1) / 2>([&](auto JC) {
+        constexpr int J = decltype(JC)::value;
+        if (J >= nCk) return;
+        consume([&](uint32_t so) {
+          const unsigned char* Aw = stages + so;
 #pragma unroll
-        for (int fr = 0; fr < 2; ++fr) {
-          const int64_t grow = tile_row0 + arow[fr];
-          if (grow >= p.n_loc) continue;
-          const double* cr = p.cext + grow * p.ldce;
+          for (int h = 0; h < 2; ++h) {
+            if (2 * J + h >= NFW) continue;
 #pragma unroll
-          for (int q = 0; q < NFW; ++q) {
-            const int col = 8 * q + 2 * t;
-            if (col + 1 < m) {
-              const double2 cv = __ldg(reinterpret_cast<const double2*>(cr + col));
-              acc[fr][q][0] += cv.x;
-              acc[fr][q][1] += cv.y;
-            } else if (col < m) {
-              acc[fr][q][0] += __ldg(cr + col);
-            }
+            for (int fr = 0; fr < 2; ++fr)
+#pragma unroll
+              for (int v = 0; v < 2; ++v)
+                acc[fr][2 * J + h][v] +=
+                    *reinterpret_cast<const double*>(Aw + swz_off(arow[fr], 8 * h + 2 * t + v));
           }
-        }
-      }
+        });
+      });
       mark(3);
       trc(k, 5);
     } else {
@@ -754,7 +769,9 @@ int launch_t(const UpdateParams& p, cudaStream_t st) {
             make_map(&mXS, p.xs, p.dpad, C::NB, p.dpad, C::NB) &&
             make_map(&mF, p.F, p.kcur, p.n_loc, p.ldf, C::BM) &&
             make_map(&mFS, p.fs, p.kcur, C::NB, p.ldfs, C::NB) &&
-            make_map(&mG, p.F, p.kcur + p.m, p.n_loc, p.ldf, C::BM) &&
+            ((WC == 1 && !COLS && p.cext)  // tmG: C (tensor-core residual) when present
+                 ? make_map(&mG, p.cext, p.ldce, p.n_loc, p.ldce, C::BM)
+                 : make_map(&mG, p.F, p.kcur + p.m, p.n_loc, p.ldf, C::BM)) &&
             make_map(&mL, p.linv, p.ldl, C::NB, p.ldl, C::NB);
   if (!ok) return -3;
   const auto t2 = std::chrono::steady_clock::now();
