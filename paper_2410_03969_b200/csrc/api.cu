@@ -29,10 +29,10 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 }
 
 // First factor width at which a round's residual GEMM goes to the tensor cores (i8gemm.cu):
-// below it the FP64 DMMA phase of the update is as fast (C4 crossover ~400 columns).
+// below it the FP64 DMMA phase of the update is as fast (C4: ~300 columns).
 static int64_t i8_min_k_env() {
   const char* e = std::getenv("RPC_I8_MIN_K");
-  return e ? std::atoll(e) : 480;
+  return e ? std::atoll(e) : 384;
 }
 
 // Launch tags of the fused sweep + prep (its progress word and the host sequence word):
@@ -245,36 +245,38 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       scan_tsum[si] = DBuf(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, 4 * ntiles64));
     }
   // Residual GEMM on the tensor cores (i8gemm.cu): F's int8 digit planes are kept beside F
-  // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 480) and
+  // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 384) and
   // m <= 128 compute F B'^T there; the update kernel then adds it.  Used when the planes fit
   // next to F (7 bytes per factor entry); RPC_NO_I8 forces the FP64 DMMA path.
   bool i8_ok = !lowmem && algo == kAlgoAccelerated && !grouped && cap > i8_min_k_env() &&
                std::getenv("RPC_NO_I8") == nullptr;
-  if (i8_ok) {
-    size_t fr = 0, tot = 0;
-    int64_t rows = 0;
-    for (const Shard& sh : res->shards) rows += round_up(std::max<int64_t>(sh.n_loc, 1), 128);
-    const double need = (double)kI8Slices * rows * round_up(cap, 64) + 8.0 * rows * kI8MaxCols;
-    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess || need > 0.8 * (double)fr) {
-      cudaGetLastError();
-      i8_ok = false;
-    }
-  }
+
   const int64_t i8_min_k = i8_min_k_env();
   const int64_t i8_kcap = round_up(std::max<int64_t>(cap, 1), 64);
   std::vector<DBuf> i8_planes(res->shards.size());
   std::vector<int64_t> i8_rows(res->shards.size(), 0);
   DBuf i8_bplanes, i8_cscale, i8_c;
   if (i8_ok) {
-    int64_t maxrows = 0;
-    for (size_t si = 0; si < res->shards.size(); ++si) {
-      i8_rows[si] = round_up(std::max<int64_t>(res->shards[si].n_loc, 1), 128);
-      maxrows = std::max(maxrows, i8_rows[si]);
-      i8_planes[si] = DBuf(ctx, (size_t)kI8Slices * i8_rows[si] * i8_kcap);
+    // (the planes take 7 bytes per factor entry: when they do not fit next to F the run
+    // stays on the FP64 DMMA path instead of failing)
+    try {
+      int64_t maxrows = 0;
+      for (size_t si = 0; si < res->shards.size(); ++si) {
+        i8_rows[si] = round_up(std::max<int64_t>(res->shards[si].n_loc, 1), 128);
+        maxrows = std::max(maxrows, i8_rows[si]);
+        i8_planes[si] = DBuf(ctx, (size_t)kI8Slices * i8_rows[si] * i8_kcap);
+      }
+      i8_bplanes = DBuf(ctx, (size_t)kI8Slices * kI8MaxCols * i8_kcap);
+      i8_cscale = DBuf(ctx, sizeof(double) * kI8MaxCols);
+      i8_c = DBuf(ctx, sizeof(double) * (size_t)maxrows * kI8MaxCols);
+    } catch (const RpcError&) {
+      cudaGetLastError();
+      for (auto& b : i8_planes) b.release();
+      i8_bplanes.release();
+      i8_cscale.release();
+      i8_c.release();
+      i8_ok = false;
     }
-    i8_bplanes = DBuf(ctx, (size_t)kI8Slices * kI8MaxCols * i8_kcap);
-    i8_cscale = DBuf(ctx, sizeof(double) * kI8MaxCols);
-    i8_c = DBuf(ctx, sizeof(double) * (size_t)maxrows * kI8MaxCols);
   }
   int64_t i8_launches = 0;
   double tc_ops = 0.0, tc_fl = 0.0;
@@ -844,7 +846,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       }  // groups
       // this round's columns into F's digit planes (coalesced: a warp per row segment; byte
       // stores from the update epilogue's fragment layout measured 3-4x slower per round)
-      if (i8_ok) {
+      // (not after the last round: nothing reads its digits)
+      const bool last_round = cfg.mode == RPC_FIXED_ROUNDS ? round + 1 >= cfg.rounds
+                                                           : kcur + m >= cfg.target_rank;
+      if (i8_ok && !last_round) {
         sl_ev.emplace_back();
         sl_ev.emplace_back();
         CK(cudaEventRecord(sl_ev[sl_ev.size() - 2].e, st));
