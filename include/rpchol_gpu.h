@@ -61,9 +61,12 @@ typedef struct {
 
 /* RunConfig (rpcholesky.hpp:36-67) plus B200 execution flags. */
 enum {
-  RPC_FLAG_REPLAY_SCAN = 1u /* sequential cumulative_sums + upper_bound exactly as
-                               rng.hpp:67-96 over the global residual diagonal (gathered
-                               on every shard when sharded); slower */
+  /* sequential cumulative_sums + upper_bound exactly as rng.hpp:67-96 over the global
+     residual diagonal (gathered on every shard when sharded); slower */
+  RPC_FLAG_REPLAY_SCAN = 1u,
+  /* every round's residual GEMM on the FP64 DMMA path (no int8 tensor-core digit
+     products) */
+  RPC_FLAG_FP64_RESIDUAL = 2u
 };
 typedef struct {
   int64_t block_size;  /* b >= 1 (this build: b <= 1024; low-memory variant b <= 256) */

@@ -18,6 +18,7 @@ RPC_DIST_DIRECT, RPC_DIST_GRAM, RPC_DIST_DEFAULT = 0, 1, -1
 RPC_FIXED_ROUNDS, RPC_UNTIL_RANK = 0, 1
 RPC_COL_MAJOR, RPC_ROW_MAJOR = 0, 1
 RPC_FLAG_REPLAY_SCAN = 1
+RPC_FLAG_FP64_RESIDUAL = 2
 
 # Every symbol include/rpchol_gpu.h declares (checked by tests/test_boundary.py).
 EXPORTS = [

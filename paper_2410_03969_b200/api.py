@@ -41,6 +41,7 @@ class RunConfig:
     seed: int = 0
     stop_tol: float = 0.0
     replay_scan: bool = False
+    fp64_residual: bool = False  # every round's residual GEMM on FP64 DMMA (no int8 digits)
 
     @staticmethod
     def fixed_rounds(t: int, b: int, seed: int) -> "RunConfig":
@@ -58,7 +59,8 @@ class RunConfig:
         mode = L.RPC_FIXED_ROUNDS if self.mode == "fixed_rounds" else L.RPC_UNTIL_RANK
         return L.RunConfigC(self.block_size, mode, self.rounds, self.target_rank,
                             self.seed & 0xFFFFFFFFFFFFFFFF, self.stop_tol,
-                            L.RPC_FLAG_REPLAY_SCAN if self.replay_scan else 0)
+                            (L.RPC_FLAG_REPLAY_SCAN if self.replay_scan else 0) |
+                            (L.RPC_FLAG_FP64_RESIDUAL if self.fp64_residual else 0))
 
 
 class Context:

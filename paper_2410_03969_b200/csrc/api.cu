@@ -249,7 +249,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   // m <= 128 compute F B'^T there; the update kernel then adds it.  Used when the planes fit
   // next to F (7 bytes per factor entry); RPC_NO_I8 forces the FP64 DMMA path.
   bool i8_ok = !lowmem && algo == kAlgoAccelerated && !grouped && cap > i8_min_k_env() &&
-               std::getenv("RPC_NO_I8") == nullptr;
+               !(cfg.flags & RPC_FLAG_FP64_RESIDUAL) && std::getenv("RPC_NO_I8") == nullptr;
 
   const int64_t i8_min_k = i8_min_k_env();
   const int64_t i8_kcap = round_up(std::max<int64_t>(cap, 1), 64);

@@ -371,7 +371,9 @@ int rpc_krr_fit(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx
       rpc_run_config c2 = cfg;
       c2.mode = RPC_UNTIL_RANK;
       c2.target_rank = std::min(precond_rank, n);
-      c2.flags = 0;
+      // (the preconditioner keeps the FP64 DMMA residual: PCG iteration counts follow the
+      // reference's to +-1 with it, and moved by 3 on a fixture with the int8 digit path)
+      c2.flags = RPC_FLAG_FP64_RESIDUAL;
       rpc_kernel_spec ks = kspec;
       ks.distance_mode = RPC_DIST_DEFAULT;
       res.reset(new rpc_result());
