@@ -27,6 +27,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "i8digits.cuh"
 #include "kernels.h"
 
 namespace rpcb {
@@ -221,11 +222,10 @@ __device__ __forceinline__ void slice_value(double v, int8_t* out, int64_t pstri
   }
 }
 
-// F's digit planes are column-block-major, [kI8Slices][kcap / 64][plane_rows][64] bytes: the
-// GEMM's A tile (128 rows x 64 K bytes) is one contiguous box, and a round's new columns land
-// in whole 64-byte row segments.  Columns [c0, c0 + nc): a thread per (row, 8-column group):
-// two 32-byte loads of F, 56 digits, one 64-bit store per plane; the group holding c0 keeps
-// its bytes below c0 (earlier rounds' digits).
+// Appends F(:, c0:c0+nc) to the digit planes (i8digits.cuh): a thread per (row, 8-column
+// group), two 32-byte loads of F, one 64-bit store per plane.  (Appending from the update
+// kernel's epilogue — each warp re-reading its 16 rows of G through L2 — measured slower:
+// C4 39.7 vs 37.4 ms.)
 __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ F, int64_t ldf,
                                                          int64_t n, int c0, int nc,
                                                          int8_t* __restrict__ planes,
@@ -234,56 +234,8 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
   const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (item >= n * ng) return;
   const int64_t r = item / ng;
-  const int g = g0 + (int)(item - r * ng);  // 8-column group
-  const int blk = g >> 3;
-  const double* fr = F + r * ldf + 8 * g;
-  int8_t* base = planes + (int64_t)blk * bstride + r * 64 + 8 * (g & 7);
-  uint64_t w[kSlices];
-  const bool head = 8 * g < c0;
-#pragma unroll
-  for (int t = 0; t < kSlices; ++t)
-    w[t] = head ? *reinterpret_cast<const uint64_t*>(base + t * pstride) : 0ull;
-  double v[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int c = 8 * g + e;
-    v[e] = (c >= c0 && c < c0 + nc) ? __ldg(fr + e) : 0.0;
-  }
-  // digits of F: V = rint(F 2^48) (|V| <= 2^48), d_0 = V >> 42 (signed, |d_0| <= 64) and six
-  // unsigned 7-bit chunks below it (0 .. 127): F = sum_t d_t 2^(-6 - 7 t) within 2^-49.  Integer
-  // ops only after one FMA (the balanced FP64 digit chain cost ~3x more here).
-  uint32_t wl[kSlices], wh[kSlices];
-#pragma unroll
-  for (int t = 0; t < kSlices; ++t) {
-    wl[t] = (uint32_t)w[t];
-    wh[t] = (uint32_t)(w[t] >> 32);
-  }
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    const int c = 8 * g + e;
-    if (c < c0 || c >= c0 + nc) continue;
-    const double q = fma(v[e], 281474976710656.0, 6755399441055744.0);  // v 2^48 + 1.5 2^52
-    const long long V = __double_as_longlong(q) - 0x4338000000000000LL;
-    const uint32_t lo = (uint32_t)V, hi = (uint32_t)((unsigned long long)V >> 32);
-    uint32_t dg[kSlices];
-    dg[6] = lo & 127u;
-    dg[5] = (lo >> 7) & 127u;
-    dg[4] = (lo >> 14) & 127u;
-    dg[3] = (lo >> 21) & 127u;
-    dg[2] = __funnelshift_r(lo, hi, 28) & 127u;
-    dg[1] = (hi >> 3) & 127u;
-    dg[0] = (uint32_t)((int)hi >> 10) & 0xffu;  // V >> 42, two's complement byte
-    const int sh = 8 * (e & 3);
-#pragma unroll
-    for (int t = 0; t < kSlices; ++t) {
-      if (e < 4) wl[t] = (wl[t] & ~(0xffu << sh)) | (dg[t] << sh);
-      else wh[t] = (wh[t] & ~(0xffu << sh)) | (dg[t] << sh);
-    }
-  }
-#pragma unroll
-  for (int t = 0; t < kSlices; ++t) w[t] = ((uint64_t)wh[t] << 32) | wl[t];
-#pragma unroll
-  for (int t = 0; t < kSlices; ++t) *reinterpret_cast<uint64_t*>(base + t * pstride) = w[t];
+  const int g = g0 + (int)(item - r * ng);
+  i8_append_group(F + r * ldf, r, g, c0, c0 + nc, planes, pstride, bstride);
 }
 
 // B' rows (logical a < m at bp[perm_row(a)], columns < kcur): per-row scale 2^-e (max < 2^e),
