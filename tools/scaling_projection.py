@@ -5,7 +5,8 @@ processes exactly the rows one GPU of a P-GPU job would (same kernel, same sizes
 per-GPU update time at P is measured here directly (sum over the shards' launches / P; the
 shards are chunk-aligned and equal but for the last).  The replicated per-round chain
 (chunk totals, sampler, H block, sweep, round prep) runs on every GPU at full size: it is
-taken from the P = 1 run.  The exchange per round (chunk-total allgather, record owner
+taken from the P = 1 run.  The update (FP64 fused kernel + tensor-core residual) and the
+digit-plane appends are row-local: their sum over the shards / P is one GPU's share.  The exchange per round (chunk-total allgather, record owner
 reduce, ||G||^2 allgather) is not measurable on one GPU; it is charged at a stated estimate
 per collective (--coll-us, default 15 us: small NCCL collectives over NVLink/NVSwitch).
 
@@ -46,17 +47,19 @@ def main():
     base = None
     for P in (1, 2, 4, 8):
         ctx = api.Context(0, virtual_shards=P)
-        t_fact, t_upd, rounds, piv = [], [], 0, None
+        t_fact, t_upd, t_sl, rounds, piv = [], [], [], 0, None
         for i in range(args.reps + 1):
             r = api.accelerated_rpcholesky_device(xd.data_ptr(), w.n, w.d, w.d, L.RPC_ROW_MAJOR,
                                                   spec, cfg, ctx)
             if i:
                 t_fact.append(r.timing["factorize_ms"])
                 t_upd.append(r.timing["update_ms"])
+                t_sl.append(r.timing["tc_slice_ms"])  # digit-plane appends: per-shard work
             rounds, piv = len(r.proposed), r.pivots.copy()
             r.free()
         ctx.close()
         fact, upd = statistics.median(t_fact), statistics.median(t_upd)
+        upd += statistics.median(t_sl)  # (row-local like the update)
         if base is None:
             base = {"factorize_ms": fact, "update_ms": upd, "chain_ms": fact - upd, "pivots": piv}
         per_gpu_update = upd / P
