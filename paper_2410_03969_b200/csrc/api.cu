@@ -14,6 +14,7 @@
 // and the b proposal records (id, ||x||^2, x, F row).  The sweep and L^{-1}
 // are computed redundantly and bit-identically on every shard.
 #include <atomic>
+#include <memory>
 
 #include "runtime.h"
 
@@ -1469,6 +1470,19 @@ __global__ void draw_column_records_kernel(const double* __restrict__ X, const d
 }  // namespace rpcb_rt
 
 // ---- component entry points --------------------------------------------------
+// Standalone Gaussian Gram columns go to the tensor-core kernel (i8cols.cu) for d <= 32
+// unless RPC_NO_I8COLS is set (the FP64 DMMA columns-only update kernel otherwise).
+static bool use_i8cols(int kind, int64_t d, int64_t n) {
+  return kind == kGaussGram && d <= kI8ColsMaxD && n < ((int64_t)1 << 31) &&
+         !std::getenv("RPC_NO_I8COLS");
+}
+struct I8ColsBufs {
+  DBuf planes, xexp, bplanes, cinfo;
+  I8ColsBufs(rpc_ctx* ctx, int64_t n)
+      : planes(ctx, i8cols_plane_bytes(n)), xexp(ctx, sizeof(int) * n),
+        bplanes(ctx, (size_t)kI8ColsSlices * 128 * 32), cinfo(ctx, sizeof(double) * 384) {}
+};
+
 int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int64_t ldx,
                                 int layout, rpc_kernel_spec kspec, const int64_t* block_sizes,
                                 int n_sizes, uint64_t seed, rpc_throughput_row* rows,
@@ -1504,6 +1518,14 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
     std::vector<int> hpos(256);
     for (int i = 0; i < 256; ++i) hpos[i] = i;
     CK(cudaMemcpyAsync(pos.p, hpos.data(), sizeof(int) * 256, cudaMemcpyHostToDevice, st));
+    // point digit planes for the tensor-core Gram columns: prepared with the points (as the
+    // packed copy and the squared norms), outside the timed blocks
+    std::unique_ptr<I8ColsBufs> i8b;
+    if (kspec.kind != RPC_KERNEL_L1LAPLACE && use_i8cols(kGaussGram, d, n)) {
+      i8b.reset(new I8ColsBufs(ctx, n));
+      launch_i8cols_prep(X.as<double>(), dpad, (int)d, n, i8b->planes.as<int8_t>(),
+                         i8b->xexp.as<int>(), st);
+    }
     int nr = 0;
     for (int i = 0; i < n_sizes; ++i) {
       const int64_t b = block_sizes[i];
@@ -1516,11 +1538,22 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
         auto run = [&]() {
           for (int64_t blk = 0; blk < n_blocks; ++blk) {
             // one oracle.columns(cols) call: b columns, in launches of <= 256
-            for (int64_t c0 = 0; c0 < b; c0 += 256) {
-              const int nc = (int)std::min<int64_t>(256, b - c0);
+            const int64_t step = (i8b && kind == kGaussGram) ? 128 : 256;
+            for (int64_t c0 = 0; c0 < b; c0 += step) {
+              const int nc = (int)std::min<int64_t>(step, b - c0);
               draw_column_records_kernel<<<nc, 64, 0, st>>>(X.as<double>(), sqn.as<double>(), n,
                                                              dpad, seed, (uint64_t)(blk * b + c0),
                                                              lay, prop.as<double>());
+              if (i8b && kind == kGaussGram) {
+                double esc = 0.0;
+                const int kf = kernel_fun(ks, &esc);
+                if (launch_i8cols(i8b->planes.as<int8_t>(), i8b->xexp.as<int>(), sqn.as<double>(),
+                                  n, prop.as<double>(), lay.rec, nc, kf, esc,
+                                  i8b->bplanes.as<int8_t>(), i8b->cinfo.as<double>(),
+                                  outd.as<double>() + (c0 % mb) * n, n, st) < 0)
+                  raise(RPC_ECUDA, "tensor-core kernel-column launch failed");
+                continue;
+              }
               launch_gather_accepted(prop.as<double>(), lay, pos.as<int>(), nc, 256, 0, (int)dpad,
                                      xs.as<double>(), fs.as<double>(), 16, sqnS.as<double>(),
                                      idS.as<double>(), st, nullptr, gram_xscale(kind));
@@ -1596,7 +1629,13 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
                        layout == RPC_ROW_MAJOR, dpad, X.as<double>(), sqn.as<double>(), nullptr,
                        st);
     RecordLayout lay{2 + dpad, 2, 2 + dpad};
-    const int64_t mb = std::min<int64_t>(m, 256);
+    std::unique_ptr<I8ColsBufs> i8b;
+    if (use_i8cols(kind, d, n)) {
+      i8b.reset(new I8ColsBufs(ctx, n));
+      launch_i8cols_prep(X.as<double>(), dpad, (int)d, n, i8b->planes.as<int8_t>(),
+                         i8b->xexp.as<int>(), st);
+    }
+    const int64_t mb = std::min<int64_t>(m, i8b ? 128 : 256);
     DBuf prop(ctx, sizeof(double) * 256 * lay.rec), pos(ctx, sizeof(int) * 256),
         outd(ctx, sizeof(double) * n * std::max<int64_t>(mb, 1)), tile(ctx, sizeof(double) * (n / 64 + 2)),
         xs(ctx, sizeof(double) * 256 * dpad), fs(ctx, sizeof(double) * 256 * 16),
@@ -1650,7 +1689,12 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.cols_out = outd.as<double>();
       up.ld_out = n;
       CK(cudaEventRecord(e0.e, st));
-      const int bm = launch_update(up, st);
+      const int bm =
+          i8b ? launch_i8cols(i8b->planes.as<int8_t>(), i8b->xexp.as<int>(), sqn.as<double>(), n,
+                              prop.as<double>(), lay.rec, (int)nc, up.kfun, up.escale,
+                              i8b->bplanes.as<int8_t>(), i8b->cinfo.as<double>(),
+                              outd.as<double>(), n, st)
+              : launch_update(up, st);
       if (bm < 0) raise(RPC_ECUDA, "kernel-column launch failed (code " + std::to_string(bm) + ")");
       CK(cudaEventRecord(e1.e, st));
       CK(cudaMemcpy2DAsync(out + c0 * ld_out, ld_out * 8, outd.p, n * 8, n * 8, nc,

@@ -181,6 +181,20 @@ int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, 
                        const double* bp, int64_t ldbp, int m, int kcur, int8_t* bplanes,
                        double* cscale, double* C, int64_t ldc, cudaStream_t st);
 
+// ---- K5 standalone, Gaussian Gram, d <= 32: Gram on tcgen05 int8 digit planes (i8cols.cu) ----
+constexpr int kI8ColsMaxD = 32;
+constexpr int kI8ColsSlices = 8;  // digits per point coordinate (i8cols.cu)
+// bytes of the point digit planes ([kI8ColsSlices][round_up(n, 128)][32] int8)
+int64_t i8cols_plane_bytes(int64_t n);
+// planes + per-row exponents (int[n]) of the packed points X [n][dpad]
+void launch_i8cols_prep(const double* X, int64_t dpad, int d, int64_t n, int8_t* planes,
+                        int* xexp, cudaStream_t st);
+// out[c ld_out + r] = k(x_r, x_{id_c}) for c < m <= 128 (ids in the proposal records' slot 0);
+// bplanes: kI8ColsSlices * 128 * 32 bytes, cinfo: 384 doubles (scratch).  0, or < 0 on failure.
+int launch_i8cols(const int8_t* planes, const int* xexp, const double* sqn, int64_t n,
+                  const double* prop, int64_t rec, int m, int kfun, double escale,
+                  int8_t* bplanes, double* cinfo, double* out, int64_t ld_out, cudaStream_t st);
+
 // ---- K5+K6: fused kernel columns + residual GEMM + L^{-T} + diag update ----
 struct UpdateParams {
   const double* X; int64_t dpad; int dchunks;   // X shard [n_loc][dpad]
