@@ -1544,7 +1544,7 @@ int rpc_bench_column_throughput(rpc_ctx* ctx, const double* x, int64_t n, int64_
               draw_column_records_kernel<<<nc, 64, 0, st>>>(X.as<double>(), sqn.as<double>(), n,
                                                              dpad, seed, (uint64_t)(blk * b + c0),
                                                              lay, prop.as<double>());
-              if (i8b && kind == kGaussGram) {
+              if (i8b && kind == kGaussGram && nc >= kI8ColsMinM) {
                 double esc = 0.0;
                 const int kf = kernel_fun(ks, &esc);
                 if (launch_i8cols(i8b->planes.as<int8_t>(), i8b->xexp.as<int>(), sqn.as<double>(),
@@ -1690,7 +1690,7 @@ int rpc_kernel_columns(rpc_ctx* ctx, const double* x, int64_t n, int64_t d, int6
       up.ld_out = n;
       CK(cudaEventRecord(e0.e, st));
       const int bm =
-          i8b ? launch_i8cols(i8b->planes.as<int8_t>(), i8b->xexp.as<int>(), sqn.as<double>(), n,
+          (i8b && nc >= kI8ColsMinM) ? launch_i8cols(i8b->planes.as<int8_t>(), i8b->xexp.as<int>(), sqn.as<double>(), n,
                               prop.as<double>(), lay.rec, (int)nc, up.kfun, up.escale,
                               i8b->bplanes.as<int8_t>(), i8b->cinfo.as<double>(),
                               outd.as<double>(), n, st)

@@ -202,9 +202,9 @@ __global__ void __launch_bounds__(kCThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = 64
-      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
-                             ((uint32_t)(kCBN >> 3) << 17) | ((uint32_t)(kCBM >> 4) << 24);
+      // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = 64 (a partial last
+      // column half: N = its live columns rounded up to 16)
+      const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kCBM >> 4) << 24);
       mbar_wait_sleep(&bfull, 0);
       const uint32_t bb = smem_u32(sb);
       int it = 0, job = 0;
@@ -214,6 +214,8 @@ __global__ void __launch_bounds__(kCThreads, 1)
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
         const uint32_t ba = smem_u32(sm + s * kCAst);
         for (int h = 0; h < ncolt; ++h, ++job) {
+          const int nmma = min(kCBN, (m - h * kCBN + 15) & ~15);
+          const uint32_t idesc = idesc0 | ((uint32_t)(nmma >> 3) << 17);
 #pragma unroll
           for (int d = 0; d < kCS; ++d) {
             if (job > 0) {
@@ -255,6 +257,13 @@ __global__ void __launch_bounds__(kCThreads, 1)
       for (int h = 0; h < ncolt; ++h, ++job) {
         mbar_wait(&done, job & 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const int c0 = h * kCBN + cs * 16;
+        if (c0 >= m) {  // no live column in this warp's slice (warp-uniform): release only
+          __syncwarp();
+          if (lane == 0)
+            for (int d = 0; d < kCS; ++d) mbar_arrive(&drained[d]);
+          continue;
+        }
         // Diagonals read two at a time and released at once; folded as they arrive:
         // P_p = A_{2p} 2^7 + A_{2p+1} (exact int32, |A_d| < (d + 1) 2^17), then
         // sum_d 2^(-7 d) A_d = 2^-49 S,  S = H 2^28 + L,  H = P0 2^14 + P1,  L = P2 2^14 + P3
@@ -297,7 +306,6 @@ __global__ void __launch_bounds__(kCThreads, 1)
             }
           }
         }
-        const int c0 = h * kCBN + cs * 16;
         double* op = orow + (int64_t)c0 * ld_out;  // advanced by one column per element
 #pragma unroll
         for (int j = 0; j < 16; ++j, op += ld_out) {

@@ -184,6 +184,9 @@ int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, 
 // ---- K5 standalone, Gaussian Gram, d <= 32: Gram on tcgen05 int8 digit planes (i8cols.cu) ----
 constexpr int kI8ColsMaxD = 32;
 constexpr int kI8ColsSlices = 8;  // digits per point coordinate (i8cols.cu)
+// launches with fewer columns stay on the FP64 kernel (C4 points: i8 slower at m <= 40,
+// faster from m = 48: 217k vs 167k columns/s)
+constexpr int kI8ColsMinM = 48;
 // bytes of the point digit planes ([kI8ColsSlices][round_up(n, 128)][32] int8)
 int64_t i8cols_plane_bytes(int64_t n);
 // planes + per-row exponents (int[n]) of the packed points X [n][dpad]
