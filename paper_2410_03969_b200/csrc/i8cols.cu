@@ -152,8 +152,9 @@ __global__ void __launch_bounds__(kCThreads, 1)
   unsigned char* sb = sm + kCNst * kCAst;  // resident B planes
   __shared__ uint64_t afull[kCNst], aempty[kCNst], bfull, done, drained[kCS];
   __shared__ uint32_t tmem_base_s;
-  __shared__ double s_sqc[128], s_exp2[64];
-  __shared__ int s_ce[128], s_id[128];
+  // per column: {||x_j||^2, bits (lo: high word of -2^(e_j - 60), hi: pinned row or -1)}
+  __shared__ double2 s_col[128];
+  __shared__ double s_exp2[64];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < kCNst; ++s) {
@@ -168,11 +169,11 @@ __global__ void __launch_bounds__(kCThreads, 1)
     tma_prefetch_desc(&tmB);
   }
   for (int i = threadIdx.x; i < 128; i += blockDim.x) {
-    s_sqc[i] = cinfo[i];
-    // pinned row of column i (-1: none; ids < 2^31 here, n <= rows of one device buffer)
-    s_id[i] = (int)cinfo[128 + i];
-    // high word of -2^(e_j - 60 + 1023 - 1023): the row adds e_i << 20
-    s_ce[i] = (int)(0x80000000u | (uint32_t)(((int)cinfo[256 + i] - 60 + 1023) << 20));
+    // pinned row of column i (-1: none; ids < 2^31 here, n <= rows of one device buffer);
+    // high word of -2^(e_j - 60): the row adds e_i << 20
+    const int id = (int)cinfo[128 + i];
+    const int ce = (int)(0x80000000u | (uint32_t)(((int)cinfo[256 + i] - 60 + 1023) << 20));
+    s_col[i] = make_double2(cinfo[i], __hiloint2double(id, ce));
   }
   if (threadIdx.x < 64) s_exp2[threadIdx.x] = exp2((double)threadIdx.x / 64.0);
   if (warp == 1) {
@@ -306,16 +307,19 @@ __global__ void __launch_bounds__(kCThreads, 1)
             }
           }
         }
+        // warp-uniform: every lane's row and all 16 columns live -> stores without predicates
+        const bool full = (c0 + 16 <= m) && (tile * kCBM + q * 32 + 32 <= n);
         double* op = orow + (int64_t)c0 * ld_out;  // advanced by one column per element
 #pragma unroll
         for (int j = 0; j < 16; ++j, op += ld_out) {
           const int c = c0 + j;
+          const double2 cinf = s_col[c];
           // -2 dot = -2 * 2^(e_i + e_j - 12) * 2^-49 * S = S * (-2^(e_i + e_j - 60)), exact, so
           // fma(S, sc, |x_i|^2) is the reference's ((-2 dot) + |x_i|^2) rounding
-          const double sc = __hiloint2double(s_ce[c] + er, 0);
-          double dd = __dadd_rn(fma(S[j], sc, sqr), s_sqc[c]);
+          const double sc = __hiloint2double(__double2loint(cinf.y) + er, 0);
+          double dd = __dadd_rn(fma(S[j], sc, sqr), cinf.x);
           // clamp at 0 and the same-index pin (oracle.hpp:84-88), integer tests
-          if ((__double2hiint(dd) < 0) | (ri == s_id[c])) dd = 0.0;
+          if ((__double2hiint(dd) < 0) | (ri == __double2hiint(cinf.y))) dd = 0.0;
           double val;
           if constexpr (KF == kFunExp) {
             // exp_tab (update_impl.cuh) inline, the -708 clamp as one FP64 max (same values)
@@ -336,7 +340,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
           } else {
             val = kfun_eval(dd, KF, escale, s_exp2);
           }
-          if (rin && c < m) __stcs(op, val);
+          if (full || (rin && c < m)) __stcs(op, val);
         }
       }
     }
