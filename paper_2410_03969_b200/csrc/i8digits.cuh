@@ -13,8 +13,7 @@ namespace rpcb {
 
 // Digits of F(r, 8 g .. 8 g + 7) for the columns in [c0, c1) into the planes (one 64-bit store
 // per plane); bytes of columns below c0 are kept (earlier rounds'), those from c1 on are
-// don't-care (the next round rewrites them).  frow: F's row r (read through L2: the values
-// may have been written by this kernel).
+// don't-care (the next round rewrites them).  frow: F's row r.
 __device__ __forceinline__ void i8_append_group(const double* frow, int64_t r, int g, int c0,
                                                 int c1, int8_t* planes, int64_t pstride,
                                                 int64_t bstride) {
@@ -27,11 +26,19 @@ __device__ __forceinline__ void i8_append_group(const double* frow, int64_t r, i
     wl[t] = (uint32_t)w;
     wh[t] = (uint32_t)(w >> 32);
   }
+  // the group's 64 bytes of F as two 256-bit loads (F rows are 128-byte aligned and padded to
+  // 16 columns, so the whole group is readable); entries outside [c0, c1) are not used
   double v[8];
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(frow + 8 * g));
+  asm volatile("ld.global.cg.v4.f64 {%0, %1, %2, %3}, [%4];"
+               : "=d"(v[4]), "=d"(v[5]), "=d"(v[6]), "=d"(v[7])
+               : "l"(frow + 8 * g + 4));
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int c = 8 * g + e;
-    v[e] = (c >= c0 && c < c1) ? __ldcg(frow + c) : 0.0;
+    if (!(c >= c0 && c < c1)) v[e] = 0.0;
   }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {

@@ -210,6 +210,186 @@ __global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
 
+// Two-pass variant for 64 < m <= 128: tiles of 128 F rows x all (<= 128) output columns, MMAs
+// with N = m rounded up to 16.  By operand traffic the one-pass kernel above is bound by shared
+// memory (an M = 128, N = 64, K = 32 product reads 4 KB of A and 2 KB of B for 32 cycles of
+// tensor work); N = 128 halves the A reads per output, but seven 128-column accumulators do
+// not fit tensor memory, so a tile makes two passes over K: diagonals 0 .. 3 (10 products; only
+// digit planes 0 .. 3 of either operand are loaded) in four 128-column slots, then diagonals
+// 4 .. 6 (18 products, all planes) in slots 0 .. 2.  Per 128 x 128 x 64-byte block that is
+// 176 KB of TMA writes + 448 KB of operand reads against 168 + 672 KB for two one-pass tiles.
+// The epilogue (8 warps: TMEM lane quadrant x column half) keeps its FP64 sums in registers
+// across the two passes and releases each slot as soon as it is read, as above.
+constexpr int kI8N2 = 128, kI8Bpl2 = kI8N2 * kI8KB;
+constexpr int kI8Stage2 = kSlices * (kI8Apl + kI8Bpl2);
+constexpr int kI8P1 = 4;  // diagonals (and digit planes) of the first pass
+
+__global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
+                                                        const __grid_constant__ CUtensorMap tmB,
+                                                        int a_nblk, int64_t n_rows, int m, int nkb,
+                                                        int64_t ntiles,
+                                                        const double* __restrict__ cscale,
+                                                        double* __restrict__ C, int64_t ldc) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
+  __shared__ uint64_t full[kI8Nst], empty[kI8Nst], done, drained[kI8P1];
+  __shared__ uint32_t tmem_base_s;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nmma = (m + 15) & ~15;  // MMA N: live columns rounded up to 16
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kI8Nst; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&done, 1);
+    for (int d = 0; d < kI8P1; ++d) mbar_init(&drained[d], 8);
+    mbar_fence_init();
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+        smem_u32(&tmem_base_s)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const uint32_t tbase = tmem_base_s;
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;  // stage use counter across tiles and passes
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const int64_t row0 = tile * kI8BM;
+        for (int pass = 0; pass < 2; ++pass) {
+          const int np = pass == 0 ? kI8P1 : kSlices;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % kI8Nst;
+            if (it >= kI8Nst) mbar_wait(&empty[s], ((it / kI8Nst) - 1) & 1);
+            mbar_arrive_expect_tx(&full[s], (uint32_t)np * (kI8Apl + kI8Bpl2));
+            unsigned char* st = sm + s * kI8Stage2;
+            for (int t = 0; t < np; ++t)
+              tma_load_3d(st + t * kI8Apl, &tmA, 0, (int)row0, t * a_nblk + kb, &full[s]);
+            for (int u = 0; u < np; ++u)
+              tma_load_2d(st + kSlices * kI8Apl + u * kI8Bpl2, &tmB, kb * kI8KB, u * kI8N2,
+                          &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = nmma
+      const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nmma >> 3) << 17) |
+                             ((uint32_t)(kI8BM >> 4) << 24);
+      int it = 0;
+      uint32_t uses[kI8P1] = {0, 0, 0, 0};  // completed uses of each accumulator slot
+      for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        for (int pass = 0; pass < 2; ++pass) {
+          const int d0 = pass == 0 ? 0 : kI8P1;
+          for (int kb = 0; kb < nkb; ++kb, ++it) {
+            const int s = it % kI8Nst;
+            mbar_wait(&full[s], (it / kI8Nst) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t ba = smem_u32(sm + s * kI8Stage2), bb = ba + kSlices * kI8Apl;
+#pragma unroll
+            for (int sl = 0; sl < kI8P1; ++sl) {
+              const int d = d0 + sl;
+              if (d >= kSlices) break;
+              if (kb == 0 && uses[sl] > 0) {
+                mbar_wait(&drained[sl], (uses[sl] - 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+              }
+              for (int t = 0; t <= d; ++t)
+#pragma unroll
+                for (int ks = 0; ks < kI8KB / 32; ++ks) {
+                  const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
+                  const uint64_t db = umma_desc_sw64(bb + (d - t) * kI8Bpl2 + ks * 32);
+                  const uint32_t accum = (kb | ks | t) != 0;
+                  asm volatile(
+                      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                          tbase + (uint32_t)(sl * kI8N2)),
+                      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                }
+            }
+            asm volatile(
+                "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&empty[s])));
+          }
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                  smem_u32(&done)));
+#pragma unroll
+          for (int sl = 0; sl < kI8P1; ++sl)
+            if (d0 + sl < kSlices) ++uses[sl];
+        }
+      }
+    }
+  } else {
+    const int q = warp & 3;         // the TMEM lane quadrant this warp may read
+    const int h = (warp - 2) >> 2;  // column half
+    const int nch = min(4, max(0, (nmma - h * 64) >> 4));  // live 16-column chunks of this half
+    uint32_t np = 0;                // passes seen (parity of `done`)
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      const int64_t r = tile * kI8BM + q * 32 + lane;
+      double acc[64];
+#pragma unroll
+      for (int j = 0; j < 64; ++j) acc[j] = 0.0;
+      double wd = 1.0;  // 2^(-7 d)
+#pragma unroll
+      for (int pass = 0; pass < 2; ++pass) {
+        mbar_wait(&done, np & 1);
+        ++np;
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+#pragma unroll
+        for (int sl = 0; sl < (pass == 0 ? kI8P1 : kSlices - kI8P1); ++sl) {
+#pragma unroll
+          for (int cc = 0; cc < 4; ++cc) {
+            if (cc < nch) {
+              uint32_t v[16];
+              const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) +
+                                  (uint32_t)(sl * kI8N2 + h * 64 + cc * 16);
+              asm volatile(
+                  "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, "
+                  "%10, %11, %12, %13, %14, %15}, [%16];\n"
+                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                    "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                    "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                  : "r"(ta));
+              asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                acc[cc * 16 + j] = fma((double)(int)v[j], wd, acc[cc * 16 + j]);
+            }
+          }
+          // this warp's reads of the slot are complete: release its TMEM columns
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&drained[sl]);
+          wd *= 0.0078125;
+        }
+      }
+      if (r < n_rows) {
+        double* cr = C + r * ldc + h * 64;
+#pragma unroll
+        for (int j = 0; j < 64; j += 2) {
+          const int c = h * 64 + j;
+          if (c + 1 < m)
+            *reinterpret_cast<double2*>(cr + j) =
+                make_double2(acc[j] * cscale[c], acc[j + 1] * cscale[c + 1]);
+          else if (c < m)
+            cr[j] = acc[j] * cscale[c];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if (warp == 1)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
+}
+
 // kSlices digits of v * 2^6 (|v| <= 1) in base 2^7, each rounded to nearest (magic-number rint)
 __device__ __forceinline__ void slice_value(double v, int8_t* out, int64_t pstride) {
   constexpr double kM = 6755399441055744.0;  // 1.5 * 2^52
@@ -223,7 +403,7 @@ __device__ __forceinline__ void slice_value(double v, int8_t* out, int64_t pstri
 }
 
 // Appends F(:, c0:c0+nc) to the digit planes (i8digits.cuh): a thread per (row, 8-column
-// group), two 32-byte loads of F, one 64-bit store per plane.  (Appending from the update
+// group), two 256-bit loads of F, one 64-bit store per plane.  (Appending from the update
 // kernel's epilogue — each warp re-reading its 16 rows of G through L2 — measured slower:
 // C4 39.7 vs 37.4 ms.)
 __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restrict__ F, int64_t ldf,
@@ -233,7 +413,9 @@ __global__ void __launch_bounds__(256) slice_cols_kernel(const double* __restric
   const int g0 = c0 >> 3, ng = ((c0 + nc + 7) >> 3) - g0;
   const int64_t item = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (item >= n * ng) return;
-  const int64_t r = item / ng;
+  int64_t r;
+  if (n * ng < (int64_t)1 << 31) r = (int64_t)((uint32_t)item / (uint32_t)ng);
+  else r = item / ng;
   const int g = g0 + (int)(item - r * ng);
   i8_append_group(F + r * ldf, r, g, c0, c0 + nc, planes, pstride, bstride);
 }
@@ -325,12 +507,24 @@ int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, 
   const int mpad = (m + kI8BN - 1) / kI8BN * kI8BN;  // B plane rows (zeros beyond m)
   slice_bprime_kernel<<<mpad, 256, 0, st>>>(bp, ldbp, m, kcur, kpad, bplanes,
                                             (int64_t)mpad * kpad, cscale);
+  // 64 < m <= 128: the two-pass kernel (RPC_I8_ONEPASS keeps the one-pass tiles for comparison)
+  static const bool one_pass = std::getenv("RPC_I8_ONEPASS") != nullptr;
+  const bool two_pass = mpad == kI8N2 && !one_pass;
   CUtensorMap mA, mB;
   if (!i8_map_a(&mA, fplanes, plane_rows, (int64_t)kSlices * (kcap / 64)) ||
-      !i8_map(&mB, bplanes, kpad, (int64_t)kSlices * mpad, kpad, kI8BN))
+      !i8_map(&mB, bplanes, kpad, (int64_t)kSlices * mpad, kpad, two_pass ? kI8N2 : kI8BN))
     return -3;
-  const size_t smem = (size_t)kI8Nst * kI8Stage + 1024;
   const int a_nblk = (int)(kcap / 64), nkb = kpad / kI8KB, ncolt = mpad / kI8BN;
+  if (two_pass) {
+    const size_t smem2 = (size_t)kI8Nst * kI8Stage2 + 1024;
+    const int64_t ntiles2 = (n_rows + kI8BM - 1) / kI8BM;
+    if (ensure_smem_attr((const void*)i8gemm2_kernel, (int)smem2) != cudaSuccess) return -2;
+    const unsigned grid2 = (unsigned)std::min<int64_t>(ntiles2, num_sms());
+    i8gemm2_kernel<<<grid2, 320, smem2, st>>>(mA, mB, a_nblk, n_rows, m, nkb, ntiles2, cscale, C,
+                                              ldc);
+    return 0;
+  }
+  const size_t smem = (size_t)kI8Nst * kI8Stage + 1024;
   const int64_t ntiles = (n_rows + kI8BM - 1) / kI8BM * ncolt;
   if (ensure_smem_attr((const void*)i8gemm_kernel, (int)smem) != cudaSuccess) return -2;
   const unsigned grid = (unsigned)std::min<int64_t>(ntiles, num_sms());
