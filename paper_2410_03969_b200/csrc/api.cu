@@ -249,7 +249,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
   // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 384) and
   // m <= 128 compute F B'^T there; the update kernel then adds it.  Used when the planes fit
   // next to F (7 bytes per factor entry); RPC_NO_I8 forces the FP64 DMMA path.
-  bool i8_ok = !lowmem && algo == kAlgoAccelerated && !grouped && cap > i8_min_k_env() &&
+  bool i8_ok = !lowmem && algo == kAlgoAccelerated && cap > i8_min_k_env() &&
                !(cfg.flags & RPC_FLAG_FP64_RESIDUAL) && std::getenv("RPC_NO_I8") == nullptr;
 
   const int64_t i8_min_k = i8_min_k_env();
@@ -844,24 +844,25 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         upd_flops.push_back(fl);
         bytes += 8.0 * (N * kg + N * mg + N * d + 2.0 * N);
       }
-      }  // groups
-      // this round's columns into F's digit planes (coalesced: a warp per row segment; byte
-      // stores from the update epilogue's fragment layout measured 3-4x slower per round)
-      // (not after the last round: nothing reads its digits)
+      // this group's columns into F's digit planes (coalesced: a warp per row segment; byte
+      // stores from the update epilogue's fragment layout measured 3-4x slower per round): the
+      // next group's (or round's) residual GEMM reads them
+      // (not after the last group of the last round: nothing reads its digits)
       const bool last_round = cfg.mode == RPC_FIXED_ROUNDS ? round + 1 >= cfg.rounds
                                                            : kcur + m >= cfg.target_rank;
-      if (i8_ok && !last_round) {
+      if (i8_ok && !(last_round && g0 + mg >= m)) {
         sl_ev.emplace_back();
         sl_ev.emplace_back();
         CK(cudaEventRecord(sl_ev[sl_ev.size() - 2].e, st));
         for (size_t si = 0; si < res->shards.size(); ++si) {
           Shard& s = res->shards[si];
-          launch_slice_cols(s.F.as<double>(), ldf, s.n_loc, (int)kcur, m,
+          launch_slice_cols(s.F.as<double>(), ldf, s.n_loc, (int)kg, mg,
                             reinterpret_cast<int8_t*>(i8_planes[si].p), i8_rows[si], i8_kcap, st);
           ++launches;
         }
         CK(cudaEventRecord(sl_ev.back().e, st));
       }
+      }  // groups
       pending_g2 = true;
       if (sink.p) {
         const auto hs0 = clk::now();
