@@ -496,8 +496,9 @@ def main():
             tc_ach = tc_ops / (tc_ms * 1e-3) / 1e12
             roof_tc = {"bound": "tensor", "achieved": tc_ach, "peak": i8_peak, "unit": "TOP/s (int8)",
                        "frac": tc_ach / i8_peak if i8_peak else None, "traffic": None,
-                       "kernel": ("i8gemm_kernel (residual GEMM F B'^T from 7 int8 digit planes per "
-                                  "operand, tcgen05.mma kind::i8, int32 TMEM accumulators)"),
+                       "kernel": ("i8gemm2_kernel (residual GEMM F B'^T from 7 int8 digit planes per "
+                                  "operand, tcgen05.mma kind::i8 M=128 N=m, int32 TMEM accumulators, "
+                                  "two passes over K: diagonals 0-3 then 4-6; i8gemm_kernel for m <= 64)"),
                        "peak_source": i8_src,
                        "fp64_equivalent_tflops": tc_fl / (tc_ms * 1e-3) / 1e12,
                        "kernel_ms_per_step": tc_ms,

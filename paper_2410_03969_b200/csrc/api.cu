@@ -801,7 +801,9 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
             up.ldce = kI8MaxCols;
             ++i8_launches;
             launches += 2;
-            const double rows = (double)round_up(s.n_loc, 128), cols = (double)round_up(mg, 64);
+            // products as issued: N = 64 per column half (m <= 64), else m rounded up to 16
+            const double rows = (double)round_up(s.n_loc, 128),
+                         cols = (double)(mg <= 64 ? 64 : round_up(mg, 16));
             tc_ops += 2.0 * (kI8Slices * (kI8Slices + 1) / 2) * rows * cols * (double)round_up(kg, 64);
             tc_fl += 2.0 * (double)s.n_loc * mg * (double)kg;
           }

@@ -497,10 +497,14 @@ def test_update_fused_scan_bitwise_equals_totals_pass(ctx, monkeypatch, n, d, b,
 
 @pytest.mark.parametrize("n,d,b,k,kernel", [(60000, 30, 120, 800, "gaussian"),
                                             (40000, 10, 64, 700, "gaussian"),
-                                            (50000, 20, 100, 650, "laplace")])
+                                            (50000, 20, 100, 650, "laplace"),
+                                            (40000, 24, 200, 900, "laplace"),
+                                            (30000, 12, 300, 800, "gaussian")])
 def test_tensor_core_residual_matches_dmma_and_oracle(ctx, monkeypatch, n, d, b, k, kernel):
     """Rounds past RPC_I8_MIN_K compute F B'^T from int8 digit planes on tcgen05 (i8gemm.cu):
-    same pivots as the FP64 DMMA path and the oracle, factor within the parity bar."""
+    same pivots as the FP64 DMMA path and the oracle, factor within the parity bar.  b > 128:
+    grouped rounds, each group's columns appended to the digit planes before the next group's
+    product (the C5 shape)."""
     x = wl.gen_c1(n, d, 6)
     sigma = math.sqrt(d)
     spec = api.KernelSpec(kernel, sigma)

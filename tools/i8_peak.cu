@@ -53,7 +53,41 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int n, int niter, long lon
   if (MODE == 0) me = threadIdx.x == 0;
   else if (MODE == 1) me = threadIdx.x < 32 && elect_one();
   else me = threadIdx.x < 32;
-  if (me) {
+  if (MODE == 3) {
+    // descriptors change with every product (7 A planes x 7 B planes of 8 KB, the residual
+    // GEMM's diagonal order), issued from an elect.sync region
+    if (threadIdx.x < 32 && elect_one()) {
+      const uint32_t idesc = ((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24));
+      const uint32_t ba = smem_u32(sm), bb = ba + 7 * 8192;
+      const long long t0 = clock64();
+      int cnt = 0;
+      for (int i = 0; cnt < niter; ++i) {
+#pragma unroll
+        for (int d = 0; d < 7; ++d) {
+#pragma unroll
+          for (int t = 0; t <= d; ++t) {
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks) {
+              const uint64_t da = desc_sw64(ba + t * 8192 + ks * 32);
+              const uint64_t db = desc_sw64(bb + (d - t) * 8192 + ks * 32);
+              const uint32_t acc = tbase + (uint32_t)((d & 3) * 128);
+              asm volatile("{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                           "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc),
+                           "l"(da), "l"(db), "r"(idesc), "r"((uint32_t)(i | t | ks)));
+              ++cnt;
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          smem_u32(&bar)));
+      uint32_t ok = 0;
+      while (!ok)
+        asm volatile("{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n"
+                     "selp.u32 %0, 1, 0, p;\n}\n" : "=r"(ok) : "r"(smem_u32(&bar)) : "memory");
+      cyc[blockIdx.x] = (clock64() - t0) * niter / cnt;
+    }
+  } else if (me) {
     const uint32_t idesc = KIND == 0 ? ((2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24))
                                      : ((1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | (8u << 24));
     const uint64_t da = desc_sw64(smem_u32(sm)), db = desc_sw64(smem_u32(sm) + 128 * 64);
@@ -95,7 +129,7 @@ static void run(const char* name, int n, int sms) {
   const int niter = 8192;
   long long* cyc;
   cudaMalloc(&cyc, sizeof(long long) * sms);
-  const size_t smem = (128 + 256) * 64 + 1024;
+  const size_t smem = (MODE == 3 ? 14 * 8192 : (128 + 256) * 64) + 1024;
   cudaFuncSetAttribute(peak_kernel<KIND, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -122,6 +156,7 @@ int main() {
   for (int n : {64, 128, 256}) run<0, 0>("i8", n, sms);
   for (int n : {64, 128, 256}) run<0, 1>("i8", n, sms);
   for (int n : {64, 128, 256}) run<0, 2>("i8", n, sms);
+  for (int n : {64, 96, 112, 128}) run<0, 3>("i8-varying", n, sms);
   for (int n : {64, 128, 256}) run<1, 1>("bf16", n, sms);
   return 0;
 }
