@@ -23,6 +23,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
@@ -224,12 +225,53 @@ constexpr int kI8N2 = 128, kI8Bpl2 = kI8N2 * kI8KB;
 constexpr int kI8Stage2 = kSlices * (kI8Apl + kI8Bpl2);
 constexpr int kI8P1 = 4;  // diagonals (and digit planes) of the first pass
 
+// One lane of the (converged) warp: the single-thread MMA role runs under elect.sync, so the
+// compiler knows one lane is active and keeps descriptors in uniform registers (an
+// `if (lane == 0)` region gets an election loop and broadcast moves around every product).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(p));
+  return p != 0;
+}
+
+// The products of one K block of pass PASS (diagonals 0 .. 3 or 4 .. 6) from the stage at `ba`
+// (a loop-invariant address: every descriptor is that base plus a constant).  Not the first K
+// block of a pass (those products overwrite and wait for the drains).
+template <int PASS>
+__device__ __forceinline__ void i8_issue_kblock(uint32_t ba, uint32_t tbase, uint32_t idesc) {
+  constexpr int d0 = PASS == 0 ? 0 : kI8P1, d1 = PASS == 0 ? kI8P1 : kSlices;
+  const uint32_t bb = ba + kSlices * kI8Apl;
+#pragma unroll
+  for (int d = d0; d < d1; ++d)
+#pragma unroll
+    for (int t = 0; t <= d; ++t)
+#pragma unroll
+      for (int ks = 0; ks < kI8KB / 32; ++ks) {
+        const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
+        const uint64_t db = umma_desc_sw64(bb + (d - t) * kI8Bpl2 + ks * 32);
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                tbase + (uint32_t)((d - d0) * kI8N2)),
+            "l"(da), "l"(db), "r"(idesc), "r"(1u));
+      }
+}
+
 __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__ CUtensorMap tmA,
                                                         const __grid_constant__ CUtensorMap tmB,
                                                         int a_nblk, int64_t n_rows, int m, int nkb,
                                                         int64_t ntiles,
                                                         const double* __restrict__ cscale,
-                                                        double* __restrict__ C, int64_t ldc) {
+                                                        double* __restrict__ C, int64_t ldc,
+                                                        int dbg, long long* trace) {
+  // RPC_I8_DEBUG bit 4: block 0 stamps its first tiles' pass transitions (16 slots per tile)
+#define I8_STAMP(ev)                                                                       \
+  do {                                                                                     \
+    if (trace != nullptr && blockIdx.x == 0 && tile < 8 * (int64_t)gridDim.x)              \
+      trace[(tile / gridDim.x) * 16 + (ev)] = clock64();                                   \
+  } while (0)
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char* sm = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u);
   __shared__ uint64_t full[kI8Nst], empty[kI8Nst], done, drained[kI8P1];
@@ -266,6 +308,10 @@ __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__
           for (int kb = 0; kb < nkb; ++kb, ++it) {
             const int s = it % kI8Nst;
             if (it >= kI8Nst) mbar_wait(&empty[s], ((it / kI8Nst) - 1) & 1);
+            if (dbg & 1) {  // RPC_I8_DEBUG bit 0: no loads (the products read stale stages)
+              mbar_arrive(&full[s]);
+              continue;
+            }
             mbar_arrive_expect_tx(&full[s], (uint32_t)np * (kI8Apl + kI8Bpl2));
             unsigned char* st = sm + s * kI8Stage2;
             for (int t = 0; t < np; ++t)
@@ -278,40 +324,57 @@ __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (elect_one()) {
       // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = nmma
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nmma >> 3) << 17) |
                              ((uint32_t)(kI8BM >> 4) << 24);
+      const uint32_t ba0 = smem_u32(sm), ba1 = ba0 + kI8Stage2;  // the two stages
       int it = 0;
       uint32_t uses[kI8P1] = {0, 0, 0, 0};  // completed uses of each accumulator slot
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         for (int pass = 0; pass < 2; ++pass) {
           const int d0 = pass == 0 ? 0 : kI8P1;
           for (int kb = 0; kb < nkb; ++kb, ++it) {
-            const int s = it % kI8Nst;
-            mbar_wait(&full[s], (it / kI8Nst) & 1);
+            const int s = it & 1;
+            mbar_wait(&full[s], (it >> 1) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t ba = smem_u32(sm + s * kI8Stage2), bb = ba + kSlices * kI8Apl;
-#pragma unroll
-            for (int sl = 0; sl < kI8P1; ++sl) {
-              const int d = d0 + sl;
-              if (d >= kSlices) break;
-              if (kb == 0 && uses[sl] > 0) {
-                mbar_wait(&drained[sl], (uses[sl] - 1) & 1);
-                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (dbg & 2) {  // RPC_I8_DEBUG bit 1: no products (loads + drains only)
+            } else if (kb > 0) {
+              if (pass == 0) {
+                if (s == 0) i8_issue_kblock<0>(ba0, tbase, idesc);
+                else i8_issue_kblock<0>(ba1, tbase, idesc);
+              } else {
+                if (s == 0) i8_issue_kblock<1>(ba0, tbase, idesc);
+                else i8_issue_kblock<1>(ba1, tbase, idesc);
               }
-              for (int t = 0; t <= d; ++t)
+            } else {
+              // first K block of the pass: a slot's first product overwrites it, after the
+              // epilogue has drained its previous use
+              const uint32_t ba = s == 0 ? ba0 : ba1, bb = ba + kSlices * kI8Apl;
 #pragma unroll
-                for (int ks = 0; ks < kI8KB / 32; ++ks) {
-                  const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
-                  const uint64_t db = umma_desc_sw64(bb + (d - t) * kI8Bpl2 + ks * 32);
-                  const uint32_t accum = (kb | ks | t) != 0;
-                  asm volatile(
-                      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
-                          tbase + (uint32_t)(sl * kI8N2)),
-                      "l"(da), "l"(db), "r"(idesc), "r"(accum));
+              for (int sl = 0; sl < kI8P1; ++sl) {
+                const int d = d0 + sl;
+                if (d >= kSlices) break;
+                if (uses[sl] > 0) {
+                  if (sl == 0) I8_STAMP(pass * 4 + 0);
+                  mbar_wait(&drained[sl], (uses[sl] - 1) & 1);
+                  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                  if (sl == 0) I8_STAMP(pass * 4 + 1);
+                  if (sl == 2) I8_STAMP(pass * 4 + 2);
                 }
+                for (int t = 0; t <= d; ++t)
+#pragma unroll
+                  for (int ks = 0; ks < kI8KB / 32; ++ks) {
+                    const uint64_t da = umma_desc_sw64(ba + t * kI8Apl + ks * 32);
+                    const uint64_t db = umma_desc_sw64(bb + (d - t) * kI8Bpl2 + ks * 32);
+                    const uint32_t accum = (ks | t) != 0;
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(
+                            tbase + (uint32_t)(sl * kI8N2)),
+                        "l"(da), "l"(db), "r"(idesc), "r"(accum));
+                  }
+              }
             }
             asm volatile(
                 "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -320,6 +383,7 @@ __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__
           asm volatile(
               "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                   smem_u32(&done)));
+          I8_STAMP(pass * 4 + 3);
 #pragma unroll
           for (int sl = 0; sl < kI8P1; ++sl)
             if (d0 + sl < kSlices) ++uses[sl];
@@ -336,18 +400,25 @@ __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__
       double acc[64];
 #pragma unroll
       for (int j = 0; j < 64; ++j) acc[j] = 0.0;
-      double wd = 1.0;  // 2^(-7 d)
 #pragma unroll
       for (int pass = 0; pass < 2; ++pass) {
         mbar_wait(&done, np & 1);
         ++np;
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (threadIdx.x == 64) I8_STAMP(8 + pass * 3);
+        // slots drained in pairs: P = 128 A_d + A_(d+1) folded exactly in int64 (|A_d| < 2^28) and
+        // converted through the 1.5 2^52 bit pattern: two full-rate FP64 operations per output
+        // and pair instead of two I2F.F64 + two DFMA; both slots are released right after their
+        // last TMEM read, ahead of that chunk's arithmetic
 #pragma unroll
-        for (int sl = 0; sl < (pass == 0 ? kI8P1 : kSlices - kI8P1); ++sl) {
+        for (int sl = 0; sl < (pass == 0 ? kI8P1 : kSlices - kI8P1); sl += 2) {
+          const int d = pass * kI8P1 + sl;
+          const bool pairq = d + 1 < kSlices;
+          const double wd = 1.0 / (double)(1ull << (7 * (pairq ? d + 1 : d)));  // weight of the fold
 #pragma unroll
           for (int cc = 0; cc < 4; ++cc) {
             if (cc < nch) {
-              uint32_t v[16];
+              uint32_t v[16], w[16];
               const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) +
                                   (uint32_t)(sl * kI8N2 + h * 64 + cc * 16);
               asm volatile(
@@ -357,31 +428,70 @@ __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__
                     "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
                     "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
                   : "r"(ta));
+              if (pairq)
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, "
+                    "%9, %10, %11, %12, %13, %14, %15}, [%16];\n"
+                    : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                      "=r"(w[6]), "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]),
+                      "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+                    : "r"(ta + (uint32_t)kI8N2));
               asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+              if (cc == nch - 1) {
+                // this warp's reads of the slots are complete: release their TMEM columns
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) {
+                  mbar_arrive(&drained[sl]);
+                  if (pairq) mbar_arrive(&drained[sl + 1]);
+                }
+                if (threadIdx.x == 64) I8_STAMP(8 + pass * 3 + 1 + (sl >> 1));
+              }
+              if (dbg & 8) {  // RPC_I8_DEBUG bit 3: no conversions
+                acc[cc * 16] += __longlong_as_double((long long)(v[0] ^ v[5] ^ w[10] ^ w[15]));
+                continue;
+              }
 #pragma unroll
-              for (int j = 0; j < 16; ++j)
-                acc[cc * 16 + j] = fma((double)(int)v[j], wd, acc[cc * 16 + j]);
+              for (int j = 0; j < 16; ++j) {
+                double x;
+                if (pairq) {
+                  const long long P = (long long)(int)v[j] * 128 + (long long)(int)w[j];
+                  x = __longlong_as_double(P + 0x4338000000000000LL) - 6755399441055744.0;
+                } else {
+                  x = __hiloint2double(0x43300000, (int)(v[j] ^ 0x80000000u)) - 4503601774854144.0;
+                }
+                acc[cc * 16 + j] = fma(x, wd, acc[cc * 16 + j]);
+              }
             }
           }
-          // this warp's reads of the slot are complete: release its TMEM columns
-          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&drained[sl]);
-          wd *= 0.0078125;
         }
       }
-      if (r < n_rows) {
+      if (dbg & 4) {  // RPC_I8_DEBUG bit 2: no C stores
+        double sacc = 0.0;
+#pragma unroll
+        for (int j = 0; j < 64; ++j) sacc += acc[j];
+        if (sacc == 1.2345e300) C[0] = sacc;
+      } else if (r < n_rows) {
+        // a thread owns 512 contiguous bytes of its row of C: 256-bit stores (whole 32-byte
+        // sectors; 16-byte stores at the 1 KB row stride cost 275 us of a 1.5 ms launch).
+        // Columns from m on are written too (zeros: their cscale is 0, C is 128 columns wide).
         double* cr = C + r * ldc + h * 64;
 #pragma unroll
-        for (int j = 0; j < 64; j += 2) {
-          const int c = h * 64 + j;
-          if (c + 1 < m)
-            *reinterpret_cast<double2*>(cr + j) =
-                make_double2(acc[j] * cscale[c], acc[j + 1] * cscale[c + 1]);
-          else if (c < m)
-            cr[j] = acc[j] * cscale[c];
+        for (int cc = 0; cc < 4; ++cc) {
+          if (cc < nch) {
+#pragma unroll
+            for (int j = cc * 16; j < cc * 16 + 16; j += 4) {
+              const int c = h * 64 + j;
+              const double4 sc4 = *reinterpret_cast<const double4*>(cscale + c);
+              asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(cr + j),
+                           "d"(acc[j] * sc4.x), "d"(acc[j + 1] * sc4.y), "d"(acc[j + 2] * sc4.z),
+                           "d"(acc[j + 3] * sc4.w)
+                           : "memory");
+            }
+          }
         }
       }
+      if (threadIdx.x == 64) I8_STAMP(14);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -389,6 +499,7 @@ __global__ void __launch_bounds__(320, 1) i8gemm2_kernel(const __grid_constant__
   if (warp == 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tbase));
 }
+#undef I8_STAMP
 
 // kSlices digits of v * 2^6 (|v| <= 1) in base 2^7, each rounded to nearest (magic-number rint)
 __device__ __forceinline__ void slice_value(double v, int8_t* out, int64_t pstride) {
@@ -520,8 +631,28 @@ int launch_i8_residual(const int8_t* fplanes, int64_t plane_rows, int64_t kcap, 
     const int64_t ntiles2 = (n_rows + kI8BM - 1) / kI8BM;
     if (ensure_smem_attr((const void*)i8gemm2_kernel, (int)smem2) != cudaSuccess) return -2;
     const unsigned grid2 = (unsigned)std::min<int64_t>(ntiles2, num_sms());
+    // RPC_I8_DEBUG (timing experiments only, wrong results): 1 = no TMA loads, 2 = no products
+    static const int dbg = [] {
+      const char* e = std::getenv("RPC_I8_DEBUG");
+      return e ? std::atoi(e) : 0;
+    }();
+    static long long* trace = nullptr;
+    if ((dbg & 16) && trace == nullptr) {
+      cudaMalloc(&trace, sizeof(long long) * 128);
+      cudaMemset(trace, 0, sizeof(long long) * 128);
+    }
     i8gemm2_kernel<<<grid2, 320, smem2, st>>>(mA, mB, a_nblk, n_rows, m, nkb, ntiles2, cscale, C,
-                                              ldc);
+                                              ldc, dbg, trace);
+    if (dbg & 16) {
+      long long h[128];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, trace, sizeof(h), cudaMemcpyDeviceToHost);
+      for (int t = 0; t < 8; ++t) {
+        std::fprintf(stderr, "[i8 trace] tile %d nkb %d:", t, nkb);
+        for (int e = 0; e < 16; ++e) std::fprintf(stderr, " %lld", h[t * 16 + e] ? h[t * 16 + e] - h[3] : 0);
+        std::fprintf(stderr, "\n");
+      }
+    }
     return 0;
   }
   const size_t smem = (size_t)kI8Nst * kI8Stage + 1024;
