@@ -185,6 +185,17 @@ __device__ __forceinline__ bool mbar_test_wait(uint64_t* bar, uint32_t parity) {
 }
 // The retry loop is plain C++ so the compiler sees the branch and reconverges the
 // warp before any following .aligned instruction (mma.sync, shfl.sync).
+// One lane of the (converged) warp.  Single-thread TMA / MMA roles run under elect.sync so the
+// compiler knows one lane is active and keeps addresses and descriptors in uniform registers
+// (an `if (lane == 0)` region gets an election loop and broadcast moves around every TMA or
+// MMA instruction).
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
+      : "=r"(p));
+  return p != 0;
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(bar, parity)) {
   }

@@ -225,17 +225,6 @@ constexpr int kI8N2 = 128, kI8Bpl2 = kI8N2 * kI8KB;
 constexpr int kI8Stage2 = kSlices * (kI8Apl + kI8Bpl2);
 constexpr int kI8P1 = 4;  // diagonals (and digit planes) of the first pass
 
-// One lane of the (converged) warp: the single-thread MMA role runs under elect.sync, so the
-// compiler knows one lane is active and keeps descriptors in uniform registers (an
-// `if (lane == 0)` region gets an election loop and broadcast moves around every product).
-__device__ __forceinline__ bool elect_one() {
-  uint32_t p;
-  asm volatile(
-      "{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}\n"
-      : "=r"(p));
-  return p != 0;
-}
-
 // The products of one K block of pass PASS (diagonals 0 .. 3 or 4 .. 6) from the stage at `ba`
 // (a loop-invariant address: every descriptor is that base plus a constant).  Not the first K
 // block of a pass (those products overwrite and wait for the drains).
