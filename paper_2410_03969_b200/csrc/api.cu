@@ -30,10 +30,11 @@ __global__ void chol_gather_kernel(const double* __restrict__ F, int64_t ldf, in
 }
 
 // First factor width at which a round's residual GEMM goes to the tensor cores (i8gemm.cu):
-// below it the FP64 DMMA phase of the update is as fast (C4: ~300 columns).
+// below it the FP64 DMMA phase of the update is as fast (C4, two-pass kernel: 33.0 / 32.9 / 33.4 ms
+// at 192 / 256 / 384).
 static int64_t i8_min_k_env() {
   const char* e = std::getenv("RPC_I8_MIN_K");
-  return e ? std::atoll(e) : 384;
+  return e ? std::atoll(e) : 256;
 }
 
 // Launch tags of the fused sweep + prep (its progress word and the host sequence word):
@@ -246,10 +247,13 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       scan_tsum[si] = DBuf(ctx, sizeof(double) * (size_t)std::max<int64_t>(1, 4 * ntiles64));
     }
   // Residual GEMM on the tensor cores (i8gemm.cu): F's int8 digit planes are kept beside F
-  // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 384) and
+  // (each round appends its columns), and rounds with kcur >= RPC_I8_MIN_K (default 256) and
   // m <= 128 compute F B'^T there; the update kernel then adds it.  Used when the planes fit
   // next to F (7 bytes per factor entry); RPC_NO_I8 forces the FP64 DMMA path.
-  bool i8_ok = !lowmem && algo == kAlgoAccelerated && cap > i8_min_k_env() &&
+  // (block_rpcholesky too: same update path, |F| <= 1 holds with the diagonal shift; not
+  // simple_rpcholesky: one column per round)
+  bool i8_ok = !lowmem && (algo == kAlgoAccelerated || algo == kAlgoBlock) &&
+               cap > i8_min_k_env() &&
                !(cfg.flags & RPC_FLAG_FP64_RESIDUAL) && std::getenv("RPC_NO_I8") == nullptr;
 
   const int64_t i8_min_k = i8_min_k_env();
@@ -788,7 +792,8 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
         // (the tensor-core residual GEMM is timed as part of the round's update)
-        if (i8_ok && kg >= i8_min_k && mg <= kI8MaxCols) {
+        // (the int8 product costs as much as 64 columns whatever m is: small groups stay on DMMA)
+        if (i8_ok && kg >= i8_min_k && mg <= kI8MaxCols && mg >= kI8MinCols) {
           const size_t si = &s - res->shards.data();
           tc_ev.emplace_back();
           tc_ev.emplace_back();

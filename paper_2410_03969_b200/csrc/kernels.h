@@ -150,6 +150,7 @@ void launch_linv_dev(const double* lacc_cm, const int* m_dev, int m_max, int nb,
 // ---- residual GEMM on int8 slices (i8gemm.cu) ----------------------------------------
 constexpr int kI8Slices = 7;     // base-2^7 digits per operand (Ozaki scheme I)
 constexpr int kI8MaxCols = 128;  // output columns (accepted pivots) per launch
+constexpr int kI8MinCols = 32;   // fewer accepted pivots: the FP64 DMMA residual is cheaper
 // The digits of v (|v| <= 1): V = rint(v 2^48) split into balanced base-2^7 digits, most
 // significant first, v = sum_t d_t 2^(-6 - 7 t) + e, |d_t| <= 64, |e| <= 2^-49 (one rounding;
 // integer ops only after the first FMA).

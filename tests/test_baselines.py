@@ -146,6 +146,27 @@ def test_gpu_block_vs_oracle(ctx, kw):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("b", [120, 200])
+def test_gpu_block_tensor_core_residual(ctx, monkeypatch, b):
+    """block_rpcholesky's later rounds on the int8 tensor-core residual (i8gemm.cu; b = 200:
+    grouped rounds): same pivots as the FP64 DMMA path and the oracle, factor within TOL."""
+    x = wl.gen_c1(30000, 12, 8)
+    sigma = math.sqrt(12.0)
+    monkeypatch.setenv("RPC_I8_MIN_K", "256")
+    monkeypatch.delenv("RPC_NO_I8", raising=False)
+    g = gpu_run(ctx, "block", x, "gaussian", sigma, 700, b, 9)
+    monkeypatch.setenv("RPC_NO_I8", "1")
+    f = gpu_run(ctx, "block", x, "gaussian", sigma, 700, b, 9)
+    assert np.array_equal(g.pivots, f.pivots)
+    assert rel(g.factor, f.factor) <= TOL
+    assert g.timing["tc_int8_ops"] > 0 and f.timing["tc_int8_ops"] == 0
+    r = po.block_rpcholesky(po.Oracle(x=x, kernel="gaussian", sigma=sigma, n_threads=8),
+                            block_size=b, seed=9, target_rank=700)
+    assert np.array_equal(g.pivots, r.pivots)
+    assert rel(g.factor, r.factor) <= TOL
+
+
+@pytest.mark.gpu
 def test_gpu_simple_exhaustion_and_errors(ctx):
     from paper_2410_03969_b200 import api
     g = gpu_run(ctx, "simple", np.zeros((30, 2)), "gaussian", 1.0, 5, 1, 0)
