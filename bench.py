@@ -526,6 +526,10 @@ def main():
             "roofline_secondary": roof_tc,
             "update_step": {"ms": upd_ms, "fp64_flops": flops,
                             "fp64_equivalent_tflops": flops / (upd_ms * 1e-3) / 1e12 if upd_ms else None,
+                            # the whole update step (int8 residual GEMM + fused FP64 kernel + digit
+                            # appends) against the FP64 DMMA peak the round-1 design was bound by
+                            "frac_of_fp64_peak": (flops / (upd_ms * 1e-3) / 1e12 / peak)
+                            if (upd_ms and peak) else None,
                             "share_of_step": upd_ms / (sec_per_step * 1e3)},
             "cpu_baseline": cpu, "e2e": e2e, "parity": parity,
             "gpu_launches": int(timing["kernel_launches"]) * args.steps,
