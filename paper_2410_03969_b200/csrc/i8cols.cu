@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tbase = tmem_base_s;
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       mbar_arrive_expect_tx(&bfull, kCS * ncolt * kCBN * kCKB);
       for (int u = 0; u < kCS; ++u)
         for (int h = 0; h < ncolt; ++h)
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(kCThreads, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (elect_one()) {
       // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = 64 (a partial last
       // column half: N = its live columns rounded up to 16)
       const uint32_t idesc0 = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(kCBM >> 4) << 24);

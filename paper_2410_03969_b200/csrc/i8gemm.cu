@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ 
   asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
   const uint32_t tbase = tmem_base_s;
   if (warp == 0) {
-    if (lane == 0) {
+    if (elect_one()) {
       int it = 0;  // stage use counter across tiles
       for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
         const int64_t row0 = (tile / ncolt) * kI8BM;
@@ -114,7 +114,7 @@ __global__ void __launch_bounds__(192, 1) i8gemm_kernel(const __grid_constant__ 
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    if (elect_one()) {
       // kind::i8: D s32, A and B signed int8, both K-major, M = 128, N = 64
       const uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) |
                              ((uint32_t)(kI8BN >> 3) << 17) | ((uint32_t)(kI8BM >> 4) << 24);
