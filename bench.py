@@ -486,6 +486,11 @@ def main():
                                 "residual GEMM on FP64 DMMA in the rounds below RPC_I8_MIN_K, "
                                 "added from the tensor-core launch above it)"),
                      "traffic_note": traffic_note,
+                     "note": ("rounds whose residual GEMM runs on the int8 tensor cores leave this "
+                              "kernel the Gram, the kernel-function transform, A L^-T and the "
+                              "epilogue (ncu round 9: DMMA 47 % + FP64 19 % of the shared FP64 "
+                              "pipe, profiles/r02_update_kernel_ncu_r9_s4.txt); the whole update "
+                              "step is in update_step.frac_of_fp64_peak") if tc_ms > 0 else None,
                      "peak_source": peak_src,
                      "per_launch_flops": fp64_flops / max(1, timing["update_launches"]),
                      "kernel_ms_per_step": fp64_ms,
