@@ -396,6 +396,15 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       if (s) cudaStreamSynchronize(s);
     }
   } copy_drain{sink.p ? cst : nullptr};
+  // Digit-plane appends run on a third stream: a round's append is only read by the next
+  // tensor-core product, so it overlaps the next round's chain (scan, sampler, H block, sweep,
+  // prep: single-CTA kernels that leave the GPU idle) instead of preceding it.  RPC_NO_AUX_SLICE
+  // keeps it on the main stream.
+  static const bool aux_slice = std::getenv("RPC_NO_AUX_SLICE") == nullptr;
+  cudaStream_t ast = (i8_ok && aux_slice && ctx->aux_stream) ? ctx->aux_stream : st;
+  Ev ev_upd_done, ev_slice_done;
+  bool slice_pending = false;
+  CopyDrain aux_drain{ast != st ? ast : nullptr};
   const double setup_ms = ms_since(h0);
   const auto h1 = clk::now();
   CK(cudaEventRecord(ev_t0.e, st));
@@ -797,6 +806,10 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           const size_t si = &s - res->shards.data();
           tc_ev.emplace_back();
           tc_ev.emplace_back();
+          if (slice_pending) {  // the planes hold every column below kg
+            CK(cudaStreamWaitEvent(st, ev_slice_done.e, 0));
+            slice_pending = false;
+          }
           CK(cudaEventRecord(tc_ev[tc_ev.size() - 2].e, st));
           if (launch_i8_residual(reinterpret_cast<const int8_t*>(i8_planes[si].p), i8_rows[si],
                                  i8_kcap, s.n_loc, fs.as<double>(), ldf, mg, (int)kg,
@@ -860,14 +873,22 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
       if (i8_ok && !(last_round && g0 + mg >= m)) {
         sl_ev.emplace_back();
         sl_ev.emplace_back();
-        CK(cudaEventRecord(sl_ev[sl_ev.size() - 2].e, st));
+        if (ast != st) {
+          CK(cudaEventRecord(ev_upd_done.e, st));
+          CK(cudaStreamWaitEvent(ast, ev_upd_done.e, 0));
+        }
+        CK(cudaEventRecord(sl_ev[sl_ev.size() - 2].e, ast));
         for (size_t si = 0; si < res->shards.size(); ++si) {
           Shard& s = res->shards[si];
           launch_slice_cols(s.F.as<double>(), ldf, s.n_loc, (int)kg, mg,
-                            reinterpret_cast<int8_t*>(i8_planes[si].p), i8_rows[si], i8_kcap, st);
+                            reinterpret_cast<int8_t*>(i8_planes[si].p), i8_rows[si], i8_kcap, ast);
           ++launches;
         }
-        CK(cudaEventRecord(sl_ev.back().e, st));
+        CK(cudaEventRecord(sl_ev.back().e, ast));
+        if (ast != st) {
+          CK(cudaEventRecord(ev_slice_done.e, ast));
+          slice_pending = true;
+        }
       }
       }  // groups
       pending_g2 = true;
@@ -897,6 +918,7 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
     res->proposed.push_back(std::move(pr));
     res->accepted.push_back(std::move(ac));
   }
+  if (slice_pending) CK(cudaStreamWaitEvent(st, ev_slice_done.e, 0));
   CK(cudaEventRecord(ev_t1.e, st));
   if (sink.p) CK(cudaStreamSynchronize(cst));  // every column is on the host
   const double loop_ms = ms_since(h1);
@@ -1051,8 +1073,13 @@ static int make_ctx(int device, int nvirt, rpc_ctx** out) {
     ctx->device = device;
     ctx->nvirt = nvirt;
     CK(cudaSetDevice(device));
-    CK(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&ctx->copy_stream, cudaStreamNonBlocking));
+    // the main stream outranks the copy and append streams: the round chain's small kernels
+    // are scheduled ahead of the blocks those streams still have queued
+    int prio_least = 0, prio_greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest));
+    CK(cudaStreamCreateWithPriority(&ctx->stream, cudaStreamNonBlocking, prio_greatest));
+    CK(cudaStreamCreateWithPriority(&ctx->copy_stream, cudaStreamNonBlocking, prio_least));
+    CK(cudaStreamCreateWithPriority(&ctx->aux_stream, cudaStreamNonBlocking, prio_least));
   });
   if (rc) {
     g_last_error = ctx->err;
@@ -1127,6 +1154,7 @@ void rpc_destroy(rpc_ctx* ctx) {
   if (ctx->comm) ncclCommDestroy(ctx->comm);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  if (ctx->aux_stream) cudaStreamDestroy(ctx->aux_stream);
   delete ctx;
 }
 
@@ -1454,6 +1482,7 @@ void rpc_result_free(rpc_result* r) {
     std::lock_guard<std::mutex> lk(r->ctx->mu);
     cudaStreamSynchronize(r->ctx->stream);
     cudaStreamSynchronize(r->ctx->copy_stream);
+    if (r->ctx->aux_stream) cudaStreamSynchronize(r->ctx->aux_stream);
     r->shards.clear();  // buffers return to the ctx pool
     r->chol_dev.release();
   }

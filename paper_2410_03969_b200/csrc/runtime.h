@@ -83,6 +83,7 @@ struct rpc_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t copy_stream = nullptr;  // factor streaming to the host (overlaps the rounds)
+  cudaStream_t aux_stream = nullptr;   // digit-plane appends beside the next round's chain
   int world = 1, rank = 0;
   ncclComm_t comm = nullptr;
   bool hostcoll = false;      // collectives through caller-provided host callbacks
@@ -127,6 +128,7 @@ struct rpc_ctx {
   void trim() {
     cudaStreamSynchronize(stream);
     if (copy_stream) cudaStreamSynchronize(copy_stream);
+    if (aux_stream) cudaStreamSynchronize(aux_stream);
     for (auto& kv : pool) cudaFree(kv.second);
     pool.clear();
   }
