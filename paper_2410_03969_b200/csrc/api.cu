@@ -797,19 +797,20 @@ void run_factorization(rpc_ctx* ctx, const double* src, bool src_on_device, int6
           CK(cudaMemsetAsync(phase_clk.p, 0, phase_clk.bytes, st));
           up.phase_clk = phase_clk.as<unsigned long long>();
         }
+        const bool use_i8 = i8_ok && kg >= i8_min_k && mg <= kI8MaxCols && mg >= kI8MinCols;
+        if (use_i8 && slice_pending) {  // the planes must hold every column below kg
+          CK(cudaStreamWaitEvent(st, ev_slice_done.e, 0));  // (ahead of the update's timing events)
+          slice_pending = false;
+        }
         upd_ev.emplace_back();
         upd_ev.emplace_back();
         CK(cudaEventRecord(upd_ev[upd_ev.size() - 2].e, st));
         // (the tensor-core residual GEMM is timed as part of the round's update)
         // (the int8 product costs as much as 64 columns whatever m is: small groups stay on DMMA)
-        if (i8_ok && kg >= i8_min_k && mg <= kI8MaxCols && mg >= kI8MinCols) {
+        if (use_i8) {
           const size_t si = &s - res->shards.data();
           tc_ev.emplace_back();
           tc_ev.emplace_back();
-          if (slice_pending) {  // the planes hold every column below kg
-            CK(cudaStreamWaitEvent(st, ev_slice_done.e, 0));
-            slice_pending = false;
-          }
           CK(cudaEventRecord(tc_ev[tc_ev.size() - 2].e, st));
           if (launch_i8_residual(reinterpret_cast<const int8_t*>(i8_planes[si].p), i8_rows[si],
                                  i8_kcap, s.n_loc, fs.as<double>(), ldf, mg, (int)kg,
