@@ -14,11 +14,15 @@
 // representation error bound the result at ~6e-14 of sum_j |F_ij| |B'_cj| (tools/ozaki_probe.cu:
 // 6.2e-14 measured at the C4 round-9 shape; the FP64 DMMA GEMM it replaces is ~1e-16 of that).
 //
-// Kernel: persistent, tiles of 128 F rows x 64 output columns; kSlices accumulators x 64 TMEM
-// columns (448 of 512).  Warp 0 issues the TMA loads (kSlices + kSlices planes per 64-byte K
-// block, 64-byte swizzle, two stages), warp 1 the MMAs (one thread; tcgen05.commit frees a
-// stage), warps 2-5 the epilogue (tcgen05.ld 32x32b, FP64 sum over the diagonals, column
-// scale), which releases each diagonal to the next tile's MMAs as soon as it has read it.
+// Kernels (both persistent, one CTA per SM; warp 0 issues the TMA loads of 64-byte K blocks with
+// the 64-byte swizzle, one elected thread of warp 1 the MMAs, the other warps drain tensor
+// memory with tcgen05.ld, sum the diagonals in FP64 and apply the column scale, releasing each
+// accumulator to the next MMAs as soon as it is read):
+//   i8gemm_kernel   m <= 64: tiles of 128 rows x 64 columns, kSlices accumulators x 64 TMEM
+//                   columns (448 of 512), two stages;
+//   i8gemm2_kernel  64 < m <= 128: tiles of 128 rows x all columns, N = m rounded up to 16, two
+//                   passes over K (diagonals 0-3, then 4-6) in four 128-column accumulators.
+// DESIGN.md 4.6 has the measurements and the shared-memory-port bound.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
